@@ -1,0 +1,140 @@
+/*
+ * scmoe.h — C ABI of libscmoe.so, the B200 (sm_100a) kernels behind the
+ * ScMoE layer of arXiv 2404.05019.
+ *
+ * Conventions:
+ *  - every pointer is a DEVICE pointer unless stated; every call is
+ *    asynchronous on `stream` (a cudaStream_t passed as void*); no call
+ *    synchronises the host or allocates memory (workspaces are caller-owned);
+ *  - row-major matrices; weights are stored K-major ("transposed"):
+ *    w1t[e] is (d_hidden, d_model), w2t[e] is (d_model, d_hidden), so that
+ *    both tcgen05 operands are K-major 128B-swizzled TMA tiles;
+ *  - return 0 (SCMOE_OK) on success, otherwise an error code with a message
+ *    available from scmoe_last_error() (thread-local).
+ *
+ * Each entry point cites the reference function (file:line, relative to
+ * /root/reference/pkg/src/scmoelab/) whose semantics it reproduces.  The
+ * reference is a numpy library; its "binding" to these entries is the ctypes
+ * layer in paper_2404_05019_b200/_lib.py.
+ */
+#ifndef SCMOE_H_
+#define SCMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCMOE_OK 0
+#define SCMOE_ERR_ARG 1          /* invalid argument (reference: ValueError / ShapeError) */
+#define SCMOE_ERR_CUDA 2         /* CUDA runtime / driver error */
+#define SCMOE_ERR_UNSUPPORTED 3  /* no sm_100 device or unsupported shape */
+
+#define SCMOE_F32 0
+#define SCMOE_BF16 1
+
+/* combine modes, arch.py:380-392 (COMBINE_MODES arch.py:27) */
+#define SCMOE_COMBINE_DIRECT_ADD 0
+#define SCMOE_COMBINE_CG1 1
+#define SCMOE_COMBINE_CG2 2
+
+/* GEMM epilogues of expert_forward, arch.py:349-351 */
+#define SCMOE_EPI_BIAS 0
+#define SCMOE_EPI_BIAS_GELU 1
+
+#define SCMOE_MAX_EXPERTS 64
+#define SCMOE_MAX_K 8
+
+int scmoe_version(void);
+const char* scmoe_last_error(void);
+/* 0 when device `device` is an sm_100 part this library can run on. */
+int scmoe_device_check(int device);
+
+/*
+ * K1 / K1b — gate + top-k + capacity slots in one pass.
+ * Replaces gating.gate_logits (gating.py:93-107) / arch._gate_logits_node
+ * (arch.py:405-415), gating.topk_indices + select_topk (gating.py:110-131),
+ * gating.expert_quota + apply_capacity (gating.py:134-156) and the
+ * count / mean-probability half of load_balance_loss (gating.py:159-170).
+ *
+ *   logits[t,e]  = x[t,:] . w_gate[:,e]  (+ eps[t,e]*softplus(x[t,:].w_noise[:,e]))  fp32
+ *   indices[t,j] = j-th largest logit, ties -> lowest expert index (strict >)
+ *   weights[t,j] = softmax over the k selected logits (top-1: exactly 1.0)
+ *   slots[t,j]   = #earlier selections of the same expert in token-major order
+ *   dropped[t,j] = slots[t,j] >= quota   (quota = ceil(cf*T*k/N), host-computed)
+ *   counts[e]    = pre-drop selections of expert e   (int32, overwritten)
+ *   prob_sum[e]  = sum_t softmax(logits[t,:])[e]     (fp32, overwritten)
+ * w_gate_t / w_noise_t are (N, d) fp32 (transposed gate weights); w_noise_t
+ * and eps are NULL when noise is disabled.  x is (T, d) with row stride
+ * ld_x elements, dtype SCMOE_F32 or SCMOE_BF16.  N <= 64, 1 <= k <= min(N, 8).
+ */
+size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts);
+int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
+                    const float* w_gate_t, const float* w_noise_t, const float* eps,
+                    int n_tokens, int d_model, int n_experts, int k, int quota,
+                    float* logits, int32_t* indices, float* weights, int32_t* slots,
+                    uint8_t* dropped, int32_t* counts, float* prob_sum,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * K2 — dispatch ("encode"): copy each kept selection's row
+ * of x_src into the capacity-slotted buffer
+ *   dispatch_buf[(e * capacity + slots[t,j]) * d_model + :] = x[t,:]
+ * for slots[t,j] < capacity.  Rows past an expert's fill are left untouched.
+ * The reference never permutes (it evaluates experts densely,
+ * arch.py:418-433); this is the sparse equivalent.
+ */
+int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens, int d_model,
+                   int k, const int32_t* indices, const int32_t* slots, int capacity,
+                   void* dispatch_buf, void* stream);
+
+/*
+ * K3 / K4 / K8 — one grouped GEMM of expert_forward (arch.py:349-351):
+ *   out[g, r, :] = epi( a[g, r, :] . wt[g % n_wgroups, :, :]^T + bias[g % n_wgroups, :] )
+ * for r < rows(g), rows(g) = min(group_rows[g], rows_clip) (group_rows NULL:
+ * rows(g) = group_cap).  a is (num_groups, group_cap, k_in), wt is
+ * (n_wgroups, n_out, k_in), bias (n_wgroups, n_out) fp32 or NULL, out is
+ * (num_groups, group_cap, n_out); epi = bias (+ exact-erf GELU).
+ * SCMOE_BF16 runs the tcgen05/TMEM/TMA kernel (fp32 accumulate);
+ * SCMOE_F32 runs the fp32 FFMA parity kernel.
+ */
+int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias, void* out,
+                       int num_groups, int n_wgroups, int group_cap,
+                       const int32_t* group_rows, int rows_clip,
+                       int n_out, int k_in, int epilogue, void* stream);
+
+/*
+ * Full expert_forward (arch.py:349-351) over groups: GEMM1 (bias+GELU) into
+ * `hidden` (num_groups, group_cap, d_hidden), then GEMM2 (bias) into `out`.
+ * The dense shared expert / Block-MLP is num_groups = n_wgroups = 1,
+ * group_rows = NULL, group_cap = T.
+ */
+int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const float* b1,
+                     const void* w2t, const float* b2, void* hidden, void* out,
+                     int num_groups, int n_wgroups, int group_cap,
+                     const int32_t* group_rows, int rows_clip,
+                     int d_model, int d_hidden, void* stream);
+
+/*
+ * K5 — combine ("decode") + combination gate + optional residual:
+ *   routed[t] = sum_j (slots[t,j] < capacity) * weights[t,j] * expert_out[indices[t,j], slots[t,j], :]
+ *   direct_add: f = se + routed; cg1: f = sigmoid(x_cur.w_cg[0]) * se + routed;
+ *   cg2: c = softmax(x_cur.w_cg^T); f = c0 * se + c1 * routed
+ *   out[t] = f (+ residual[t] when residual != NULL)
+ * (arch.py:380-392 combine, arch.py:481-483 weights*keep, arch.py:616
+ * residual add).  w_cg is (1|2, d) fp32; x_cur only read for CG modes;
+ * se_out NULL means "no shared expert" (moe_standard, arch.py:489-493).
+ */
+int scmoe_combine(const void* se_out, const void* expert_out, const void* x_cur,
+                  const float* w_cg, int mode, const void* residual,
+                  const int32_t* indices, const int32_t* slots, const float* weights,
+                  int capacity, int n_tokens, int d_model, int k, int dtype,
+                  void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCMOE_H_ */

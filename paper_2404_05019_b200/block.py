@@ -1,0 +1,283 @@
+"""The ScMoE block pair (Block-MLP + Block-MoE) with scheduler-driven issue.
+
+Wiring follows arch.model_forward's pair loop (arch.py:580-631):
+
+    h_mh_prev  = h_in      + Attn_prev(feed(h_in))
+    h_mlp_prev = h_mh_prev + MLP_prev(feed(h_mh_prev))
+    h_mh_cur   = h_mlp_prev + Attn_cur(feed(h_mlp_prev))
+    x_cur      = feed(h_mh_cur)                    (feed = LN iff pre_layernorm)
+    out        = h_mh_cur + combine(SE(x_cur), routed(src), x_cur)
+    src        = {pos1: h_mlp_prev, pos2: h_mh_prev, pos3: h_in}[pos]
+
+The ops are issued in the order of the reference's shortcut-overlap DAG
+(distsim.py:330-387): backbone pre-ops, gate + encode (dispatch kernel), the
+window ops with the routed expert at the slot sched.choose_slot picks from
+measured CUDA-event costs, then decode (combine kernel, fused with the
+residual add).  Under expert parallelism the two all-to-alls run on a side
+stream and overlap the window ops; `timeline.Recorder` captures every op on
+its stream so the overlap fraction and exposed communication are measured on
+the device.
+
+Attention is the backbone, not the hot path: projections use the same
+tcgen05 GEMM (bias-free), the core is torch SDPA.  `n_heads=1, seq_len=None,
+causal=False` reproduces the reference's single-head unmasked attention over
+all T rows with 1/sqrt(d_model) scaling (arch.py:354-358).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, Optional
+
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from . import ep as ep_mod
+from . import kernels as K
+from . import sched
+from .layers import (CapacityConfig, ConfigError, MoEReplay, ScMoELayer, SharedExpert,
+                     Top2MoELayer, _as_tensor, _normal_)
+from .timeline import Recorder
+
+VARIANTS = ("scmoe", "shared", "standard")
+POSITIONS = ("pos1", "pos2", "pos3")
+
+
+def layer_norm(x: torch.Tensor) -> torch.Tensor:
+    """Parameter-free row LayerNorm, eps 1e-6 (arch.py:361-377)."""
+    return F.layer_norm(x.float(), (x.shape[-1],), eps=1e-6).to(x.dtype)
+
+
+class Attention(nn.Module):
+    """Multi-head SDPA with bias-free projections W_q, W_k, W_v, W_o (d x d)."""
+
+    def __init__(self, d_model: int, n_heads: int = 1, seq_len: Optional[int] = None,
+                 causal: bool = False, dtype=torch.bfloat16, device=None, generator=None):
+        super().__init__()
+        if d_model % n_heads:
+            raise ConfigError("d_model must be divisible by n_heads")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.d_model, self.n_heads, self.seq_len, self.causal = d_model, n_heads, seq_len, causal
+        self.w_qkv_t = nn.Parameter(torch.empty(3 * d_model, d_model, device=dev, dtype=dtype), requires_grad=False)
+        self.w_o_t = nn.Parameter(torch.empty(d_model, d_model, device=dev, dtype=dtype), requires_grad=False)
+        _normal_(self.w_qkv_t, 1.0 / math.sqrt(d_model), generator)
+        _normal_(self.w_o_t, 1.0 / math.sqrt(d_model), generator)
+
+    def load_reference(self, a) -> "Attention":
+        import numpy as np
+        d = self.d_model
+        dev, dt = self.w_qkv_t.device, self.w_qkv_t.dtype
+        with torch.no_grad():
+            for i, w in enumerate((a.w_q, a.w_k, a.w_v)):
+                self.w_qkv_t[i * d:(i + 1) * d].copy_(_as_tensor(np.asarray(w).T, dev, dt))
+            self.w_o_t.copy_(_as_tensor(np.asarray(a.w_o).T, dev, dt))
+        return self
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        t, d = x.shape
+        h = self.n_heads
+        s = self.seq_len or t
+        if t % s:
+            raise ValueError(f"{t} tokens do not split into sequences of {s}")
+        b, hd = t // s, d // h
+        qkv = K.grouped_gemm(x, self.w_qkv_t, None)                        # (T, 3d)
+        q, k, v = qkv.view(b, s, 3, h, hd).permute(2, 0, 3, 1, 4).unbind(0)  # (B, H, S, hd)
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal,
+                                           scale=1.0 / math.sqrt(d) if h == 1 else None)
+        o = o.permute(0, 2, 1, 3).reshape(t, d).contiguous()
+        return K.grouped_gemm(o, self.w_o_t, None)
+
+
+class ScMoEBlockPair(nn.Module):
+    """Block-MLP followed by a Block-MoE (ScMoE / shared-expert / top-k)."""
+
+    def __init__(self, d_model: int, d_hidden: int, n_experts: int, variant: str = "scmoe",
+                 shortcut_pos: Optional[str] = "pos2", k_routed: int = 1,
+                 combine_mode: str = "direct_add", capacity_factor: float = 2.0,
+                 noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
+                 seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
+                 device=None, generator=None, ep_group=None):
+        super().__init__()
+        if variant not in VARIANTS:
+            raise ConfigError(f"unknown variant {variant!r}")
+        if variant == "scmoe" and shortcut_pos not in POSITIONS:
+            raise ConfigError(f"variant 'scmoe' needs shortcut_pos in {POSITIONS}")
+        if variant != "scmoe":
+            shortcut_pos = None
+        if variant == "standard" and combine_mode != "direct_add":
+            raise ConfigError("variant 'standard' has no shared/routed combination")
+        self.variant, self.shortcut_pos = variant, shortcut_pos
+        self.pre_layernorm = pre_layernorm
+        self.dtype = dtype
+        kw = dict(dtype=dtype, device=device, generator=generator)
+        self.attn_prev = Attention(d_model, n_heads, seq_len, causal, **kw)
+        self.mlp_prev = SharedExpert(d_model, d_hidden, **kw)
+        self.attn_cur = Attention(d_model, n_heads, seq_len, causal, **kw)
+        if variant == "standard":
+            self.moe = Top2MoELayer(d_model, d_hidden, n_experts, k_routed=k_routed,
+                                    capacity_factor=capacity_factor, noise_enabled=noise_enabled,
+                                    ep_group=ep_group, **kw)
+        else:
+            self.moe = ScMoELayer(d_model, d_hidden, n_experts, k_routed=k_routed,
+                                  combine_mode=combine_mode, capacity_factor=capacity_factor,
+                                  noise_enabled=noise_enabled, ep_group=ep_group, **kw)
+        self.ep_group = ep_group
+        self.slot: Optional[int] = None
+        self.last_costs: Optional[sched.CostVector] = None
+        self._comm_stream: Optional[torch.cuda.Stream] = None
+
+    # -- construction from the reference's parameter tree --------------------
+    @classmethod
+    def from_reference(cls, cfg, prev_blk, cur_blk, dtype=torch.bfloat16, device=None,
+                       n_heads: int = 1, seq_len=None, causal=False, ep_group=None):
+        """cfg: reference ModelConfig; prev_blk/cur_blk: BlockParams of one pair."""
+        import numpy as np
+        m = cls(cfg.d_model, cfg.d_hidden, cfg.n_experts, variant=cfg.variant,
+                shortcut_pos=cfg.shortcut_pos, k_routed=cfg.k_routed,
+                combine_mode=cfg.combine_mode, capacity_factor=cfg.capacity_factor,
+                noise_enabled=cfg.noise_enabled, pre_layernorm=cfg.pre_layernorm,
+                n_heads=n_heads, seq_len=seq_len, causal=causal, dtype=dtype, device=device,
+                ep_group=ep_group)
+        m.attn_prev.load_reference(prev_blk.attn)
+        m.mlp_prev.load_reference(prev_blk.feed)
+        m.attn_cur.load_reference(cur_blk.attn)
+        cap = CapacityConfig(cfg.capacity_factor)
+        layer = cur_blk.feed
+        if cfg.variant == "standard":
+            ref = Top2MoELayer.from_reference(layer, cap, k=cfg.k_routed, dtype=dtype,
+                                              device=device, ep_group=ep_group)
+        else:
+            ref = ScMoELayer.from_reference(layer, cap, dtype=dtype, device=device,
+                                            ep_group=ep_group)
+        m.moe = ref
+        return m
+
+    def _feed(self, h):
+        return layer_norm(h) if self.pre_layernorm else h
+
+    def comm_stream(self) -> torch.cuda.Stream:
+        if self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(priority=-1)
+        return self._comm_stream
+
+    def order(self):
+        if self.variant == "scmoe":
+            return sched.issue_order(self.shortcut_pos, self.slot if self.slot is not None else 0)
+        o = sched.sequential_order()
+        if self.variant == "standard":
+            o.remove("shared")
+        return o
+
+    # -- forward -------------------------------------------------------------
+    def forward(self, h_in: torch.Tensor, eps=None, replay: Optional[MoEReplay] = None,
+                recorder: Optional[Recorder] = None, return_taps: bool = False):
+        """Returns (out, decision, aux[, taps])."""
+        moe = self.moe
+        rec = recorder or Recorder(enabled=False)
+        st = torch.cuda.current_stream()
+        use_ep = self.ep_group is not None
+        cs = self.comm_stream() if use_ep else None
+        env: Dict[str, object] = {}
+        rec.begin(st)
+
+        def attn_prev():
+            env["h_mh_prev"] = h_in + self.attn_prev(self._feed(h_in))
+
+        def mlp_prev():
+            h = env["h_mh_prev"]
+            env["h_mlp_prev"] = h + self.mlp_prev(self._feed(h))
+
+        def attn_cur():
+            h = env["h_mlp_prev"]
+            hc = h + self.attn_cur(self._feed(h))
+            env["h_mh_cur"] = hc
+            env["x_cur"] = self._feed(hc)
+
+        def src():
+            if self.variant == "scmoe":
+                return env[{"pos1": "h_mlp_prev", "pos2": "h_mh_prev", "pos3": "h_in"}[self.shortcut_pos]]
+            return env["x_cur"]
+
+        env["h_in"] = h_in
+
+        def gate():
+            env["dec"] = moe.route(src(), eps=eps, replay=replay)
+
+        def encode():
+            dec = env["dec"]
+            buf = K.dispatch(src(), dec.indices, dec.slots, moe.n_experts, dec.capacity)
+            env["buf"] = buf
+            if use_ep:
+                cs.wait_stream(st)    # the span starts once the buffer is ready
+                with rec.op("dispatch", "comm", cs):
+                    env["pending"] = ep_mod.dispatch_exchange(buf, dec.kept_counts(), dec.capacity,
+                                                              self.ep_group, cs)
+
+        def expert():
+            dec = env["dec"]
+            if use_ep:
+                p = env["pending"]
+                st.wait_event(p.event)
+                y = moe.experts(p.recv, p.recv_counts, p.capacity)
+                cs.wait_stream(st)
+                with rec.op("combine", "comm", cs):
+                    env["y"], env["y_ev"] = ep_mod.combine_exchange(y, self.ep_group, cs)
+            else:
+                rows = dec.counts if dec.capacity == dec.quota else dec.kept_counts()
+                env["y"] = moe.experts(env["buf"], rows, dec.capacity)
+
+        def shared():
+            env["se"] = moe.shared(env["x_cur"])
+
+        def decode():
+            dec = env["dec"]
+            if use_ep:
+                st.wait_event(env["y_ev"])
+            if self.variant == "standard":
+                env["out"] = K.combine(env["y"], dec.indices, dec.slots, dec.weights, dec.capacity,
+                                       residual=env["h_mh_cur"])
+            else:
+                env["out"] = K.combine(env["y"], dec.indices, dec.slots, dec.weights, dec.capacity,
+                                       se_out=env["se"], mode=moe.combine_mode, x_cur=env["x_cur"],
+                                       w_cg=moe.w_cg, residual=env["h_mh_cur"])
+
+        ops = dict(attn_prev=attn_prev, mlp_prev=mlp_prev, attn_cur=attn_cur, gate=gate,
+                   encode=encode, expert=expert, shared=shared, decode=decode)
+        for name in self.order():
+            with rec.op(name, "compute", st):
+                ops[name]()
+        dec = env["dec"]
+        res = (env["out"], dec, dec.aux_loss())
+        if return_taps:
+            taps = {k: env[k] for k in ("h_mh_prev", "h_mlp_prev", "h_mh_cur", "x_cur")}
+            taps["src"] = src()
+            return res + (taps,)
+        return res
+
+    # -- adaptive scheduling ---------------------------------------------------
+    def calibrate(self, h_in: torch.Tensor, repeats: int = 3) -> sched.ScheduleChoice:
+        """Measure window-op, expert and all-to-all durations with CUDA events
+        and pick the expert slot (Eq. 10) — the paper's adaptive operator
+        scheduling, on real device timings."""
+        if self.variant != "scmoe":
+            raise ConfigError("only the ScMoE variant has an overlap window")
+        durs: Dict[str, float] = {}
+        for _ in range(repeats):
+            rec = Recorder()
+            self.forward(h_in, recorder=rec)
+            for k, v in rec.durations().items():
+                durs[k] = min(durs.get(k, float("inf")), v)
+        window = list(sched.WINDOW_OPS[self.shortcut_pos])
+        comm_d = durs.get("dispatch", 0.0)
+        comm_c = durs.get("combine", 0.0)
+        expert_ms = durs.get("expert", 0.0)
+        if self.ep_group is not None:
+            # the compute-stream "expert" span includes waiting on the
+            # dispatch; the exchange itself is timed on the comm stream
+            expert_ms = max(0.0, expert_ms - comm_d)
+        cv = sched.CostVector([durs.get(n, 0.0) for n in window], comm_d, comm_c, expert_ms)
+        choice = sched.choose_slot(cv)
+        self.slot = choice.slot
+        self.last_costs = cv
+        return choice

@@ -1,0 +1,114 @@
+// Shared helpers for the sm_100a ScMoE kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/scmoe.h"
+
+namespace scmoe {
+
+// Records a message for scmoe_last_error(); defined in capi.cu.
+void set_error(const char* fmt, ...);
+
+#define SCMOE_CHECK_ARG(cond, ...)            \
+  do {                                        \
+    if (!(cond)) {                            \
+      ::scmoe::set_error(__VA_ARGS__);        \
+      return SCMOE_ERR_ARG;                   \
+    }                                         \
+  } while (0)
+
+#define SCMOE_CUDA_TRY(expr)                                                   \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::scmoe::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                         __FILE__, __LINE__);                                  \
+      return SCMOE_ERR_CUDA;                                                   \
+    }                                                                          \
+  } while (0)
+
+#define SCMOE_LAUNCH_CHECK()                                                   \
+  do {                                                                         \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::scmoe::set_error("kernel launch failed: %s (%s:%d)",                  \
+                         cudaGetErrorString(_e), __FILE__, __LINE__);          \
+      return SCMOE_ERR_CUDA;                                                   \
+    }                                                                          \
+  } while (0)
+
+int num_sms();
+
+// ---- element access ---------------------------------------------------------
+
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// 16-byte vector of T: 8 x bf16 or 4 x f32.
+template <typename T> struct Vec16;
+template <> struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  uint4 raw;
+  __device__ __forceinline__ void to_float(float* f) const {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 p = __bfloat1622float2(h[i]);
+      f[2 * i] = p.x;
+      f[2 * i + 1] = p.y;
+    }
+  }
+  __device__ __forceinline__ void from_float(const float* f) {
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  }
+};
+template <> struct Vec16<float> {
+  static constexpr int N = 4;
+  uint4 raw;
+  __device__ __forceinline__ void to_float(float* f) const {
+    const float* s = reinterpret_cast<const float*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = s[i];
+  }
+  __device__ __forceinline__ void from_float(const float* f) {
+    float* s = reinterpret_cast<float*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = f[i];
+  }
+};
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  return *reinterpret_cast<const uint4*>(p);
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// Exact (erf) GELU, the reference's numkit.gelu (numkit.py:96-99).
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace scmoe

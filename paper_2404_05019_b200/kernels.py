@@ -1,0 +1,156 @@
+"""Torch-tensor wrappers over the C ABI (one function per libscmoe entry).
+
+All tensors must be contiguous CUDA tensors on an sm_100 device; every call is
+asynchronous on the current stream (or `stream`).  Shapes follow
+include/scmoe.h.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import check, dtype_code, ensure_device, lib, ptr, stream_ptr
+
+
+def _c(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def expert_quota(capacity_factor: float, n_tokens: int, k: int, n_experts: int) -> int:
+    """int(ceil(cf * T * k / N)) in float64, as gating.expert_quota
+    (gating.py:134-135)."""
+    return int(math.ceil(capacity_factor * n_tokens * k / n_experts))
+
+
+@dataclass
+class GateOut:
+    logits: torch.Tensor    # (T, N) fp32
+    indices: torch.Tensor   # (T, k) int32
+    weights: torch.Tensor   # (T, k) fp32
+    slots: torch.Tensor     # (T, k) int32
+    dropped: torch.Tensor   # (T, k) uint8
+    counts: torch.Tensor    # (N,) int32, pre-drop
+    prob_sum: torch.Tensor  # (N,) fp32, sum_t softmax(logits)[t]
+    quota: int
+
+
+def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
+              w_noise_t: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
+              stream=None) -> GateOut:
+    """K1/K1b: logits, top-k, masked-softmax weights and capacity slots."""
+    ensure_device(x)
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("x must be a row-major (T, d) matrix")
+    T, d = x.shape
+    N = w_gate_t.shape[0]
+    if w_gate_t.shape != (N, d) or w_gate_t.dtype != torch.float32:
+        raise ValueError(f"w_gate_t must be fp32 ({N}, {d})")
+    dev = x.device
+    logits = torch.empty(T, N, device=dev, dtype=torch.float32)
+    indices = torch.empty(T, k, device=dev, dtype=torch.int32)
+    weights = torch.empty(T, k, device=dev, dtype=torch.float32)
+    slots = torch.empty(T, k, device=dev, dtype=torch.int32)
+    dropped = torch.empty(T, k, device=dev, dtype=torch.uint8)
+    counts = torch.empty(N, device=dev, dtype=torch.int32)
+    prob_sum = torch.empty(N, device=dev, dtype=torch.float32)
+    ws_bytes = lib().scmoe_gate_workspace_bytes(T, N)
+    ws = torch.empty(ws_bytes, device=dev, dtype=torch.uint8)
+    if eps is not None:
+        eps = _c(eps.to(torch.float32), "eps")
+    check(lib().scmoe_gate_topk(
+        ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")),
+        ptr(w_noise_t), ptr(eps), T, d, N, k, quota,
+        ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
+        ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
+    return GateOut(logits, indices, weights, slots, dropped, counts, prob_sum, quota)
+
+
+def dispatch(x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor, n_experts: int,
+             capacity: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """K2: capacity-slotted buffer (n_experts, capacity, d)."""
+    ensure_device(x)
+    T, d = x.shape
+    k = indices.shape[1]
+    if out is None:
+        out = torch.empty(n_experts, capacity, d, device=x.device, dtype=x.dtype)
+    check(lib().scmoe_dispatch(ptr(x), dtype_code(x.dtype), x.stride(0), T, d, k,
+                               ptr(_c(indices, "indices")), ptr(_c(slots, "slots")), capacity,
+                               ptr(out), stream_ptr(stream)))
+    return out
+
+
+def grouped_gemm(a: torch.Tensor, wt: torch.Tensor, bias: Optional[torch.Tensor],
+                 group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
+                 gelu: bool = False, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out[g] = epi(a[g] @ wt[g % W]^T + bias[g % W]) on rows < rows(g).
+
+    a: (G, C, K) or (C, K); wt: (W, N, K) or (N, K); bias fp32 (W, N)/(N,).
+    """
+    ensure_device(a)
+    a3 = a if a.dim() == 3 else a.unsqueeze(0)
+    w3 = wt if wt.dim() == 3 else wt.unsqueeze(0)
+    G, C, K = a3.shape
+    W, N, K2 = w3.shape
+    if K2 != K:
+        raise ValueError(f"inner dims differ: {K} vs {K2}")
+    if a.dtype != wt.dtype:
+        raise ValueError("a and wt must share a dtype")
+    if out is None:
+        out = torch.empty(G, C, N, device=a.device, dtype=a.dtype)
+    if bias is not None and bias.dtype != torch.float32:
+        raise ValueError("bias must be fp32")
+    check(lib().scmoe_grouped_gemm(
+        ptr(_c(a3, "a")), dtype_code(a.dtype), ptr(_c(w3, "wt")), ptr(bias), ptr(out), G, W, C,
+        ptr(group_rows), rows_clip, N, K, _lib.EPI_BIAS_GELU if gelu else _lib.EPI_BIAS,
+        stream_ptr(stream)))
+    return out if a.dim() == 3 else out.squeeze(0)
+
+
+def expert_ffn(x: torch.Tensor, w1t: torch.Tensor, b1: torch.Tensor, w2t: torch.Tensor,
+               b2: torch.Tensor, group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
+               hidden: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+    """expert_forward (arch.py:349-351) for every group: gelu(x W1 + b1) W2 + b2."""
+    ensure_device(x)
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    w13 = w1t if w1t.dim() == 3 else w1t.unsqueeze(0)
+    w23 = w2t if w2t.dim() == 3 else w2t.unsqueeze(0)
+    G, C, d = x3.shape
+    W, h, _ = w13.shape
+    if hidden is None:
+        hidden = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
+    if out is None:
+        out = torch.empty(G, C, d, device=x.device, dtype=x.dtype)
+    check(lib().scmoe_expert_ffn(
+        ptr(_c(x3, "x")), dtype_code(x.dtype), ptr(_c(w13, "w1t")), ptr(b1), ptr(_c(w23, "w2t")),
+        ptr(b2), ptr(hidden), ptr(out), G, W, C, ptr(group_rows), rows_clip, d, h,
+        stream_ptr(stream)))
+    return out if x.dim() == 3 else out.view(C, d)
+
+
+def combine(expert_out: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor,
+            weights: torch.Tensor, capacity: int, se_out: Optional[torch.Tensor] = None,
+            mode: str = "direct_add", x_cur: Optional[torch.Tensor] = None,
+            w_cg: Optional[torch.Tensor] = None, residual: Optional[torch.Tensor] = None,
+            out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """K5: routed gather-sum + combination gate + optional residual."""
+    ensure_device(expert_out)
+    for name, t in (("se_out", se_out), ("x_cur", x_cur), ("residual", residual), ("w_cg", w_cg)):
+        if t is not None:
+            _c(t, name)
+    T, k = indices.shape
+    d = expert_out.shape[-1]
+    if out is None:
+        out = torch.empty(T, d, device=expert_out.device, dtype=expert_out.dtype)
+    check(lib().scmoe_combine(
+        ptr(se_out), ptr(_c(expert_out, "expert_out")), ptr(x_cur), ptr(w_cg),
+        _lib.COMBINE_MODES[mode], ptr(residual), ptr(indices), ptr(slots), ptr(weights),
+        capacity, T, d, k, dtype_code(expert_out.dtype), ptr(out), stream_ptr(stream)))
+    return out

@@ -1,0 +1,469 @@
+"""Torch modules of the ScMoE layer (arXiv 2404.05019) on the sm_100a kernels.
+
+API mirror of the reference (`/root/reference/pkg/src/scmoelab/`):
+
+  reference                               here
+  --------------------------------------  -----------------------------------------
+  gating.CapacityConfig  (gating.py:39)   CapacityConfig
+  gating.GateDecision    (gating.py:51)   GateDecision (+ slots, counts, prob_sum)
+  gating.GateParams + gate_logits /       Top1Gate(d_model, n_experts, k=1,
+   select_topk / apply_capacity             noise_enabled=False) — one kernel (K1)
+   (gating.py:20-156)
+  arch.expert_forward    (arch.py:349)    SharedExpert(d_model, d_hidden) (K4)
+  arch.combine           (arch.py:380)    fused into the combine kernel (K5)
+  arch.moe_shared        (arch.py:496)    ScMoELayer(...).forward(x_cur, routed_src)
+  arch.moe_standard k=2  (arch.py:489)    Top2MoELayer(...).forward(x)
+  arch.MoEReplay         (arch.py:315)    MoEReplay (pinned indices / drops / eps)
+
+Constructor arguments are the reference's ModelConfig / dataclass fields
+(d_model, d_hidden, n_experts, k_routed, combine_mode, capacity_factor,
+noise_enabled); `forward` returns (out, decision, aux) like moe_shared /
+moe_standard.  Everything runs on the GPU through libscmoe (no CPU fallback).
+Weights are stored K-major (w1t = W1^T, w2t = W2^T) for the tcgen05 tiles.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+from torch import nn
+
+from . import kernels as K
+from ._lib import MAX_EXPERTS, MAX_K
+
+COMBINE_MODES = ("direct_add", "cg1", "cg2")
+
+
+class ConfigError(ValueError):
+    """Mirror of arch.ConfigError (arch.py:31-32)."""
+
+
+@dataclass
+class CapacityConfig:
+    """gating.CapacityConfig (gating.py:39-48)."""
+    capacity_factor: float = 2.0
+    policy: str = "drop-overflow"
+
+    def __post_init__(self):
+        if self.capacity_factor <= 0:
+            raise ValueError("capacity_factor must be > 0")
+        if self.policy != "drop-overflow":
+            raise ValueError(f"unknown capacity policy {self.policy!r}")
+
+
+@dataclass
+class MoEReplay:
+    """arch.MoEReplay (arch.py:315-322): pinned noise draws and routing."""
+    eps: Optional[object] = None
+    indices: Optional[object] = None
+    dropped: Optional[object] = None
+
+
+@dataclass
+class GateDecision:
+    """gating.GateDecision (gating.py:51-90) as device tensors, plus the
+    capacity slot of every selection and the per-expert statistics the
+    balance loss needs."""
+    logits: torch.Tensor              # (T, N) fp32
+    indices: torch.Tensor             # (T, k) int32, rank order = logit order
+    weights: torch.Tensor             # (T, k) fp32 masked-softmax weights
+    dropped: torch.Tensor             # (T, k) bool
+    slots: torch.Tensor               # (T, k) int32 capacity slot
+    counts: torch.Tensor              # (N,) int32 pre-drop selections
+    prob_sum: torch.Tensor            # (N,) fp32 sum of full-softmax probs
+    quota: int                        # ceil(cf*T*k/N)
+    capacity: int                     # rows per expert in the dispatch buffer
+    eps: Optional[torch.Tensor] = None
+
+    @property
+    def n_tokens(self) -> int:
+        return self.logits.shape[0]
+
+    @property
+    def n_experts(self) -> int:
+        return self.logits.shape[1]
+
+    @property
+    def k(self) -> int:
+        return self.indices.shape[1]
+
+    def support_mask(self) -> torch.Tensor:
+        m = torch.zeros_like(self.logits, dtype=torch.bool)
+        m.scatter_(1, self.indices.long(), True)
+        return m
+
+    def keep_mask(self) -> torch.Tensor:
+        m = torch.zeros_like(self.logits)
+        m.scatter_(1, self.indices.long(), (~self.dropped).to(m.dtype))
+        return m
+
+    def kept_counts(self) -> torch.Tensor:
+        """Rows each expert holds in the dispatch buffer."""
+        if self.capacity == self.quota:
+            return torch.clamp(self.counts, max=self.quota)
+        keep = (~self.dropped).reshape(-1).to(torch.float32)
+        return torch.bincount(self.indices.reshape(-1).long(), weights=keep,
+                              minlength=self.n_experts).to(torch.int32)
+
+    def aux_loss(self) -> torch.Tensor:
+        """N * sum_i f_i P_i (arch.py:436-439 / gating.py:159-170)."""
+        t, n, k = self.n_tokens, self.n_experts, self.k
+        f = self.counts.to(torch.float32) / float(t * k)
+        p = self.prob_sum / float(t)
+        return n * (f * p).sum()
+
+    def to_numpy(self) -> dict:
+        return dict(logits=self.logits.double().cpu().numpy(),
+                    indices=self.indices.long().cpu().numpy(),
+                    weights=self.weights.double().cpu().numpy(),
+                    dropped=self.dropped.cpu().numpy().astype(bool),
+                    slots=self.slots.long().cpu().numpy(),
+                    eps=None if self.eps is None else self.eps.double().cpu().numpy())
+
+
+def _as_tensor(a, device, dtype):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype)
+    return torch.as_tensor(np.asarray(a), device=device, dtype=dtype)
+
+
+def _normal_(t: torch.Tensor, scale: float, generator: Optional[torch.Generator]):
+    with torch.no_grad():
+        tmp = torch.randn(t.shape, generator=generator, dtype=torch.float32, device=t.device)
+        t.copy_(tmp * scale)
+    return t
+
+
+# ---------------------------------------------------------------------------
+# gate
+
+
+class Top1Gate(nn.Module):
+    """Top-k softmax gate (k=1 for ScMoE) with capacity slots: GateParams +
+    gate_logits + select_topk + apply_capacity (gating.py:20-156) as one
+    kernel pass.  w_gate is stored transposed (N, d) in fp32."""
+
+    def __init__(self, d_model: int, n_experts: int, k: int = 1, noise_enabled: bool = False,
+                 capacity_factor: float = 2.0, device=None, generator=None):
+        super().__init__()
+        if not 1 <= n_experts <= MAX_EXPERTS:
+            raise ConfigError(f"n_experts={n_experts} out of [1, {MAX_EXPERTS}]")
+        if not 1 <= k <= min(n_experts, MAX_K):
+            raise ValueError(f"k={k} out of range for N={n_experts}")
+        self.d_model, self.n_experts, self.k = d_model, n_experts, k
+        self.noise_enabled = noise_enabled
+        self.capacity = CapacityConfig(capacity_factor)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.w_gate_t = nn.Parameter(torch.empty(n_experts, d_model, device=dev), requires_grad=False)
+        self.w_noise_t = nn.Parameter(torch.empty(n_experts, d_model, device=dev), requires_grad=False)
+        self.reset_parameters(generator)
+
+    def reset_parameters(self, generator=None):
+        s = 1.0 / math.sqrt(self.d_model)     # init_params scale (arch.py:169)
+        _normal_(self.w_gate_t, s, generator)
+        _normal_(self.w_noise_t, s, generator)
+
+    def quota(self, n_tokens: int) -> int:
+        return K.expert_quota(self.capacity.capacity_factor, n_tokens, self.k, self.n_experts)
+
+    def forward(self, x_src: torch.Tensor, eps: Optional[torch.Tensor] = None,
+                generator: Optional[torch.Generator] = None, replay: Optional[MoEReplay] = None,
+                stream=None) -> GateDecision:
+        t = x_src.shape[0]
+        if t == 0:
+            raise ValueError("empty token batch")
+        if x_src.shape[1] != self.d_model:
+            raise ValueError(f"x has width {x_src.shape[1]}, expected {self.d_model}")
+        if replay is not None and replay.eps is not None:
+            eps = _as_tensor(replay.eps, x_src.device, torch.float32)
+        if self.noise_enabled and eps is None:
+            eps = torch.randn(t, self.n_experts, device=x_src.device, generator=generator)
+        quota = self.quota(t)
+        g = K.gate_topk(x_src, self.w_gate_t, self.k, quota,
+                        w_noise_t=self.w_noise_t if self.noise_enabled else None,
+                        eps=eps if self.noise_enabled else None, stream=stream)
+        dec = GateDecision(g.logits, g.indices, g.weights, g.dropped.bool(), g.slots, g.counts,
+                           g.prob_sum, quota, quota, eps if self.noise_enabled else None)
+        if replay is not None and replay.indices is not None:
+            dec = _pin_routing(dec, replay)
+        return dec
+
+
+def _pin_routing(dec: GateDecision, replay: MoEReplay) -> GateDecision:
+    """Replay pinned indices / drop flags (arch.py:395-402, 474-477): weights
+    are the masked softmax of the live logits over the pinned support; kept
+    selections get consecutive slots per expert in token-major order.  This is
+    a debugging / gradient-check hook, not the throughput path (it syncs once
+    to size the dispatch buffer)."""
+    dev = dec.logits.device
+    idx = _as_tensor(replay.indices, dev, torch.int64)
+    t, k = idx.shape
+    if replay.dropped is None:
+        drop = torch.zeros(t, k, dtype=torch.bool, device=dev)
+    else:
+        drop = _as_tensor(replay.dropped, dev, torch.bool)
+    sel = dec.logits.gather(1, idx)
+    w = torch.softmax(sel, dim=1)
+    n = dec.n_experts
+    flat = idx.reshape(-1)
+    keep = (~drop).reshape(-1)
+    onehot = torch.nn.functional.one_hot(flat, n).to(torch.int32) * keep[:, None].to(torch.int32)
+    before = torch.cumsum(onehot, dim=0) - onehot
+    slots = before.gather(1, flat[:, None]).reshape(t, k).to(torch.int32)
+    kept = onehot.sum(dim=0)
+    cap = max(int(kept.max().item()) if kept.numel() else 1, 1)
+    slots = torch.where(drop, torch.full_like(slots, cap), slots)
+    counts = torch.bincount(flat, minlength=n).to(torch.int32)
+    return GateDecision(dec.logits, idx.to(torch.int32), w.float(), drop, slots, counts,
+                        dec.prob_sum, dec.quota, cap, dec.eps)
+
+
+# ---------------------------------------------------------------------------
+# experts
+
+
+class SharedExpert(nn.Module):
+    """expert_forward (arch.py:349-351) as a dense FFN: gelu(x W1 + b1) W2 + b2.
+    Used for the shared expert (x_cur) and for Block-MLP."""
+
+    def __init__(self, d_model: int, d_hidden: int, dtype=torch.bfloat16, device=None,
+                 generator=None):
+        super().__init__()
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.d_model, self.d_hidden = d_model, d_hidden
+        self.w1t = nn.Parameter(torch.empty(d_hidden, d_model, device=dev, dtype=dtype), requires_grad=False)
+        self.b1 = nn.Parameter(torch.zeros(d_hidden, device=dev), requires_grad=False)
+        self.w2t = nn.Parameter(torch.empty(d_model, d_hidden, device=dev, dtype=dtype), requires_grad=False)
+        self.b2 = nn.Parameter(torch.zeros(d_model, device=dev), requires_grad=False)
+        self.reset_parameters(generator)
+
+    def reset_parameters(self, generator=None):
+        s = 1.0 / math.sqrt(self.d_model)     # both W1 and W2 use 1/sqrt(d) (arch.py:158-164)
+        _normal_(self.w1t, s, generator)
+        _normal_(self.w2t, s, generator)
+        with torch.no_grad():
+            self.b1.zero_()
+            self.b2.zero_()
+
+    def load_reference(self, e) -> "SharedExpert":
+        """Copy an ExpertParams (w1 (d,h), b1 (1,h), w2 (h,d), b2 (1,d))."""
+        dev = self.w1t.device
+        with torch.no_grad():
+            self.w1t.copy_(_as_tensor(np.asarray(e.w1).T, dev, self.w1t.dtype))
+            self.b1.copy_(_as_tensor(np.asarray(e.b1).reshape(-1), dev, torch.float32))
+            self.w2t.copy_(_as_tensor(np.asarray(e.w2).T, dev, self.w2t.dtype))
+            self.b2.copy_(_as_tensor(np.asarray(e.b2).reshape(-1), dev, torch.float32))
+        return self
+
+    def forward(self, x: torch.Tensor, hidden: Optional[torch.Tensor] = None,
+                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if x.dtype != self.w1t.dtype:
+            raise ValueError(f"input dtype {x.dtype} != expert dtype {self.w1t.dtype}")
+        return K.expert_ffn(x, self.w1t, self.b1, self.w2t, self.b2, hidden=hidden, out=out,
+                            stream=stream)
+
+
+class RoutedExperts(nn.Module):
+    """N stacked experts (E, h, d) / (E, d, h), evaluated only on the rows
+    routed to them (the sparse equivalent of _routed_sum, arch.py:418-433)."""
+
+    def __init__(self, n_experts: int, d_model: int, d_hidden: int, dtype=torch.bfloat16,
+                 device=None, generator=None):
+        super().__init__()
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.n_experts, self.d_model, self.d_hidden = n_experts, d_model, d_hidden
+        self.w1t = nn.Parameter(torch.empty(n_experts, d_hidden, d_model, device=dev, dtype=dtype), requires_grad=False)
+        self.b1 = nn.Parameter(torch.zeros(n_experts, d_hidden, device=dev), requires_grad=False)
+        self.w2t = nn.Parameter(torch.empty(n_experts, d_model, d_hidden, device=dev, dtype=dtype), requires_grad=False)
+        self.b2 = nn.Parameter(torch.zeros(n_experts, d_model, device=dev), requires_grad=False)
+        self.reset_parameters(generator)
+
+    def reset_parameters(self, generator=None):
+        s = 1.0 / math.sqrt(self.d_model)
+        _normal_(self.w1t, s, generator)
+        _normal_(self.w2t, s, generator)
+        with torch.no_grad():
+            self.b1.zero_()
+            self.b2.zero_()
+
+    def load_reference(self, experts) -> "RoutedExperts":
+        dev = self.w1t.device
+        with torch.no_grad():
+            for i, e in enumerate(experts):
+                self.w1t[i].copy_(_as_tensor(np.asarray(e.w1).T, dev, self.w1t.dtype))
+                self.b1[i].copy_(_as_tensor(np.asarray(e.b1).reshape(-1), dev, torch.float32))
+                self.w2t[i].copy_(_as_tensor(np.asarray(e.w2).T, dev, self.w2t.dtype))
+                self.b2[i].copy_(_as_tensor(np.asarray(e.b2).reshape(-1), dev, torch.float32))
+        return self
+
+    def forward(self, buf: torch.Tensor, group_rows: torch.Tensor, rows_clip: int,
+                hidden: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+        """buf (G, C, d) with G a multiple of n_experts (EP receive buffers
+        are (ranks * local experts)); group g uses expert g % n_experts."""
+        return K.expert_ffn(buf, self.w1t, self.b1, self.w2t, self.b2, group_rows=group_rows,
+                            rows_clip=rows_clip, hidden=hidden, out=out, stream=stream)
+
+
+# ---------------------------------------------------------------------------
+# layers
+
+
+class _RoutedMoE(nn.Module):
+    """Shared machinery of routed_moe (arch.py:463-486): gate -> dispatch ->
+    grouped expert FFN -> (combine in the subclass).  With `ep_group` set the
+    experts are sharded over the group's ranks and the dispatch / combine
+    buffers travel through all-to-all (paper_2404_05019_b200.ep)."""
+
+    def __init__(self, d_model, d_hidden, n_experts, k_routed, capacity_factor, noise_enabled,
+                 dtype, device, generator, ep_group):
+        super().__init__()
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ConfigError(f"dtype must be bf16 or fp32, got {dtype}")
+        self.d_model, self.d_hidden, self.n_experts = d_model, d_hidden, n_experts
+        self.k_routed, self.dtype = k_routed, dtype
+        self.capacity = CapacityConfig(capacity_factor)
+        self.gate = Top1Gate(d_model, n_experts, k=k_routed, noise_enabled=noise_enabled,
+                             capacity_factor=capacity_factor, device=device, generator=generator)
+        self.ep_group = ep_group
+        ws = 1
+        if ep_group is not None:
+            import torch.distributed as dist
+            ws = dist.get_world_size(ep_group)
+            if n_experts % ws:
+                raise ConfigError(f"n_experts={n_experts} not divisible by EP size {ws}")
+        self.ep_size = ws
+        self.experts = RoutedExperts(n_experts // ws, d_model, d_hidden, dtype, device, generator)
+
+    @property
+    def noise_enabled(self):
+        return self.gate.noise_enabled
+
+    def ep_rank(self) -> int:
+        if self.ep_group is None:
+            return 0
+        import torch.distributed as dist
+        return dist.get_rank(self.ep_group)
+
+    def _load_reference_common(self, layer):
+        dev = self.gate.w_gate_t.device
+        with torch.no_grad():
+            self.gate.w_gate_t.copy_(_as_tensor(np.asarray(layer.gate.w_gate).T, dev, torch.float32))
+            self.gate.w_noise_t.copy_(_as_tensor(np.asarray(layer.gate.w_noise).T, dev, torch.float32))
+        el = self.experts.n_experts
+        r = self.ep_rank()
+        self.experts.load_reference(list(layer.experts)[r * el:(r + 1) * el])
+
+    def route(self, x_src, eps=None, replay=None, generator=None, stream=None) -> GateDecision:
+        return self.gate(x_src, eps=eps, generator=generator, replay=replay, stream=stream)
+
+    def routed_experts(self, x_src: torch.Tensor, dec: GateDecision, stream=None) -> torch.Tensor:
+        """dispatch + expert FFN (+ EP exchange); returns the (N, C, d) expert
+        output buffer that combine gathers from."""
+        buf = K.dispatch(x_src, dec.indices, dec.slots, self.n_experts, dec.capacity, stream=stream)
+        if self.ep_group is None:
+            # rows(g) = min(pre-drop count, capacity) is computed in the kernel
+            rows = dec.counts if dec.capacity == dec.quota else dec.kept_counts()
+            return self.experts(buf, rows, dec.capacity, stream=stream)
+        from . import ep
+        return ep.expert_parallel_ffn(self.experts, buf, dec, self.ep_group)
+
+
+class ScMoELayer(_RoutedMoE):
+    """The shortcut-connected MoE layer: combine(SE(x_cur), routed(src), x_cur)
+    — arch.moe_shared (arch.py:496-504).  `routed_src` is the preceding-layer
+    representation chosen by the shortcut position (pos1 h_mlp_prev, pos2
+    h_mh_prev, pos3 h_in; arch.py:593-597); None means x_cur (the plain
+    shared-expert MoE)."""
+
+    def __init__(self, d_model: int, d_hidden: int, n_experts: int, k_routed: int = 1,
+                 combine_mode: str = "direct_add", capacity_factor: float = 2.0,
+                 noise_enabled: bool = False, dtype=torch.bfloat16, device=None,
+                 generator: Optional[torch.Generator] = None, ep_group=None):
+        super().__init__(d_model, d_hidden, n_experts, k_routed, capacity_factor, noise_enabled,
+                         dtype, device, generator, ep_group)
+        if combine_mode not in COMBINE_MODES:
+            raise ConfigError(f"unknown combine mode {combine_mode!r}")
+        self.combine_mode = combine_mode
+        self.shared = SharedExpert(d_model, d_hidden, dtype, device, generator)
+        dev = self.gate.w_gate_t.device
+        rows = {"direct_add": 0, "cg1": 1, "cg2": 2}[combine_mode]
+        if rows:
+            self.w_cg = nn.Parameter(torch.empty(rows, d_model, device=dev), requires_grad=False)
+            _normal_(self.w_cg, 1.0 / math.sqrt(d_model), generator)
+        else:
+            self.w_cg = None
+
+    @classmethod
+    def from_reference(cls, layer, capacity=None, dtype=torch.bfloat16, device=None, ep_group=None):
+        """Build from a reference arch.MoELayer (+ gating.CapacityConfig)."""
+        d, n = np.asarray(layer.gate.w_gate).shape
+        h = np.asarray(layer.shared.w1).shape[1]
+        mode = getattr(getattr(layer, "combine", None), "mode", None) or getattr(layer, "combine_mode", "direct_add")
+        cf = capacity.capacity_factor if capacity is not None else 2.0
+        m = cls(d, h, n, k_routed=layer.gate.k, combine_mode=mode, capacity_factor=cf,
+                noise_enabled=bool(layer.gate.noise_enabled), dtype=dtype, device=device,
+                ep_group=ep_group)
+        m._load_reference_common(layer)
+        m.shared.load_reference(layer.shared)
+        w_cg = getattr(getattr(layer, "combine", None), "w_cg", None)
+        if w_cg is None:
+            w_cg = getattr(layer, "w_cg", None)
+        if m.w_cg is not None:
+            with torch.no_grad():
+                m.w_cg.copy_(_as_tensor(np.asarray(w_cg), m.w_cg.device, torch.float32))
+        return m
+
+    def forward(self, x_cur: torch.Tensor, routed_src: Optional[torch.Tensor] = None,
+                residual: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
+                replay: Optional[MoEReplay] = None, generator=None):
+        """(out, decision, aux): out = combine(SE(x_cur), routed(src), x_cur)
+        (+ residual when given, fusing the block's `h_mh_cur + feed_out`)."""
+        src = x_cur if routed_src is None else routed_src
+        if src.shape != x_cur.shape:
+            raise ValueError("routed_src and x_cur must have the same shape")
+        dec = self.route(src, eps=eps, replay=replay, generator=generator)
+        y = self.routed_experts(src, dec)
+        se = self.shared(x_cur)
+        out = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, se_out=se,
+                        mode=self.combine_mode, x_cur=x_cur, w_cg=self.w_cg, residual=residual)
+        return out, dec, dec.aux_loss()
+
+
+class Top2MoELayer(_RoutedMoE):
+    """Standard top-k MoE baseline (k=2): arch.moe_standard (arch.py:489-493)
+    — routed mixture on x, no shared expert, 2-way renormalised weights,
+    token-major capacity, dropped selections zeroed without renormalising."""
+
+    def __init__(self, d_model: int, d_hidden: int, n_experts: int, k_routed: int = 2,
+                 capacity_factor: float = 2.0, noise_enabled: bool = False,
+                 dtype=torch.bfloat16, device=None, generator: Optional[torch.Generator] = None,
+                 ep_group=None):
+        super().__init__(d_model, d_hidden, n_experts, k_routed, capacity_factor, noise_enabled,
+                         dtype, device, generator, ep_group)
+
+    @classmethod
+    def from_reference(cls, layer, capacity=None, k=None, dtype=torch.bfloat16, device=None,
+                       ep_group=None):
+        d, n = np.asarray(layer.gate.w_gate).shape
+        h = np.asarray(layer.experts[0].w1).shape[1]
+        cf = capacity.capacity_factor if capacity is not None else 2.0
+        m = cls(d, h, n, k_routed=k or layer.gate.k, capacity_factor=cf,
+                noise_enabled=bool(layer.gate.noise_enabled), dtype=dtype, device=device,
+                ep_group=ep_group)
+        m._load_reference_common(layer)
+        return m
+
+    def forward(self, x: torch.Tensor, residual: Optional[torch.Tensor] = None,
+                eps: Optional[torch.Tensor] = None, replay: Optional[MoEReplay] = None,
+                generator=None):
+        dec = self.route(x, eps=eps, replay=replay, generator=generator)
+        y = self.routed_experts(x, dec)
+        out = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, residual=residual)
+        return out, dec, dec.aux_loss()

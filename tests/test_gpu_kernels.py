@@ -1,0 +1,208 @@
+"""Kernel-level parity on the B200, through the C ABI.
+
+Gate: bit-exact expert index, capacity slot and drop flag against the
+oracle's select_topk + apply_capacity (gating.py:110-156) run on the
+kernel's own fp32 logits upcast to float64 (ties -> lowest index, signed
+zeros, T not a multiple of the tile).  GEMM / dispatch / combine: against
+torch fp32/fp64 references of the same op (tolerances stated per test).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import scmoe_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+K = None
+
+
+def setup_module(module):
+    global K
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_05019_b200 import kernels
+    K = kernels
+
+
+def _gate_case(T, d, N, k, cf, dtype, seed, ties=False, zeros=False, noise=False):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(T, d, device="cuda", generator=g).to(dtype)
+    w = torch.randn(N, d, device="cuda", generator=g) / d ** 0.5
+    if ties and N >= 3:
+        w[N - 1] = w[0]          # identical columns -> bit-identical logits
+        w[1] = w[N - 2]
+    if zeros:
+        x[::3] = 0               # all-zero logits rows: every expert ties
+    wn = eps = None
+    if noise:
+        wn = torch.randn(N, d, device="cuda", generator=g) / d ** 0.5
+        eps = torch.randn(T, N, device="cuda", generator=g)
+    quota = K.expert_quota(cf, T, k, N)
+    out = K.gate_topk(x, w, k, quota, w_noise_t=wn, eps=eps)
+    torch.cuda.synchronize()
+    h = out.logits.double().cpu().numpy()
+    ref = O.apply_capacity(O.select_topk(h, k), cf, N, T)
+    np.testing.assert_array_equal(out.indices.long().cpu().numpy(), ref.indices)
+    np.testing.assert_array_equal(out.dropped.bool().cpu().numpy(), ref.dropped)
+    slots = O.capacity_slots(ref.indices, N)
+    np.testing.assert_array_equal(out.slots.long().cpu().numpy(), slots)
+    np.testing.assert_allclose(out.weights.double().cpu().numpy(), ref.weights, rtol=2e-6, atol=1e-7)
+    np.testing.assert_array_equal(out.counts.long().cpu().numpy(),
+                                  np.bincount(ref.indices.ravel(), minlength=N))
+    p = O.row_softmax(h).sum(axis=0)
+    np.testing.assert_allclose(out.prob_sum.double().cpu().numpy(), p, rtol=1e-4, atol=1e-3)
+    # logits vs a plain fp32 torch reference of the same op
+    hl = x.float() @ w.t()
+    if noise:
+        hl = hl + eps * torch.nn.functional.softplus(x.float() @ wn.t())
+    torch.testing.assert_close(out.logits, hl, rtol=1e-4, atol=1e-4)
+    return out
+
+
+@pytest.mark.parametrize("T,d,N,k,cf", [
+    (1, 8, 1, 1, 1.0), (7, 16, 3, 2, 0.5), (64, 32, 8, 1, 1.0), (65, 64, 8, 2, 1.0),
+    (1000, 256, 8, 1, 1.0), (4097, 128, 16, 2, 1.25), (16384, 2048, 8, 1, 2.0),
+    (16384, 2048, 8, 2, 2.0), (3000, 64, 33, 4, 0.75), (2048, 96, 64, 8, 0.3),
+    (512, 256, 8, 1, 0.25)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_gate_bit_exact(T, d, N, k, cf, dtype):
+    _gate_case(T, d, N, k, cf, dtype, seed=T * 31 + N)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_gate_ties_and_zeros(dtype):
+    out = _gate_case(777, 64, 6, 2, 1.0, dtype, seed=5, ties=True, zeros=True)
+    idx = out.indices.long().cpu().numpy()
+    assert (idx[::3, 0] == 0).all() and (idx[::3, 1] == 1).all()   # all-tied rows
+
+
+def test_gate_noise():
+    _gate_case(1500, 128, 8, 2, 1.0, torch.float32, seed=9, noise=True)
+
+
+def test_gate_rejects_bad_args():
+    x = torch.randn(8, 16, device="cuda")
+    w = torch.randn(4, 16, device="cuda")
+    with pytest.raises(ValueError):
+        K.gate_topk(x, w, 5, 4)
+    with pytest.raises(ValueError):
+        K.gate_topk(torch.randn(8, 12, device="cuda"), torch.randn(4, 12, device="cuda"), 1, 4)
+
+
+def _ref_ffn_rows(a, wt, bias, gelu):
+    y = a.double() @ wt.double().t()
+    if bias is not None:
+        y = y + bias.double()
+    if gelu:
+        y = torch.nn.functional.gelu(y)
+    return y
+
+
+@pytest.mark.parametrize("G,W,C,Kd,N", [
+    (1, 1, 128, 64, 256), (1, 1, 300, 200, 136), (8, 8, 512, 256, 1024), (4, 2, 130, 72, 520),
+    (8, 8, 1024, 2048, 8192), (3, 3, 257, 1024, 264), (16, 16, 64, 384, 1536)])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu):
+    g = torch.Generator(device="cuda").manual_seed(G * 7 + C)
+    a = torch.randn(G, C, Kd, device="cuda", generator=g).bfloat16()
+    wt = (torch.randn(W, N, Kd, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
+    bias = torch.randn(W, N, device="cuda", generator=g) * 0.1
+    rows = torch.randint(0, C + 40, (G,), device="cuda", generator=g, dtype=torch.int32)
+    rows[0] = C + 7   # clipped to C
+    if G > 1:
+        rows[1] = 0   # empty group
+    out = torch.full((G, C, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=gelu, out=out)
+    torch.cuda.synchronize()
+    rr = rows.clamp(max=C).cpu().tolist()
+    for gi in range(G):
+        r = rr[gi]
+        if r == 0:
+            assert torch.isnan(out[gi].float()).all()
+            continue
+        ref = _ref_ffn_rows(a[gi, :r], wt[gi % W], bias[gi % W], gelu)
+        got = out[gi, :r].double()
+        # bf16 output: |err| <= 2e-2 * (|ref| + max|ref|)
+        tol = 2e-2 * (ref.abs() + ref.abs().max())
+        assert ((got - ref).abs() <= tol).all(), (gi, (got - ref).abs().max().item())
+        if r < C:
+            assert torch.isnan(out[gi, r:].float()).all()   # rows past the count untouched
+
+
+@pytest.mark.parametrize("G,C,Kd,N", [(1, 100, 60, 70), (4, 129, 256, 1024), (8, 64, 256, 1024)])
+def test_grouped_gemm_f32(G, C, Kd, N):
+    g = torch.Generator(device="cuda").manual_seed(C)
+    a = torch.randn(G, C, Kd, device="cuda", generator=g)
+    wt = torch.randn(G, N, Kd, device="cuda", generator=g) / Kd ** 0.5
+    bias = torch.randn(G, N, device="cuda", generator=g)
+    rows = torch.tensor([C - 3 * i for i in range(G)], device="cuda", dtype=torch.int32)
+    out = K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=True)
+    for gi in range(G):
+        r = C - 3 * gi
+        ref = _ref_ffn_rows(a[gi, :r], wt[gi], bias[gi], True)
+        torch.testing.assert_close(out[gi, :r].double(), ref, rtol=1e-5, atol=1e-5)
+
+
+def test_dense_gemm_matches_torch_large():
+    """Dense (single-group, no row counts) path used by the shared expert."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    T, d, h = 4096, 2048, 8192
+    x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    w1t = (torch.randn(h, d, device="cuda", generator=g) / d ** 0.5).bfloat16()
+    b1 = torch.zeros(h, device="cuda")
+    w2t = (torch.randn(d, h, device="cuda", generator=g) / d ** 0.5).bfloat16()
+    b2 = torch.randn(d, device="cuda", generator=g)
+    y = K.expert_ffn(x, w1t, b1, w2t, b2)
+    hid = torch.nn.functional.gelu(x.float() @ w1t.float().t()).bfloat16()
+    ref = hid.float() @ w2t.float().t() + b2
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item(), err
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("k", [1, 2])
+def test_dispatch_and_combine(dtype, k):
+    g = torch.Generator(device="cuda").manual_seed(k)
+    T, d, N = 999, 256, 8
+    x = torch.randn(T, d, device="cuda", generator=g).to(dtype)
+    w = torch.randn(N, d, device="cuda", generator=g) / d ** 0.5
+    quota = K.expert_quota(0.75, T, k, N)
+    dec = K.gate_topk(x, w, k, quota)
+    buf = torch.zeros(N, quota, d, device="cuda", dtype=dtype)
+    K.dispatch(x, dec.indices, dec.slots, N, quota, out=buf)
+    idx, sl = dec.indices.long(), dec.slots.long()
+    kept = sl < quota
+    ref_buf = torch.zeros_like(buf)
+    tt = torch.arange(T, device="cuda")[:, None].expand(T, k)
+    ref_buf[idx[kept], sl[kept]] = x[tt[kept]]
+    assert torch.equal(buf, ref_buf)
+    # combine in every mode, with / without residual
+    y = torch.randn(N, quota, d, device="cuda", generator=g).to(dtype)
+    se = torch.randn(T, d, device="cuda", generator=g).to(dtype)
+    res = torch.randn(T, d, device="cuda", generator=g).to(dtype)
+    routed = torch.zeros(T, d, device="cuda", dtype=torch.float64)
+    for j in range(k):
+        m = kept[:, j]
+        routed[m] += dec.weights[m, j, None].double() * y[idx[m, j], sl[m, j]].double()
+    for mode, rows in (("direct_add", 0), ("cg1", 1), ("cg2", 2)):
+        wcg = torch.randn(max(rows, 1), d, device="cuda", generator=g) / d ** 0.5
+        z = x.double() @ wcg.double().t()
+        if mode == "direct_add":
+            ref = se.double() + routed
+        elif mode == "cg1":
+            ref = torch.sigmoid(z[:, :1]) * se.double() + routed
+        else:
+            c = torch.softmax(z, dim=1)
+            ref = c[:, :1] * se.double() + c[:, 1:2] * routed
+        for r in (None, res):
+            out = K.combine(y, dec.indices, dec.slots, dec.weights, quota, se_out=se, mode=mode,
+                            x_cur=x, w_cg=wcg if rows else None, residual=r)
+            expect = ref + (r.double() if r is not None else 0)
+            tol = 1e-5 if dtype == torch.float32 else 2e-2
+            torch.testing.assert_close(out.double(), expect, rtol=tol, atol=tol * expect.abs().max().item())
+    # moe_standard: no shared expert
+    out = K.combine(y, dec.indices, dec.slots, dec.weights, quota)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    torch.testing.assert_close(out.double(), routed, rtol=tol, atol=tol * routed.abs().max().item())

@@ -1,0 +1,58 @@
+"""Host-side behaviour that needs no GPU: config validation, quota rule, and
+the product refusing to run on CPU tensors (no fallback)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2404_05019_b200 as P
+from oracle import scmoe_oracle as O
+
+
+def test_quota_matches_oracle():
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        cf = float(rng.uniform(0.05, 4.0))
+        t, k, n = int(rng.integers(1, 70000)), int(rng.integers(1, 3)), int(rng.integers(1, 65))
+        assert P.expert_quota(cf, t, k, n) == O.expert_quota(cf, t, k, n)
+
+
+def test_capacity_config_validation():
+    with pytest.raises(ValueError):
+        P.CapacityConfig(capacity_factor=0)
+    with pytest.raises(ValueError):
+        P.CapacityConfig(policy="reroute")
+
+
+def test_layer_config_validation():
+    with pytest.raises(P.ConfigError):
+        P.ScMoELayer(16, 32, 4, combine_mode="mystery", device="cpu")
+    with pytest.raises(P.ConfigError):
+        P.ScMoELayer(16, 32, 65, device="cpu")
+    with pytest.raises(ValueError):
+        P.Top2MoELayer(16, 32, 1, k_routed=2, device="cpu")
+    with pytest.raises(P.ConfigError):
+        P.ScMoEBlockPair(16, 32, 4, variant="scmoe", shortcut_pos=None, device="cpu")
+    with pytest.raises(P.ConfigError):
+        P.ScMoEBlockPair(16, 32, 4, variant="standard", combine_mode="cg1", device="cpu")
+
+
+def test_cpu_tensors_fail_loudly():
+    m = P.ScMoELayer(16, 32, 4, dtype=torch.float32, device="cpu")
+    x = torch.randn(8, 16)
+    with pytest.raises((RuntimeError, ImportError)):
+        m(x, x)
+
+
+def test_from_reference_layout():
+    """Weights are stored K-major (transposed) after import."""
+    pp = O.init_pair(8, 16, 4, O.Rng(3).spawn(0), variant="scmoe", combine_mode="cg2")
+    m = P.ScMoELayer.from_reference(pp.moe, P.CapacityConfig(1.25), dtype=torch.float32,
+                                    device="cpu")
+    assert m.combine_mode == "cg2" and m.capacity.capacity_factor == 1.25
+    np.testing.assert_allclose(m.experts.w1t[2].numpy(), pp.moe.experts[2].w1.T, rtol=1e-6)
+    np.testing.assert_allclose(m.shared.w2t.numpy(), pp.moe.shared.w2.T, rtol=1e-6)
+    np.testing.assert_allclose(m.gate.w_gate_t.numpy(), pp.moe.gate.w_gate.T, rtol=1e-6)
+    np.testing.assert_allclose(m.w_cg.numpy(), pp.moe.w_cg, rtol=1e-6)
