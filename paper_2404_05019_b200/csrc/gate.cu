@@ -98,32 +98,46 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
     }
     __syncthreads();
     if (valid1) {
-      for (int c = sub * VEC; c < dc; c += VEC * TPT) {
-        Vec16<T> v;
-        v.raw = ld_nc_v4(xrow + c0 + c);
-        float xf[VEC];
-        v.to_float(xf);
+      // issue every 16-byte load of this chunk before the FMAs: MAXV loads in
+      // flight per thread instead of one (the kernel is latency-bound otherwise)
+      constexpr int STEP = VEC * TPT;
+      constexpr int MAXV = 256 / STEP;
+      uint4 xr[MAXV];
 #pragma unroll
-        for (int e = 0; e < NMAX; ++e) {
-          if (e < N) {
-            const float4* w4 = reinterpret_cast<const float4*>(wsm + e * dc_max + c);
+      for (int u = 0; u < MAXV; ++u) {
+        const int c = sub * VEC + u * STEP;
+        if (c < dc) xr[u] = ld_nc_v4(xrow + c0 + c);
+      }
 #pragma unroll
-            for (int q = 0; q < VEC / 4; ++q) {
-              const float4 w = w4[q];
-              acc[e] = fmaf(xf[4 * q + 0], w.x, acc[e]);
-              acc[e] = fmaf(xf[4 * q + 1], w.y, acc[e]);
-              acc[e] = fmaf(xf[4 * q + 2], w.z, acc[e]);
-              acc[e] = fmaf(xf[4 * q + 3], w.w, acc[e]);
-            }
-            if (NOISE) {
-              const float4* n4 = reinterpret_cast<const float4*>(wsm + (N + e) * dc_max + c);
+      for (int u = 0; u < MAXV; ++u) {
+        const int c = sub * VEC + u * STEP;
+        if (c < dc) {
+          Vec16<T> v;
+          v.raw = xr[u];
+          float xf[VEC];
+          v.to_float(xf);
+#pragma unroll
+          for (int e = 0; e < NMAX; ++e) {
+            if (e < N) {
+              const float4* w4 = reinterpret_cast<const float4*>(wsm + e * dc_max + c);
 #pragma unroll
               for (int q = 0; q < VEC / 4; ++q) {
-                const float4 w = n4[q];
-                accn[e] = fmaf(xf[4 * q + 0], w.x, accn[e]);
-                accn[e] = fmaf(xf[4 * q + 1], w.y, accn[e]);
-                accn[e] = fmaf(xf[4 * q + 2], w.z, accn[e]);
-                accn[e] = fmaf(xf[4 * q + 3], w.w, accn[e]);
+                const float4 w = w4[q];
+                acc[e] = fmaf(xf[4 * q + 0], w.x, acc[e]);
+                acc[e] = fmaf(xf[4 * q + 1], w.y, acc[e]);
+                acc[e] = fmaf(xf[4 * q + 2], w.z, acc[e]);
+                acc[e] = fmaf(xf[4 * q + 3], w.w, acc[e]);
+              }
+              if (NOISE) {
+                const float4* n4 = reinterpret_cast<const float4*>(wsm + (N + e) * dc_max + c);
+#pragma unroll
+                for (int q = 0; q < VEC / 4; ++q) {
+                  const float4 w = n4[q];
+                  accn[e] = fmaf(xf[4 * q + 0], w.x, accn[e]);
+                  accn[e] = fmaf(xf[4 * q + 1], w.y, accn[e]);
+                  accn[e] = fmaf(xf[4 * q + 2], w.z, accn[e]);
+                  accn[e] = fmaf(xf[4 * q + 3], w.w, accn[e]);
+                }
               }
             }
           }
@@ -311,8 +325,8 @@ int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
   SCMOE_CUDA_TRY(cudaMemsetAsync(counts, 0, (size_t)N * sizeof(int32_t), st));
   const bool noise = wn != nullptr;
   // gate-weight chunk: keep the staged block <= 64 KB
-  int dc = 256;
-  while (dc > 16 && (size_t)(noise ? 2 : 1) * N * dc * 4 > 65536) dc >>= 1;
+  int dc = 256;  // <= 256: the kernel's per-chunk load batch covers 256 columns
+  while (dc > 32 && (size_t)(noise ? 2 : 1) * N * dc * 4 > 65536) dc >>= 1;
   const size_t smem = (size_t)(noise ? 2 : 1) * N * dc * 4;
   if (noise) {
     auto kern = gate_topk_kernel<T, NMAX, true>;

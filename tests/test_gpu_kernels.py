@@ -88,7 +88,7 @@ def test_gate_rejects_bad_args():
     with pytest.raises(ValueError):
         K.gate_topk(x, w, 5, 4)
     with pytest.raises(ValueError):
-        K.gate_topk(torch.randn(8, 12, device="cuda"), torch.randn(4, 12, device="cuda"), 1, 4)
+        K.gate_topk(torch.randn(8, 10, device="cuda"), torch.randn(4, 10, device="cuda"), 1, 4)
 
 
 def _ref_ffn_rows(a, wt, bias, gelu):
