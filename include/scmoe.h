@@ -96,23 +96,32 @@ int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens, int d
  * for r < rows(g), rows(g) = min(group_rows[g], rows_clip) (group_rows NULL:
  * rows(g) = group_cap).  a is (num_groups, group_cap, k_in), wt is
  * (n_wgroups, n_out, k_in), bias (n_wgroups, n_out) fp32 or NULL, out is
- * (num_groups, group_cap, n_out); epi = bias (+ exact-erf GELU).
+ * (num_groups, group_cap, n_out); epi = bias (+ exact-erf GELU), then
+ * + residual[g, r, :] when `residual` (same layout as out) is not NULL — the
+ * block's residual add (arch.py:542, 587-588) fused into the epilogue.
  * SCMOE_BF16 runs the tcgen05/TMEM/TMA kernel (fp32 accumulate);
  * SCMOE_F32 runs the fp32 FFMA parity kernel.
  */
-int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias, void* out,
+int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias,
+                       const void* residual, void* out,
                        int num_groups, int n_wgroups, int group_cap,
                        const int32_t* group_rows, int rows_clip,
                        int n_out, int k_in, int epilogue, void* stream);
 
+/* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
+ * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
+int scmoe_set_gemm_mode(int mode);
+
 /*
  * Full expert_forward (arch.py:349-351) over groups: GEMM1 (bias+GELU) into
- * `hidden` (num_groups, group_cap, d_hidden), then GEMM2 (bias) into `out`.
+ * `hidden` (num_groups, group_cap, d_hidden), then GEMM2 (bias, + residual
+ * when not NULL) into `out`.
  * The dense shared expert / Block-MLP is num_groups = n_wgroups = 1,
  * group_rows = NULL, group_cap = T.
  */
 int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const float* b1,
-                     const void* w2t, const float* b2, void* hidden, void* out,
+                     const void* w2t, const float* b2, const void* residual,
+                     void* hidden, void* out,
                      int num_groups, int n_wgroups, int group_cap,
                      const int32_t* group_rows, int rows_clip,
                      int d_model, int d_hidden, void* stream);

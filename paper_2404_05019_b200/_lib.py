@@ -33,8 +33,10 @@ SIGNATURES = [
     ("scmoe_gate_topk", _i, [_vp, _i, _ll, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                              _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     ("scmoe_dispatch", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),
-    ("scmoe_grouped_gemm", _i, [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i, _vp]),
-    ("scmoe_expert_ffn", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i,
+    ("scmoe_grouped_gemm", _i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i,
+                                _vp]),
+    ("scmoe_set_gemm_mode", _i, [_i]),
+    ("scmoe_expert_ffn", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i,
                               _i, _i, _vp]),
     ("scmoe_combine", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                            _vp, _vp]),

@@ -74,7 +74,8 @@ class Attention(nn.Module):
             self.w_o_t.copy_(_as_tensor(np.asarray(a.w_o).T, dev, dt))
         return self
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, residual: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Attention output (+ residual, fused into the W_o GEMM epilogue)."""
         t, d = x.shape
         h = self.n_heads
         s = self.seq_len or t
@@ -86,7 +87,7 @@ class Attention(nn.Module):
         o = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal,
                                            scale=1.0 / math.sqrt(d) if h == 1 else None)
         o = o.permute(0, 2, 1, 3).reshape(t, d).contiguous()
-        return K.grouped_gemm(o, self.w_o_t, None)
+        return K.grouped_gemm(o, self.w_o_t, None, residual=residual)
 
 
 class ScMoEBlockPair(nn.Module):
@@ -181,16 +182,17 @@ class ScMoEBlockPair(nn.Module):
         env: Dict[str, object] = {}
         rec.begin(st)
 
+        # residual adds are fused into the GEMM epilogues (arch.py:542, 587-589)
         def attn_prev():
-            env["h_mh_prev"] = h_in + self.attn_prev(self._feed(h_in))
+            env["h_mh_prev"] = self.attn_prev(self._feed(h_in), residual=h_in)
 
         def mlp_prev():
             h = env["h_mh_prev"]
-            env["h_mlp_prev"] = h + self.mlp_prev(self._feed(h))
+            env["h_mlp_prev"] = self.mlp_prev(self._feed(h), residual=h)
 
         def attn_cur():
             h = env["h_mlp_prev"]
-            hc = h + self.attn_cur(self._feed(h))
+            hc = self.attn_cur(self._feed(h), residual=h)
             env["h_mh_cur"] = hc
             env["x_cur"] = self._feed(hc)
 

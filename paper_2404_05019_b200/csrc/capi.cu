@@ -26,11 +26,11 @@ int num_sms() {
   return n;
 }
 
-int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, void* out, int num_groups,
-                      int n_wgroups, int cap, const int32_t* group_rows, int rows_clip, int N,
-                      int K, int epi, cudaStream_t st);
-int grouped_gemm_f32(const float* a, const float* wt, const float* bias, float* out,
-                     int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, const void* residual,
+                      void* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                      int rows_clip, int N, int K, int epi, cudaStream_t st);
+int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const float* residual,
+                     float* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st);
 
 }  // namespace scmoe
@@ -55,7 +55,7 @@ extern "C" int scmoe_device_check(int device) {
 }
 
 extern "C" int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias,
-                                  void* out, int num_groups, int n_wgroups, int group_cap,
+                                  const void* residual, void* out, int num_groups, int n_wgroups, int group_cap,
                                   const int32_t* group_rows, int rows_clip, int n_out, int k_in,
                                   int epilogue, void* stream) {
   using namespace scmoe;
@@ -68,21 +68,23 @@ extern "C" int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, cons
   if (rows_clip <= 0) rows_clip = group_cap;
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == SCMOE_BF16)
-    return grouped_gemm_bf16(a, wt, bias, out, num_groups, n_wgroups, group_cap, group_rows,
+    return grouped_gemm_bf16(a, wt, bias, residual, out, num_groups, n_wgroups, group_cap, group_rows,
                              rows_clip, n_out, k_in, epilogue, st);
-  return grouped_gemm_f32((const float*)a, (const float*)wt, bias, (float*)out, num_groups,
+  return grouped_gemm_f32((const float*)a, (const float*)wt, bias, (const float*)residual,
+                          (float*)out, num_groups,
                           n_wgroups, group_cap, group_rows, rows_clip, n_out, k_in, epilogue, st);
 }
 
 extern "C" int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const float* b1,
-                                const void* w2t, const float* b2, void* hidden, void* out,
+                                const void* w2t, const float* b2, const void* residual,
+                                void* hidden, void* out,
                                 int num_groups, int n_wgroups, int group_cap,
                                 const int32_t* group_rows, int rows_clip, int d_model,
                                 int d_hidden, void* stream) {
-  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, hidden, num_groups, n_wgroups, group_cap,
+  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, num_groups, n_wgroups, group_cap,
                               group_rows, rows_clip, d_hidden, d_model, SCMOE_EPI_BIAS_GELU,
                               stream);
   if (rc) return rc;
-  return scmoe_grouped_gemm(hidden, dtype, w2t, b2, out, num_groups, n_wgroups, group_cap,
+  return scmoe_grouped_gemm(hidden, dtype, w2t, b2, residual, out, num_groups, n_wgroups, group_cap,
                             group_rows, rows_clip, d_model, d_hidden, SCMOE_EPI_BIAS, stream);
 }

@@ -88,62 +88,82 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
 #pragma unroll
   for (int e = 0; e < (NOISE ? NMAX : 1); ++e) accn[e] = 0.f;
 
-  for (int c0 = 0; c0 < d; c0 += dc_max) {
-    const int dc = min(dc_max, d - c0);
-    __syncthreads();
-    for (int i = tid; i < N * dc; i += THREADS) {
-      const int e = i / dc, c = i - e * dc;
-      wsm[e * dc_max + c] = wg_t[(long long)e * d + c0 + c];
-      if (NOISE) wsm[(N + e) * dc_max + c] = wn_t[(long long)e * d + c0 + c];
-    }
-    __syncthreads();
-    if (valid1) {
-      // issue every 16-byte load of this chunk before the FMAs: MAXV loads in
-      // flight per thread instead of one (the kernel is latency-bound otherwise)
-      constexpr int STEP = VEC * TPT;
-      constexpr int MAXV = 256 / STEP;
-      uint4 xr[MAXV];
+  // Load blocks of LB columns; each thread keeps MAXV 16-byte loads in flight
+  // and prefetches block b+1 while it multiplies block b.  Gate weights are
+  // staged in shared memory chunks of dc_max (a multiple of LB) columns.
+  constexpr int STEP = VEC * TPT;
+  constexpr int MAXV = (NMAX * (NOISE ? 2 : 1) >= 64) ? 4 : 8;  // bounded registers
+  constexpr int LB = MAXV * STEP;
+  const int nlb = (d + LB - 1) / LB;
+  uint4 cur[MAXV], nxt[MAXV];
 #pragma unroll
-      for (int u = 0; u < MAXV; ++u) {
-        const int c = sub * VEC + u * STEP;
-        if (c < dc) xr[u] = ld_nc_v4(xrow + c0 + c);
+  for (int u = 0; u < MAXV; ++u) {
+    const int c = sub * VEC + u * STEP;
+    cur[u] = (valid1 && c < d) ? ld_nc_v4(xrow + c) : make_uint4(0, 0, 0, 0);
+  }
+  int chunk0 = 0;
+  for (int lb = 0; lb < nlb; ++lb) {
+    const int cb = lb * LB;
+    if (cb % dc_max == 0) {
+      chunk0 = cb;
+      const int dc = min(dc_max, d - cb);
+      __syncthreads();
+      for (int i = tid * 4; i < N * dc; i += THREADS * 4) {
+        // dc is a multiple of 4: a float4 never straddles two experts
+        const int e = i / dc, c = i - e * dc;
+        *reinterpret_cast<float4*>(wsm + e * dc_max + c) =
+            __ldg(reinterpret_cast<const float4*>(wg_t + (long long)e * d + cb + c));
+        if (NOISE)
+          *reinterpret_cast<float4*>(wsm + (N + e) * dc_max + c) =
+              __ldg(reinterpret_cast<const float4*>(wn_t + (long long)e * d + cb + c));
       }
+      __syncthreads();
+    }
+    if (lb + 1 < nlb) {
 #pragma unroll
       for (int u = 0; u < MAXV; ++u) {
-        const int c = sub * VEC + u * STEP;
-        if (c < dc) {
-          Vec16<T> v;
-          v.raw = xr[u];
-          float xf[VEC];
-          v.to_float(xf);
+        const int c = cb + LB + sub * VEC + u * STEP;
+        nxt[u] = (valid1 && c < d) ? ld_nc_v4(xrow + c) : make_uint4(0, 0, 0, 0);
+      }
+    }
 #pragma unroll
-          for (int e = 0; e < NMAX; ++e) {
-            if (e < N) {
-              const float4* w4 = reinterpret_cast<const float4*>(wsm + e * dc_max + c);
+    for (int u = 0; u < MAXV; ++u) {
+      const int c = cb + sub * VEC + u * STEP;
+      if (c < d) {
+        Vec16<T> v;
+        v.raw = cur[u];
+        float xf[VEC];
+        v.to_float(xf);
+        const int cw = c - chunk0;
+#pragma unroll
+        for (int e = 0; e < NMAX; ++e) {
+          if (e < N) {
+            const float4* w4 = reinterpret_cast<const float4*>(wsm + e * dc_max + cw);
+#pragma unroll
+            for (int q = 0; q < VEC / 4; ++q) {
+              const float4 w = w4[q];
+              acc[e] = fmaf(xf[4 * q + 0], w.x, acc[e]);
+              acc[e] = fmaf(xf[4 * q + 1], w.y, acc[e]);
+              acc[e] = fmaf(xf[4 * q + 2], w.z, acc[e]);
+              acc[e] = fmaf(xf[4 * q + 3], w.w, acc[e]);
+            }
+            if (NOISE) {
+              const float4* n4 = reinterpret_cast<const float4*>(wsm + (N + e) * dc_max + cw);
 #pragma unroll
               for (int q = 0; q < VEC / 4; ++q) {
-                const float4 w = w4[q];
-                acc[e] = fmaf(xf[4 * q + 0], w.x, acc[e]);
-                acc[e] = fmaf(xf[4 * q + 1], w.y, acc[e]);
-                acc[e] = fmaf(xf[4 * q + 2], w.z, acc[e]);
-                acc[e] = fmaf(xf[4 * q + 3], w.w, acc[e]);
-              }
-              if (NOISE) {
-                const float4* n4 = reinterpret_cast<const float4*>(wsm + (N + e) * dc_max + c);
-#pragma unroll
-                for (int q = 0; q < VEC / 4; ++q) {
-                  const float4 w = n4[q];
-                  accn[e] = fmaf(xf[4 * q + 0], w.x, accn[e]);
-                  accn[e] = fmaf(xf[4 * q + 1], w.y, accn[e]);
-                  accn[e] = fmaf(xf[4 * q + 2], w.z, accn[e]);
-                  accn[e] = fmaf(xf[4 * q + 3], w.w, accn[e]);
-                }
+                const float4 w = n4[q];
+                accn[e] = fmaf(xf[4 * q + 0], w.x, accn[e]);
+                accn[e] = fmaf(xf[4 * q + 1], w.y, accn[e]);
+                accn[e] = fmaf(xf[4 * q + 2], w.z, accn[e]);
+                accn[e] = fmaf(xf[4 * q + 3], w.w, accn[e]);
               }
             }
           }
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < MAXV; ++u) cur[u] = nxt[u];
   }
   // reduce the TPT partial sums of a token (adjacent lanes)
 #pragma unroll
@@ -324,10 +344,13 @@ int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
   SCMOE_CUDA_TRY(cudaMemsetAsync(ws, 0, CTR_BYTES + (size_t)tiles * N * 4, st));
   SCMOE_CUDA_TRY(cudaMemsetAsync(counts, 0, (size_t)N * sizeof(int32_t), st));
   const bool noise = wn != nullptr;
-  // gate-weight chunk: keep the staged block <= 64 KB
-  int dc = 256;  // <= 256: the kernel's per-chunk load batch covers 256 columns
-  while (dc > 32 && (size_t)(noise ? 2 : 1) * N * dc * 4 > 65536) dc >>= 1;
-  const size_t smem = (size_t)(noise ? 2 : 1) * N * dc * 4;
+  // gate-weight chunk: a multiple of the (largest) load block, the whole row when it
+  // fits in 64 KB of shared memory
+  constexpr int LB = 8 * Vec16<T>::N * TPT;
+  const size_t per_col = (size_t)(noise ? 2 : 1) * N * 4;
+  int dc = ((d + LB - 1) / LB) * LB;
+  while (dc > LB && per_col * dc > 65536) dc -= LB;
+  const size_t smem = per_col * dc;
   if (noise) {
     auto kern = gate_topk_kernel<T, NMAX, true>;
     SCMOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

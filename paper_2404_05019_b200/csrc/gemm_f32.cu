@@ -14,7 +14,7 @@ constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256;
 template <int EPI>
 __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(
     const float* __restrict__ a, const float* __restrict__ wt, const float* __restrict__ bias,
-    float* __restrict__ out, int n_wgroups, int cap, const int32_t* __restrict__ group_rows,
+    const float* __restrict__ residual, float* __restrict__ out, int n_wgroups, int cap, const int32_t* __restrict__ group_rows,
     int rows_clip, int N, int K) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
@@ -81,21 +81,24 @@ __global__ void __launch_bounds__(THREADS) gemm_f32_kernel(
       if (n >= N) continue;
       float v = acc[i][j] + (bias ? bias[(long long)wg * N + n] : 0.f);
       if (EPI == SCMOE_EPI_BIAS_GELU) v = gelu_erf(v);
-      out[((long long)g * cap + m) * N + n] = v;
+      const long long o = ((long long)g * cap + m) * N + n;
+      if (residual) v += residual[o];
+      out[o] = v;
     }
   }
 }
 }  // namespace
 
-int grouped_gemm_f32(const float* a, const float* wt, const float* bias, float* out,
+int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const float* residual,
+                     float* out,
                      int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st) {
   dim3 grid((N + BN - 1) / BN, (cap + BM - 1) / BM, num_groups);
   if (epi == SCMOE_EPI_BIAS_GELU)
-    gemm_f32_kernel<SCMOE_EPI_BIAS_GELU><<<grid, THREADS, 0, st>>>(a, wt, bias, out, n_wgroups, cap,
+    gemm_f32_kernel<SCMOE_EPI_BIAS_GELU><<<grid, THREADS, 0, st>>>(a, wt, bias, residual, out, n_wgroups, cap,
                                                                    group_rows, rows_clip, N, K);
   else
-    gemm_f32_kernel<SCMOE_EPI_BIAS><<<grid, THREADS, 0, st>>>(a, wt, bias, out, n_wgroups, cap,
+    gemm_f32_kernel<SCMOE_EPI_BIAS><<<grid, THREADS, 0, st>>>(a, wt, bias, residual, out, n_wgroups, cap,
                                                               group_rows, rows_clip, N, K);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;

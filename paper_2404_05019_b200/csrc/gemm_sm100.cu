@@ -1,23 +1,30 @@
 // K3 / K4 — grouped bf16 GEMM on 5th-generation tensor cores (tcgen05).
 //
-//   out[g, r, :] = epi( a[g, r, :] . wt[g % n_wgroups, :, :]^T + bias )
+//   out[g, r, :] = epi( a[g, r, :] . wt[g % n_wgroups, :, :]^T + bias (+ residual[g, r, :]) )
 //
 // for r < rows(g) = min(group_rows[g], rows_clip): the routed experts read the
 // capacity-slotted dispatch buffer (group = expert, rows = kept tokens, known
 // only on the device), the shared expert / Block-MLP is a single group.  The
-// epilogue is expert_forward's bias (+ exact-erf GELU) (arch.py:349-351).
+// epilogue is expert_forward's bias (+ exact-erf GELU) (arch.py:349-351),
+// optionally fused with the block's residual add (arch.py:542, 587-588).
 //
-// Structure (persistent, one CTA per SM, 384 threads):
-//   warp 0      TMA producer: A (128x64) and B (256x64) bf16 tiles, 128B
-//               swizzle, into a 4-stage shared-memory ring (full/empty mbarriers)
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
-//               128x256x16, accumulating in TMEM; tcgen05.commit frees smem
-//               stages and signals the epilogue
-//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//   warps 4-11  epilogue: tcgen05.ld 32x32b -> bias/GELU -> bf16 -> global,
-//               double-buffered against the MMA of the next tile
+// Structure (persistent, 384 threads per CTA, one CTA per SM):
+//   warp 0      TMA producer: 128B-swizzled A / B tiles into a shared-memory
+//               ring (full / empty mbarriers)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma kind::f16, fp32
+//               accumulators in TMEM; tcgen05.commit frees ring stages and
+//               signals the epilogue
+//   warp 2      TMEM allocator (512 columns = two 256-column accumulators)
+//   warps 4-11  epilogue: tcgen05.ld 32x32b -> bias / GELU / residual -> bf16
+//               -> global, double-buffered against the next tile's MMAs
+// Two variants:
+//   1SM  tile 128x256, cta_group::1, 4 stages of 48 KB
+//   2SM  tile 256x256 per CTA pair (cluster of 2), cta_group::2: each CTA
+//        loads its 128 rows of A and half of B (128 rows), the leader issues
+//        M=256 MMAs that read both CTAs' shared memory and write both TMEMs;
+//        6 stages of 32 KB per CTA
 // Tiles are walked in (group, m-tile, n-tile) order with n fastest, skipping
-// the m-tiles past each group's device-side row count.
+// m-tiles past each group's device-side row count.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -26,30 +33,48 @@
 namespace scmoe {
 namespace sm100 {
 
-constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int STAGES = 4;
-constexpr int ACC_STAGES = 2;
+constexpr int BN = 256, BK = 64;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + EPI_WARPS * 32;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
+constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = ACC_STAGES * BN;
 constexpr int MAX_GROUPS = 1024;
-constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 256 + (MAX_GROUPS + 1) * 4;
 
-// instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=256
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+template <bool TWO_SM>
+struct Cfg {
+  static constexpr int CTA_M = 128;                       // rows of A per CTA
+  static constexpr int TILE_M = TWO_SM ? 256 : 128;       // rows per (cluster) tile
+  static constexpr int B_ROWS = TWO_SM ? BN / 2 : BN;     // rows of B per CTA
+  static constexpr int STAGES = TWO_SM ? 6 : 4;
+  static constexpr int A_BYTES = CTA_M * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256 + (MAX_GROUPS + 1) * 4;
+  // instruction descriptor: D fp32, A/B bf16, K-major, M=TILE_M, N=256
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
+                                    ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(TILE_M >> 4) << 24);
+};
 
 struct Params {
   int num_groups, n_wgroups, cap, rows_clip, N, K, epi;
   const int32_t* group_rows;
   const float* bias;
+  const __nv_bfloat16* residual;
   __nv_bfloat16* out;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -61,6 +86,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on the same-offset barrier of CTA `rank` in the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -81,25 +113,54 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// 2-SM TMA: bytes land in this CTA's shared memory, completion is counted on
+// the leader CTA's barrier (peer bit cleared in the cluster address).
+__device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+template <bool TWO_SM>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+  if (TWO_SM) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  }
 }
+template <bool TWO_SM>
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+  if (TWO_SM) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(Cfg<true>::IDESC), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(Cfg<false>::IDESC), "r"(accumulate));
+  }
 }
 // K-major operand, 128-byte swizzle: rows of 64 bf16 (128 B), 8-row groups
 // 1024 B apart (SBO), version 1 (sm_100), layout type 2 (SWIZZLE_128B).
@@ -124,6 +185,7 @@ struct TileCoord {
   int g, m0, n0;
 };
 
+template <int TILE_M>
 __device__ __forceinline__ TileCoord decode_tile(int t, int n_tiles_n, const int* prefix,
                                                  int num_groups) {
   const int mlin = t / n_tiles_n;
@@ -136,7 +198,7 @@ __device__ __forceinline__ TileCoord decode_tile(int t, int n_tiles_n, const int
   }
   TileCoord c;
   c.g = lo;
-  c.m0 = (mlin - prefix[lo]) * BM;
+  c.m0 = (mlin - prefix[lo]) * TILE_M;
   c.n0 = nt * BN;
   return c;
 }
@@ -145,43 +207,56 @@ __device__ __forceinline__ int group_rows_of(const Params& p, int g) {
   return p.group_rows ? min(__ldg(p.group_rows + g), p.rows_clip) : p.cap;
 }
 
+template <bool TWO_SM>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, const Params p) {
+  using C = Cfg<TWO_SM>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_b + STAGES * B_BYTES);
+  uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_b + C::STAGES * C::B_BYTES);
   uint64_t* full_bar = bars;
-  uint64_t* empty_bar = bars + STAGES;
-  uint64_t* tfull_bar = bars + 2 * STAGES;
-  uint64_t* tempty_bar = bars + 2 * STAGES + ACC_STAGES;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
-  int* s_prefix = reinterpret_cast<int*>(smem_b + STAGES * B_BYTES + 256);
+  uint64_t* empty_bar = bars + C::STAGES;
+  uint64_t* tfull_bar = bars + 2 * C::STAGES;
+  uint64_t* tempty_bar = bars + 2 * C::STAGES + ACC_STAGES;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 2 * ACC_STAGES);
+  int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = TWO_SM ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int unit = TWO_SM ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // cluster / CTA id
+  const int n_units = TWO_SM ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], EPI_WARPS);
+      mbar_init(&tempty_bar[s], (TWO_SM ? 2 : 1) * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(s_tmem)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (TWO_SM) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (warp == 3) {
     // exclusive prefix of m-tiles per group (warp scan, 32 groups at a time)
@@ -190,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int base = 0; base < p.num_groups; base += 32) {
       const int g = base + lane;
       int v = 0;
-      if (g < p.num_groups) v = (group_rows_of(p, g) + BM - 1) / BM;
+      if (g < p.num_groups) v = (group_rows_of(p, g) + C::TILE_M - 1) / C::TILE_M;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int u = __shfl_up_sync(0xffffffffu, v, o);
@@ -202,6 +277,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (TWO_SM) cluster_sync();  // peer barriers initialised before any multicast arrive
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
 
@@ -210,78 +286,88 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs load their own halves) =====
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileCoord tc = decode_tile(t, n_tiles_n, s_prefix, p.num_groups);
+    for (int t = unit; t < total_tiles; t += n_units) {
+      const TileCoord tc = decode_tile<C::TILE_M>(t, n_tiles_n, s_prefix, p.num_groups);
       const int wg = tc.g % p.n_wgroups;
+      const int am = tc.m0 + (int)rank * C::CTA_M;
+      const int bn = tc.n0 + (int)rank * C::B_ROWS;
       for (int kb = 0; kb < num_kb; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_expect_tx(&full_bar[stage], A_BYTES + B_BYTES);
-          tma_load_3d(&map_a, &full_bar[stage], smem_a + stage * A_BYTES, kb * BK, tc.m0, tc.g);
-          tma_load_3d(&map_b, &full_bar[stage], smem_b + stage * B_BYTES, kb * BK, tc.n0, wg);
+          if (TWO_SM) {
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+            tma_load_3d_2sm(&map_a, &full_bar[stage], smem_a + stage * C::A_BYTES, kb * BK, am, tc.g);
+            tma_load_3d_2sm(&map_b, &full_bar[stage], smem_b + stage * C::B_BYTES, kb * BK, bn, wg);
+          } else {
+            mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+            tma_load_3d(&map_a, &full_bar[stage], smem_a + stage * C::A_BYTES, kb * BK, am, tc.g);
+            tma_load_3d(&map_b, &full_bar[stage], smem_b + stage * C::B_BYTES, kb * BK, bn, wg);
+          }
         }
         __syncwarp();
-        if (++stage == STAGES) {
+        if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      if (lane == 0) {
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        tc_fence_after();
-      }
-      __syncwarp();
-      for (int kb = 0; kb < num_kb; ++kb) {
+    // ===== MMA issuer (leader CTA only in 2SM mode) =====
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = unit; t < total_tiles; t += n_units, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        const uint32_t d_tmem = tmem_base + acc * BN;
         if (lane == 0) {
-          mbar_wait(&full_bar[stage], phase);
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(smem_a + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(smem_b + stage * B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            tc_mma(d_tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32),
-                   (kb | kk) != 0 ? 1u : 0u);
-          }
-          tc_commit(&empty_bar[stage]);
         }
         __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if (lane == 0) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem_a + stage * C::A_BYTES);
+            const uint32_t b0 = smem_u32(smem_b + stage * C::B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              tc_mma<TWO_SM>(d_tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32),
+                             (kb | kk) != 0 ? 1u : 0u);
+            }
+            tc_commit<TWO_SM>(&empty_bar[stage]);
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        if (lane == 0) tc_commit<TWO_SM>(&tfull_bar[acc]);
+        __syncwarp();
       }
-      if (lane == 0) tc_commit(&tfull_bar[acc]);
-      __syncwarp();
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
+    // ===== epilogue (both CTAs, each on its own 128 TMEM lanes) =====
     const int ew = warp - 4;
-    const int quad = warp & 3;       // TMEM lanes [32*quad, 32*quad+32)
-    const int half = ew >> 2;        // accumulator columns [128*half, 128*half+128)
+    const int quad = warp & 3;   // TMEM lanes [32*quad, 32*quad+32)
+    const int half = ew >> 2;    // accumulator columns [128*half, 128*half+128)
     int it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      const TileCoord tc = decode_tile(t, n_tiles_n, s_prefix, p.num_groups);
+    for (int t = unit; t < total_tiles; t += n_units, ++it) {
+      const TileCoord tc = decode_tile<C::TILE_M>(t, n_tiles_n, s_prefix, p.num_groups);
       const int wg = tc.g % p.n_wgroups;
       const int rows = group_rows_of(p, tc.g);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = tc.m0 + quad * 32 + lane;
-      __nv_bfloat16* orow = p.out + ((long long)tc.g * p.cap + row) * p.N;
+      const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
+      const long long row_off = ((long long)tc.g * p.cap + row) * p.N;
       const float* brow = p.bias ? p.bias + (long long)wg * p.N : nullptr;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -290,6 +376,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + col;
         SCMOE_TMEM_LD32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == 3) {
+          // accumulator fully in registers: hand TMEM back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (TWO_SM) mbar_arrive_cluster(&tempty_bar[acc], 0);
+            else mbar_arrive(&tempty_bar[acc]);
+          }
+        }
         const int n = tc.n0 + col;
         if (row < rows && n < p.N) {
 #pragma unroll
@@ -309,25 +404,35 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] = gelu_erf(v[i]);
               }
+              if (p.residual) {
+                Vec16<__nv_bfloat16> rv;
+                rv.raw = ld_nc_v4(p.residual + row_off + nn);
+                float rf[8];
+                rv.to_float(rf);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += rf[i];
+              }
               Vec16<__nv_bfloat16> o;
               o.from_float(v);
-              st_v4(orow + nn, o.raw);
+              st_v4(p.out + row_off + nn, o.raw);
             }
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (TWO_SM) cluster_sync();  // the leader's MMAs write the peer's TMEM
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if (TWO_SM)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -369,29 +474,47 @@ int make_map(CUtensorMap* map, const void* base, int k_in, int rows, int groups,
   return SCMOE_OK;
 }
 
+template <bool TWO_SM>
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
+           cudaStream_t st) {
+  using C = Cfg<TWO_SM>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SCMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<TWO_SM>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = TWO_SM ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SCMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<TWO_SM>, ma, mb, p));
+  return SCMOE_OK;
+}
+
 }  // namespace sm100
 
-int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, void* out, int num_groups,
-                      int n_wgroups, int cap, const int32_t* group_rows, int rows_clip, int N,
-                      int K, int epi, cudaStream_t st) {
+// mode: 0 auto, 1 force 1-SM, 2 force 2-SM (tests / tuning)
+static int g_gemm_mode = 0;
+
+int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, const void* residual,
+                      void* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                      int rows_clip, int N, int K, int epi, cudaStream_t st) {
   using namespace sm100;
   SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
   SCMOE_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "bf16 GEMM needs k_in and n_out multiples of 8");
   SCMOE_CHECK_ARG(((uintptr_t)a & 15) == 0 && ((uintptr_t)wt & 15) == 0 &&
-                      ((uintptr_t)out & 15) == 0 && ((uintptr_t)bias & 15) == 0,
+                      ((uintptr_t)out & 15) == 0 && ((uintptr_t)bias & 15) == 0 &&
+                      ((uintptr_t)residual & 15) == 0,
                   "GEMM operands must be 16-byte aligned");
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, a, K, cap, num_groups, BM);
-  if (rc) return rc;
-  rc = make_map(&mb, wt, K, N, n_wgroups, BN);
-  if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SCMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)SMEM_BYTES));
-    attr_set = true;
-  }
   Params p;
   p.num_groups = num_groups;
   p.n_wgroups = n_wgroups;
@@ -402,14 +525,39 @@ int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, void* ou
   p.epi = epi;
   p.group_rows = group_rows;
   p.bias = bias;
+  p.residual = (const __nv_bfloat16*)residual;
   p.out = (__nv_bfloat16*)out;
-  const long long max_tiles =
-      (long long)num_groups * ((cap + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = (int)(max_tiles < num_sms() ? max_tiles : num_sms());
-  if (grid <= 0) return SCMOE_OK;
-  grouped_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  const int sms = num_sms();
+  const long long n_tiles_n = (N + BN - 1) / BN;
+  const long long tiles_2sm = (long long)num_groups * ((cap + 255) / 256) * n_tiles_n;
+  bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_2sm >= sms / 2);
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, a, K, cap, num_groups, 128);
+  if (rc) return rc;
+  rc = make_map(&mb, wt, K, N, n_wgroups, two ? BN / 2 : BN);
+  if (rc) return rc;
+  if (two) {
+    const long long units = tiles_2sm < sms / 2 ? tiles_2sm : sms / 2;
+    if (units <= 0) return SCMOE_OK;
+    rc = launch<true>(ma, mb, p, (int)units * 2, st);
+  } else {
+    const long long tiles = (long long)num_groups * ((cap + 127) / 128) * n_tiles_n;
+    const int grid = (int)(tiles < sms ? tiles : sms);
+    if (grid <= 0) return SCMOE_OK;
+    rc = launch<false>(ma, mb, p, grid, st);
+  }
+  if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }
 
 }  // namespace scmoe
+
+extern "C" int scmoe_set_gemm_mode(int mode) {
+  if (mode < 0 || mode > 2) {
+    scmoe::set_error("gemm mode must be 0 (auto), 1 (1-SM) or 2 (2-SM)");
+    return SCMOE_ERR_ARG;
+  }
+  scmoe::g_gemm_mode = mode;
+  return SCMOE_OK;
+}

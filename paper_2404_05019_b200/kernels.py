@@ -88,8 +88,9 @@ def dispatch(x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor, n_expe
 
 def grouped_gemm(a: torch.Tensor, wt: torch.Tensor, bias: Optional[torch.Tensor],
                  group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
-                 gelu: bool = False, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """out[g] = epi(a[g] @ wt[g % W]^T + bias[g % W]) on rows < rows(g).
+                 gelu: bool = False, out: Optional[torch.Tensor] = None,
+                 residual: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out[g] = epi(a[g] @ wt[g % W]^T + bias[g % W]) (+ residual[g]) on rows < rows(g).
 
     a: (G, C, K) or (C, K); wt: (W, N, K) or (N, K); bias fp32 (W, N)/(N,).
     """
@@ -106,8 +107,13 @@ def grouped_gemm(a: torch.Tensor, wt: torch.Tensor, bias: Optional[torch.Tensor]
         out = torch.empty(G, C, N, device=a.device, dtype=a.dtype)
     if bias is not None and bias.dtype != torch.float32:
         raise ValueError("bias must be fp32")
+    if residual is not None:
+        _c(residual, "residual")
+        if residual.numel() != out.numel() or residual.dtype != out.dtype:
+            raise ValueError("residual must match the output's shape and dtype")
     check(lib().scmoe_grouped_gemm(
-        ptr(_c(a3, "a")), dtype_code(a.dtype), ptr(_c(w3, "wt")), ptr(bias), ptr(out), G, W, C,
+        ptr(_c(a3, "a")), dtype_code(a.dtype), ptr(_c(w3, "wt")), ptr(bias), ptr(residual),
+        ptr(out), G, W, C,
         ptr(group_rows), rows_clip, N, K, _lib.EPI_BIAS_GELU if gelu else _lib.EPI_BIAS,
         stream_ptr(stream)))
     return out if a.dim() == 3 else out.squeeze(0)
@@ -116,7 +122,7 @@ def grouped_gemm(a: torch.Tensor, wt: torch.Tensor, bias: Optional[torch.Tensor]
 def expert_ffn(x: torch.Tensor, w1t: torch.Tensor, b1: torch.Tensor, w2t: torch.Tensor,
                b2: torch.Tensor, group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
                hidden: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
-               stream=None) -> torch.Tensor:
+               residual: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """expert_forward (arch.py:349-351) for every group: gelu(x W1 + b1) W2 + b2."""
     ensure_device(x)
     x3 = x if x.dim() == 3 else x.unsqueeze(0)
@@ -128,9 +134,13 @@ def expert_ffn(x: torch.Tensor, w1t: torch.Tensor, b1: torch.Tensor, w2t: torch.
         hidden = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
     if out is None:
         out = torch.empty(G, C, d, device=x.device, dtype=x.dtype)
+    if residual is not None:
+        _c(residual, "residual")
+        if residual.numel() != out.numel() or residual.dtype != out.dtype:
+            raise ValueError("residual must match the output's shape and dtype")
     check(lib().scmoe_expert_ffn(
         ptr(_c(x3, "x")), dtype_code(x.dtype), ptr(_c(w13, "w1t")), ptr(b1), ptr(_c(w23, "w2t")),
-        ptr(b2), ptr(hidden), ptr(out), G, W, C, ptr(group_rows), rows_clip, d, h,
+        ptr(b2), ptr(residual), ptr(hidden), ptr(out), G, W, C, ptr(group_rows), rows_clip, d, h,
         stream_ptr(stream)))
     return out if x.dim() == 3 else out.view(C, d)
 
@@ -154,3 +164,8 @@ def combine(expert_out: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor
         _lib.COMBINE_MODES[mode], ptr(residual), ptr(indices), ptr(slots), ptr(weights),
         capacity, T, d, k, dtype_code(expert_out.dtype), ptr(out), stream_ptr(stream)))
     return out
+
+
+def set_gemm_mode(mode: int) -> None:
+    """0 = auto, 1 = force the 1-SM tcgen05 kernel, 2 = force the 2-SM kernel."""
+    check(lib().scmoe_set_gemm_mode(mode))

@@ -261,12 +261,14 @@ class SharedExpert(nn.Module):
             self.b2.copy_(_as_tensor(np.asarray(e.b2).reshape(-1), dev, torch.float32))
         return self
 
-    def forward(self, x: torch.Tensor, hidden: Optional[torch.Tensor] = None,
-                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, residual: Optional[torch.Tensor] = None,
+                hidden: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+        """expert_forward(x) (+ residual, fused into the second GEMM's epilogue)."""
         if x.dtype != self.w1t.dtype:
             raise ValueError(f"input dtype {x.dtype} != expert dtype {self.w1t.dtype}")
         return K.expert_ffn(x, self.w1t, self.b1, self.w2t, self.b2, hidden=hidden, out=out,
-                            stream=stream)
+                            residual=residual, stream=stream)
 
 
 class RoutedExperts(nn.Module):

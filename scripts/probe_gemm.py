@@ -26,6 +26,13 @@ def main():
     w1t = (torch.randn(h, d, device="cuda") / d ** 0.5).bfloat16()
     b1 = torch.zeros(h, device="cuda")
     out = torch.empty(T, h, device="cuda", dtype=torch.bfloat16)
+    for mode in (1, 2):
+        K.set_gemm_mode(mode)
+        ms = t_ms(lambda: K.grouped_gemm(x, w1t, b1, gelu=True, out=out))
+        res[f"mode{mode}_dense_gemm1_gelu_tflops"] = 2 * T * d * h / ms / 1e9
+        ms = t_ms(lambda: K.grouped_gemm(x, w1t, None, gelu=False, out=out))
+        res[f"mode{mode}_dense_gemm1_nobias_tflops"] = 2 * T * d * h / ms / 1e9
+    K.set_gemm_mode(0)
     ms = t_ms(lambda: K.grouped_gemm(x, w1t, b1, gelu=True, out=out))
     res["dense_gemm1_gelu_ms"] = ms
     res["dense_gemm1_tflops"] = 2 * T * d * h / ms / 1e9

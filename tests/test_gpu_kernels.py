@@ -104,7 +104,17 @@ def _ref_ffn_rows(a, wt, bias, gelu):
     (1, 1, 128, 64, 256), (1, 1, 300, 200, 136), (8, 8, 512, 256, 1024), (4, 2, 130, 72, 520),
     (8, 8, 1024, 2048, 8192), (3, 3, 257, 1024, 264), (16, 16, 64, 384, 1536)])
 @pytest.mark.parametrize("gelu", [False, True])
-def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu, mode):
+    """Both tcgen05 variants (1-SM 128x256, 2-SM cta_group::2 256x256)."""
+    K.set_gemm_mode(mode)
+    try:
+        _grouped_gemm_case(G, W, C, Kd, N, gelu, residual=(mode == 2 and gelu))
+    finally:
+        K.set_gemm_mode(0)
+
+
+def _grouped_gemm_case(G, W, C, Kd, N, gelu, residual):
     g = torch.Generator(device="cuda").manual_seed(G * 7 + C)
     a = torch.randn(G, C, Kd, device="cuda", generator=g).bfloat16()
     wt = (torch.randn(W, N, Kd, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
@@ -114,7 +124,8 @@ def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu):
     if G > 1:
         rows[1] = 0   # empty group
     out = torch.full((G, C, N), float("nan"), device="cuda", dtype=torch.bfloat16)
-    K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=gelu, out=out)
+    res = torch.randn(G, C, N, device="cuda", generator=g).bfloat16() if residual else None
+    K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=gelu, out=out, residual=res)
     torch.cuda.synchronize()
     rr = rows.clamp(max=C).cpu().tolist()
     for gi in range(G):
@@ -123,6 +134,8 @@ def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu):
             assert torch.isnan(out[gi].float()).all()
             continue
         ref = _ref_ffn_rows(a[gi, :r], wt[gi % W], bias[gi % W], gelu)
+        if res is not None:
+            ref = ref + res[gi, :r].double()
         got = out[gi, :r].double()
         # bf16 output: |err| <= 2e-2 * (|ref| + max|ref|)
         tol = 2e-2 * (ref.abs() + ref.abs().max())
@@ -138,10 +151,11 @@ def test_grouped_gemm_f32(G, C, Kd, N):
     wt = torch.randn(G, N, Kd, device="cuda", generator=g) / Kd ** 0.5
     bias = torch.randn(G, N, device="cuda", generator=g)
     rows = torch.tensor([C - 3 * i for i in range(G)], device="cuda", dtype=torch.int32)
-    out = K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=True)
+    res = torch.randn(G, C, N, device="cuda", generator=g)
+    out = K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=True, residual=res)
     for gi in range(G):
         r = C - 3 * gi
-        ref = _ref_ffn_rows(a[gi, :r], wt[gi], bias[gi], True)
+        ref = _ref_ffn_rows(a[gi, :r], wt[gi], bias[gi], True) + res[gi, :r].double()
         torch.testing.assert_close(out[gi, :r].double(), ref, rtol=1e-5, atol=1e-5)
 
 
