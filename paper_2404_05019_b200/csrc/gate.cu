@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
   }
   __syncthreads();
 
-  // per-expert tile aggregate, within-tile warp offsets, look-back
+  // per-expert tile aggregate and within-tile warp offsets; publish the
+  // aggregate at once so later tiles can make progress
   if (tid < N) {
     const int e = tid;
     uint32_t run = 0;
@@ -273,28 +274,43 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
       run += (uint32_t)c;
       psum_tile += s_wprob[w][e];
     }
-    const uint32_t agg = run;
-    uint32_t* my = status + (size_t)tile * N + e;
-    uint32_t excl = 0;
-    if (tile == 0) {
-      st_volatile_u32(my, FLAG_INC | agg);
-    } else {
-      st_volatile_u32(my, FLAG_AGG | agg);
-      int j = tile - 1;
-      while (true) {
-        const uint32_t v = ld_volatile_u32(status + (size_t)j * N + e);
-        const uint32_t f = v & ~VAL_MASK;
-        if (f == 0) continue;
-        excl += v & VAL_MASK;
-        if (f == FLAG_INC) break;
-        --j;
-      }
-      st_volatile_u32(my, FLAG_INC | (excl + agg));
-    }
-    s_excl[e] = excl;
-    if (agg) atomicAdd(&counts[e], (int)agg);
+    s_excl[e] = run;  // temporarily: this tile's aggregate
+    st_volatile_u32(status + (size_t)tile * N + e, (tile == 0 ? FLAG_INC : FLAG_AGG) | run);
+    if (run) atomicAdd(&counts[e], (int)run);
     psum[(size_t)tile * N + e] = psum_tile;
     __threadfence();
+  }
+  __syncthreads();
+  // decoupled look-back, one warp per expert, 32 predecessor tiles per step:
+  // lane l reads tile (j - l); the nearest INCLUSIVE word ends the walk, every
+  // word before it must at least carry its AGGREGATE.  Tiles finish phase 1 at
+  // about the same time, so a one-tile-per-step walk would serialise ~T/TOK
+  // dependent loads.
+  for (int e = warp; e < N; e += THREADS / 32) {
+    const uint32_t agg = s_excl[e];
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int j = tile - 1;
+      while (true) {
+        const int jj = j - lane;
+        const uint32_t v = jj >= 0 ? ld_volatile_u32(status + (size_t)jj * N + e) : FLAG_INC;
+        const uint32_t f = v & ~VAL_MASK;
+        const unsigned inc = __ballot_sync(0xffffffffu, f == FLAG_INC);
+        const unsigned not_ready = __ballot_sync(0xffffffffu, f == 0);
+        const int first = inc ? __ffs(inc) - 1 : 31;              // last lane that counts
+        const unsigned span = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if (not_ready & span) continue;                          // retry the same window
+        uint32_t part = (lane <= first) ? (v & VAL_MASK) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (inc) break;
+        j -= 32;
+      }
+      if (lane == 0) st_volatile_u32(status + (size_t)tile * N + e, FLAG_INC | (excl + agg));
+    }
+    __syncwarp();
+    if (lane == 0) s_excl[e] = excl;
   }
   __syncthreads();
 

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
               if (p.epi == SCMOE_EPI_BIAS_GELU) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = gelu_erf(v[i]);
+                for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
               }
               if (p.residual) {
                 Vec16<__nv_bfloat16> rv;
