@@ -207,6 +207,43 @@ __device__ __forceinline__ int group_rows_of(const Params& p, int g) {
   return p.group_rows ? min(__ldg(p.group_rows + g), p.rows_clip) : p.cap;
 }
 
+// bias (+GELU) (+residual) -> bf16 for 32 consecutive columns of one row
+__device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
+                                               bool row_ok, long long row_off, int n,
+                                               const float* brow) {
+  if (!row_ok || n >= p.N) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int nn = n + u * 8;
+    if (nn < p.N) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
+      if (brow) {
+        const float4 b0 = *reinterpret_cast<const float4*>(brow + nn);
+        const float4 b1 = *reinterpret_cast<const float4*>(brow + nn + 4);
+        v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+        v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+      }
+      if (p.epi == SCMOE_EPI_BIAS_GELU) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
+      }
+      if (p.residual) {
+        Vec16<__nv_bfloat16> rv;
+        rv.raw = ld_nc_v4(p.residual + row_off + nn);
+        float rf[8];
+        rv.to_float(rf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += rf[i];
+      }
+      Vec16<__nv_bfloat16> o;
+      o.from_float(v);
+      st_v4(p.out + row_off + nn, o.raw);
+    }
+  }
+}
+
 template <bool TWO_SM>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -369,53 +406,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
       const long long row_off = ((long long)tc.g * p.cap + row) * p.N;
       const float* brow = p.bias ? p.bias + (long long)wg * p.N : nullptr;
-#pragma unroll 1
+      // TMEM -> registers in 4 chunks of 32 columns, chunk c+1's tcgen05.ld in
+      // flight while chunk c is processed
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
+      uint32_t ra[32], rb[32];
+      SCMOE_TMEM_LD32(tbase, ra);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int col = half * 128 + c * 32;
-        uint32_t r[32];
-        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + col;
-        SCMOE_TMEM_LD32(taddr, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == 3) {
-          // accumulator fully in registers: hand TMEM back to the MMA warp
+        uint32_t(&cur)[32] = (c & 1) ? rb : ra;
+        uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
+        if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
+        epilogue_chunk(p, cur, row < rows, row_off, tc.n0 + half * 128 + c * 32, brow);
+        if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == 2) {
+          // the whole accumulator is in registers: hand TMEM back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
             if (TWO_SM) mbar_arrive_cluster(&tempty_bar[acc], 0);
             else mbar_arrive(&tempty_bar[acc]);
-          }
-        }
-        const int n = tc.n0 + col;
-        if (row < rows && n < p.N) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int nn = n + u * 8;
-            if (nn < p.N) {
-              float v[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
-              if (brow) {
-                const float4 b0 = *reinterpret_cast<const float4*>(brow + nn);
-                const float4 b1 = *reinterpret_cast<const float4*>(brow + nn + 4);
-                v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-                v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
-              }
-              if (p.epi == SCMOE_EPI_BIAS_GELU) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
-              }
-              if (p.residual) {
-                Vec16<__nv_bfloat16> rv;
-                rv.raw = ld_nc_v4(p.residual + row_off + nn);
-                float rf[8];
-                rv.to_float(rf);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] += rf[i];
-              }
-              Vec16<__nv_bfloat16> o;
-              o.from_float(v);
-              st_v4(p.out + row_off + nn, o.raw);
-            }
           }
         }
       }
