@@ -32,16 +32,24 @@ def _reference_decision(gating_mod, dec, eps):
                                    dropped=d["dropped"], eps=eps)
 
 
-def install(arch_module=None, dtype: torch.dtype = torch.float32, device: str = "cuda"):
-    """Rebind arch.moe_shared / arch.moe_standard to GPU implementations."""
+def install(arch_module=None, dtype: torch.dtype = torch.float32, device: str = "cuda",
+            gating_module=None):
+    """Rebind arch.moe_shared / arch.moe_standard to GPU implementations.
+
+    `arch_module` / `gating_module` default to the reference's scmoelab.arch /
+    scmoelab.gating; any objects with the same attributes work (the tests use
+    the oracle's)."""
     if arch_module is None:
         from scmoelab import arch as arch_module  # the reference package
-    from scmoelab import gating as gating_mod
+    if gating_module is None:
+        from scmoelab import gating as gating_mod
+    else:
+        gating_mod = gating_module
     from .layers import MoEReplay, ScMoELayer, Top2MoELayer
 
-    if arch_module in _saved:
+    if id(arch_module) in _saved:
         return
-    _saved[arch_module] = (arch_module.moe_shared, arch_module.moe_standard)
+    _saved[id(arch_module)] = (arch_module.moe_shared, arch_module.moe_standard)
 
     def _prepare(x, layer, rng, replay):
         if _is_tape(x) or _is_tape(layer.gate.w_gate):
@@ -83,7 +91,8 @@ def install(arch_module=None, dtype: torch.dtype = torch.float32, device: str = 
 
 
 def uninstall(arch_module=None):
+    """Restore the reference implementations."""
     if arch_module is None:
         from scmoelab import arch as arch_module
-    if arch_module in _saved:
-        arch_module.moe_shared, arch_module.moe_standard = _saved.pop(arch_module)
+    if id(arch_module) in _saved:
+        arch_module.moe_shared, arch_module.moe_standard = _saved.pop(id(arch_module))

@@ -212,3 +212,38 @@ def test_full_size_cfg3_properties():
             expect = se[t].float() + y.bfloat16().float()
         err = (out[t].float() - expect).abs().max().item()
         assert err <= 2e-2 * (expect.abs().max().item() + 1e-3), (t, err)
+
+
+def test_compat_shim_rebinds_moe_entries():
+    """compat.install() swaps moe_shared / moe_standard of an arch-like module
+    (here the oracle stands in for scmoelab.arch, which does not travel to the
+    GPU box) and returns reference-shaped results."""
+    from types import SimpleNamespace as NS
+    from paper_2404_05019_b200 import compat
+
+    class Decision:  # gating.GateDecision constructor signature
+        def __init__(self, logits, indices, weights, dropped, eps=None):
+            self.logits, self.indices, self.weights, self.dropped, self.eps = \
+                logits, indices, weights, dropped, eps
+
+    arch = NS(moe_shared=O.moe_shared, moe_standard=O.moe_standard)
+    T, d, h, N, cf = 96, 32, 64, 4, 1.0
+    pp = O.init_pair(d, h, N, O.Rng(8).spawn(0), variant="scmoe", combine_mode="cg2")
+    x = O.Rng(8).spawn(1).normal((T, d))
+    src = O.Rng(8).spawn(2).normal((T, d))
+    compat.install(arch, dtype=torch.float32, gating_module=NS(GateDecision=Decision))
+    try:
+        cap = P.CapacityConfig(cf)
+        out, dec, aux = arch.moe_shared(x, pp.moe, cap, 1, routed_src=src)
+        assert isinstance(out, np.ndarray) and out.shape == (T, d) and aux.shape == (1, 1)
+        ref, _, _ = O.moe_shared(x, pp.moe, cf, 1, routed_src=src, pinned_indices=dec.indices,
+                                 pinned_dropped=dec.dropped)
+        _check(out, ref, 1e-4, "compat moe_shared")
+        pp2 = O.init_pair(d, h, N, O.Rng(9).spawn(0), variant="standard", k=2)
+        out2, dec2, _ = arch.moe_standard(x, pp2.moe, cap, 2)
+        ref2, _, _ = O.moe_standard(x, pp2.moe, cf, 2, pinned_indices=dec2.indices,
+                                    pinned_dropped=dec2.dropped)
+        _check(out2, ref2, 1e-4, "compat moe_standard")
+    finally:
+        compat.uninstall(arch)
+    assert arch.moe_shared is O.moe_shared
