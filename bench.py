@@ -288,18 +288,27 @@ def run_ours(args):
         ms_layer_t2, _ = timed(lambda r: t2.moe(x), args.steps, ws)
 
         # ---- end to end through the public API, host buffers -----------------
+        # every step copies its input from pinned host memory and its output
+        # back; HostStreamRunner overlaps step i's compute with the H2D of
+        # step i+1 and the D2H of step i-1 (two copy engines, full duplex PCIe)
+        from paper_2404_05019_b200.runtime import HostStreamRunner
         h_host = torch.empty(T, d, dtype=dtype, pin_memory=True)
         h_host.copy_(x.cpu())
-        o_host = torch.empty(T, d, dtype=dtype, pin_memory=True)
+        o_host = [torch.empty(T, d, dtype=dtype, pin_memory=True) for _ in range(2)]
         e2e_ms = None
         if not args.no_e2e:
-            def e2e_step(_r):
-                xd = h_host.to("cuda", non_blocking=True)
-                out = sc(xd)[0]
-                o_host.copy_(out, non_blocking=True)
-            for _ in range(2):
-                e2e_step(None)
-            e2e_ms, _ = timed(e2e_step, args.steps, ws)
+            runner = HostStreamRunner(lambda xd: sc(xd))
+            runner.run([h_host] * 3, [o_host[i % 2] for i in range(3)])
+            torch.cuda.synchronize()
+            barrier(ws)
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            runner.run([h_host] * args.steps, [o_host[i % 2] for i in range(args.steps)])
+            e1.record(st)
+            torch.cuda.synchronize()
+            barrier(ws)
+            e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
 
     # spans -> per-op durations, overlap, dominant-kernel roofline
     spans = [r.spans() for r in recs]
@@ -362,7 +371,8 @@ def run_ours(args):
     if e2e_ms is not None:
         line["e2e"] = {"value": ws * T / (e2e_ms * 1e-3), "unit": "tokens/s",
                        "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
-                       "ms_per_step": e2e_ms}
+                       "ms_per_step": e2e_ms, "api": "runtime.HostStreamRunner(ScMoEBlockPair)",
+                       "copies": "pinned host, H2D/D2H overlapped with neighbouring steps"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         times, cores, blas = cpu_reference_time(w, args.cpu_tokens, args.cpu_reps)
         v = args.cpu_tokens / (sum(times) / len(times))

@@ -247,3 +247,17 @@ def test_compat_shim_rebinds_moe_entries():
     finally:
         compat.uninstall(arch)
     assert arch.moe_shared is O.moe_shared
+
+
+def test_host_stream_runner_matches_direct_forward():
+    from paper_2404_05019_b200.runtime import HostStreamRunner
+    T, d, h, N = 512, 128, 256, 4
+    blk = P.ScMoEBlockPair(d, h, N, variant="scmoe", shortcut_pos="pos2", n_heads=2, seq_len=128,
+                           dtype=torch.bfloat16,
+                           generator=torch.Generator(device="cuda").manual_seed(4))
+    xs = [torch.randn(T, d).bfloat16().pin_memory() for _ in range(5)]
+    outs = [torch.empty(T, d, dtype=torch.bfloat16).pin_memory() for _ in range(5)]
+    HostStreamRunner(lambda x: blk(x)).run(xs, outs)
+    torch.cuda.synchronize()
+    for x, o in zip(xs, outs):
+        assert torch.equal(o, blk(x.cuda())[0].cpu())
