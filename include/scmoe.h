@@ -40,9 +40,14 @@ extern "C" {
 #define SCMOE_COMBINE_CG1 1
 #define SCMOE_COMBINE_CG2 2
 
-/* GEMM epilogues of expert_forward, arch.py:349-351 */
+/* GEMM epilogues: expert_forward (arch.py:349-351) and its backward */
 #define SCMOE_EPI_BIAS 0
 #define SCMOE_EPI_BIAS_GELU 1
+#define SCMOE_EPI_GELU_BWD 2     /* out = acc * gelu'(aux_in)  (tape.py:137-142) */
+
+/* weight operand layouts of scmoe_grouped_gemm_ex */
+#define SCMOE_W_NK 0             /* (W, n_out, k_in): the stored K-major weights */
+#define SCMOE_W_KN 1             /* (W, k_in, n_out): stored weights used transposed (dgrad) */
 
 #define SCMOE_MAX_EXPERTS 64
 #define SCMOE_MAX_K 8
@@ -90,6 +95,13 @@ int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens, int d
                    int k, const int32_t* indices, const int32_t* slots, int capacity,
                    void* dispatch_buf, void* stream);
 
+/* K7 — combine backward: like scmoe_dispatch with every copied row scaled by
+ * row_scale[t, j] (fp32, (T, k)): d expert_out[e, slot] = w[t, j] * d_out[t]
+ * (the VJP of routed = sum_j w_j E_{e_j}, arch.py:418-433). */
+int scmoe_dispatch_scaled(const void* x, int dtype, long long ld_x, int n_tokens, int d_model,
+                          int k, const int32_t* indices, const int32_t* slots, int capacity,
+                          const float* row_scale, void* dispatch_buf, void* stream);
+
 /*
  * K3 / K4 / K8 — one grouped GEMM of expert_forward (arch.py:349-351):
  *   out[g, r, :] = epi( a[g, r, :] . wt[g % n_wgroups, :, :]^T + bias[g % n_wgroups, :] )
@@ -107,6 +119,47 @@ int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bi
                        int num_groups, int n_wgroups, int group_cap,
                        const int32_t* group_rows, int rows_clip,
                        int n_out, int k_in, int epilogue, void* stream);
+
+/*
+ * K3 / K7 — general form of scmoe_grouped_gemm (bf16):
+ *   out[g, r, :] = epi( a[g, r, :] . Wg + bias )  (+ residual), r < rows(g)
+ * with Wg = w[g % W]^T for w_layout SCMOE_W_NK (w is (W, n_out, k_in)) or
+ * Wg = w[g % W] for SCMOE_W_KN (w is (W, k_in, n_out)), i.e. the same stored
+ * weights read transposed for the data gradient.  Epilogues:
+ *   SCMOE_EPI_BIAS / SCMOE_EPI_BIAS_GELU (aux_out, if not NULL, receives the
+ *   pre-activation acc + bias as bf16), SCMOE_EPI_GELU_BWD (out = acc *
+ *   gelu'(aux_in), aux_in laid out like out).
+ * zero_tail != 0 writes zeros to rows [rows(g), min(cap, tile end)) — the
+ * padding the weight-gradient GEMM relies on.
+ */
+int scmoe_grouped_gemm_ex(const void* a, int dtype, const void* w, int w_layout,
+                          const float* bias, const void* residual, const void* aux_in,
+                          void* aux_out, void* out, int num_groups, int n_wgroups,
+                          int group_cap, const int32_t* group_rows, int rows_clip,
+                          int n_out, int k_in, int epilogue, int zero_tail, void* stream);
+
+/*
+ * K7 — grouped weight gradient (tape.mm VJP, tape.py:121-127):
+ *   out[w] (m_out, n_out) fp32 = sum_{g = w mod W} sum_{r < rows(g)} a[g, r, :m_out]^T b[g, r, :n_out]
+ * a is (num_groups, group_cap, m_out), b is (num_groups, group_cap, n_out),
+ * bf16.  Rows [rows(g), roundup(rows(g), 64)) of a and b must be zero (the
+ * producers' zero_tail / scmoe_zero_tails guarantee it).  splits <= 0 picks a
+ * split-K factor that fills the GPU; splits > 1 needs
+ * scmoe_grouped_wgrad_workspace_bytes() of workspace.
+ */
+size_t scmoe_grouped_wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out, int splits);
+int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out, void* workspace,
+                        size_t workspace_bytes, int num_groups, int n_wgroups, int group_cap,
+                        const int32_t* group_rows, int rows_clip, int m_out, int n_out,
+                        int splits, void* stream);
+
+/* rows [rows(g), min(cap, roundup(rows(g), align))) of every group set to 0 */
+int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_cap, int cols,
+                     const int32_t* group_rows, int rows_clip, int align, void* stream);
+
+/* out[g, c] = sum_{r < rows(g)} x[g, r, c] in fp32 (bias gradients) */
+int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap, int cols,
+                         const int32_t* group_rows, int rows_clip, float* out, void* stream);
 
 /* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */

@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libscmoe.so")
 SCMOE_OK, SCMOE_ERR_ARG, SCMOE_ERR_CUDA, SCMOE_ERR_UNSUPPORTED = 0, 1, 2, 3
 SCMOE_F32, SCMOE_BF16 = 0, 1
 COMBINE_MODES = {"direct_add": 0, "cg1": 1, "cg2": 2}
-EPI_BIAS, EPI_BIAS_GELU = 0, 1
+EPI_BIAS, EPI_BIAS_GELU, EPI_GELU_BWD = 0, 1, 2
+W_NK, W_KN = 0, 1
 MAX_EXPERTS, MAX_K = 64, 8
 
 _vp, _i, _ll, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_size_t
@@ -36,6 +37,14 @@ SIGNATURES = [
     ("scmoe_grouped_gemm", _i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i,
                                 _vp]),
     ("scmoe_set_gemm_mode", _i, [_i]),
+    ("scmoe_grouped_gemm_ex", _i, [_vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
+                                   _i, _i, _i, _i, _i, _vp]),
+    ("scmoe_grouped_wgrad_workspace_bytes", _sz, [_i, _i, _i, _i]),
+    ("scmoe_grouped_wgrad", _i, [_vp, _vp, _i, _vp, _vp, _sz, _i, _i, _i, _vp, _i, _i, _i, _i,
+                                 _vp]),
+    ("scmoe_zero_tails", _i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _vp]),
+    ("scmoe_grouped_colsum", _i, [_vp, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
+    ("scmoe_dispatch_scaled", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
     ("scmoe_expert_ffn", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i,
                               _i, _i, _vp]),
     ("scmoe_combine", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,

@@ -1,4 +1,5 @@
-// C ABI glue: error reporting, device checks and the GEMM / FFN entries.
+// C ABI glue: error reporting, device checks, the GEMM / FFN entries and the
+// small training helpers (tail zeroing, grouped column sums).
 #include <stdarg.h>
 #include <stdio.h>
 
@@ -26,65 +27,184 @@ int num_sms() {
   return n;
 }
 
-int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, const void* residual,
-                      void* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                      int rows_clip, int N, int K, int epi, cudaStream_t st);
+int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias,
+                      const void* residual, const void* aux_in, void* aux_out, void* out,
+                      int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st);
 int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const float* residual,
                      float* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st);
+size_t wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out, int splits);
+int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_t ws_bytes,
+                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st);
 
+namespace {
+
+// rows [rows(g), min(cap, roundup(rows(g), align))) of group g set to zero
+__global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs,
+                                  const int32_t* __restrict__ group_rows, int rows_clip,
+                                  int align) {
+  const int g = blockIdx.y;
+  const int r0 = group_rows ? min(group_rows[g], rows_clip) : cap;
+  const int r1 = min(cap, ((r0 + align - 1) / align) * align);
+  const long long n = (long long)(r1 - r0) * row_vecs;
+  uint4* base = buf + ((long long)g * cap + r0) * row_vecs;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    base[i] = make_uint4(0, 0, 0, 0);
+}
+
+// out[g, c] = sum_{r < rows(g)} x[g, r, c]  (fp32), bf16 or fp32 input
+template <typename T>
+__global__ void grouped_colsum_kernel(const T* __restrict__ x, int cap, int cols,
+                                      const int32_t* __restrict__ group_rows, int rows_clip,
+                                      float* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int rows = group_rows ? min(group_rows[g], rows_clip) : cap;
+  const T* p = x + (long long)g * cap * cols + c;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int r = 0;
+  for (; r + 4 <= rows; r += 4) {
+    s0 += to_f32(p[(long long)r * cols]);
+    s1 += to_f32(p[(long long)(r + 1) * cols]);
+    s2 += to_f32(p[(long long)(r + 2) * cols]);
+    s3 += to_f32(p[(long long)(r + 3) * cols]);
+  }
+  for (; r < rows; ++r) s0 += to_f32(p[(long long)r * cols]);
+  out[(long long)g * cols + c] = (s0 + s1) + (s2 + s3);
+}
+
+}  // namespace
 }  // namespace scmoe
 
-extern "C" int scmoe_version(void) { return 1; }
+using namespace scmoe;
 
-extern "C" const char* scmoe_last_error(void) { return scmoe::g_err; }
+extern "C" int scmoe_version(void) { return 2; }
+
+extern "C" const char* scmoe_last_error(void) { return g_err; }
 
 extern "C" int scmoe_device_check(int device) {
   int major = 0, minor = 0;
   cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
   if (e != cudaSuccess) {
-    scmoe::set_error("no CUDA device %d: %s", device, cudaGetErrorString(e));
+    set_error("no CUDA device %d: %s", device, cudaGetErrorString(e));
     return SCMOE_ERR_UNSUPPORTED;
   }
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
   if (major != 10 || minor != 0) {
-    scmoe::set_error("libscmoe is built for sm_100a; device %d is sm_%d%d", device, major, minor);
+    set_error("libscmoe is built for sm_100a; device %d is sm_%d%d", device, major, minor);
     return SCMOE_ERR_UNSUPPORTED;
   }
   return SCMOE_OK;
 }
 
-extern "C" int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias,
-                                  const void* residual, void* out, int num_groups, int n_wgroups, int group_cap,
-                                  const int32_t* group_rows, int rows_clip, int n_out, int k_in,
-                                  int epilogue, void* stream) {
-  using namespace scmoe;
+extern "C" int scmoe_grouped_gemm_ex(const void* a, int dtype, const void* w, int w_layout,
+                                     const float* bias, const void* residual, const void* aux_in,
+                                     void* aux_out, void* out, int num_groups, int n_wgroups,
+                                     int group_cap, const int32_t* group_rows, int rows_clip,
+                                     int n_out, int k_in, int epilogue, int zero_tail,
+                                     void* stream) {
   SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
   SCMOE_CHECK_ARG(num_groups >= 1 && n_wgroups >= 1, "num_groups/n_wgroups must be >= 1");
   SCMOE_CHECK_ARG(group_cap >= 0 && n_out >= 1 && k_in >= 1, "bad GEMM shape");
-  SCMOE_CHECK_ARG(epilogue == SCMOE_EPI_BIAS || epilogue == SCMOE_EPI_BIAS_GELU,
-                  "bad epilogue %d", epilogue);
+  SCMOE_CHECK_ARG(epilogue >= SCMOE_EPI_BIAS && epilogue <= SCMOE_EPI_GELU_BWD, "bad epilogue %d",
+                  epilogue);
+  SCMOE_CHECK_ARG(w_layout == SCMOE_W_NK || w_layout == SCMOE_W_KN, "bad weight layout %d",
+                  w_layout);
   if (group_cap == 0) return SCMOE_OK;
   if (rows_clip <= 0) rows_clip = group_cap;
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == SCMOE_BF16)
-    return grouped_gemm_bf16(a, wt, bias, residual, out, num_groups, n_wgroups, group_cap, group_rows,
-                             rows_clip, n_out, k_in, epilogue, st);
-  return grouped_gemm_f32((const float*)a, (const float*)wt, bias, (const float*)residual,
-                          (float*)out, num_groups,
-                          n_wgroups, group_cap, group_rows, rows_clip, n_out, k_in, epilogue, st);
+    return grouped_gemm_bf16(a, w, w_layout == SCMOE_W_KN, bias, residual, aux_in, aux_out, out,
+                             num_groups, n_wgroups, group_cap, group_rows, rows_clip, n_out, k_in,
+                             epilogue, zero_tail, st);
+  SCMOE_CHECK_ARG(w_layout == SCMOE_W_NK && epilogue != SCMOE_EPI_GELU_BWD && !aux_out &&
+                      !zero_tail,
+                  "the fp32 parity GEMM supports the forward epilogues only");
+  return grouped_gemm_f32((const float*)a, (const float*)w, bias, (const float*)residual,
+                          (float*)out, num_groups, n_wgroups, group_cap, group_rows, rows_clip,
+                          n_out, k_in, epilogue, st);
+}
+
+extern "C" int scmoe_grouped_gemm(const void* a, int dtype, const void* wt, const float* bias,
+                                  const void* residual, void* out, int num_groups, int n_wgroups,
+                                  int group_cap, const int32_t* group_rows, int rows_clip,
+                                  int n_out, int k_in, int epilogue, void* stream) {
+  SCMOE_CHECK_ARG(epilogue == SCMOE_EPI_BIAS || epilogue == SCMOE_EPI_BIAS_GELU,
+                  "bad epilogue %d", epilogue);
+  return scmoe_grouped_gemm_ex(a, dtype, wt, SCMOE_W_NK, bias, residual, nullptr, nullptr, out,
+                               num_groups, n_wgroups, group_cap, group_rows, rows_clip, n_out,
+                               k_in, epilogue, 0, stream);
 }
 
 extern "C" int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const float* b1,
                                 const void* w2t, const float* b2, const void* residual,
-                                void* hidden, void* out,
-                                int num_groups, int n_wgroups, int group_cap,
-                                const int32_t* group_rows, int rows_clip, int d_model,
-                                int d_hidden, void* stream) {
-  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, num_groups, n_wgroups, group_cap,
-                              group_rows, rows_clip, d_hidden, d_model, SCMOE_EPI_BIAS_GELU,
-                              stream);
+                                void* hidden, void* out, int num_groups, int n_wgroups,
+                                int group_cap, const int32_t* group_rows, int rows_clip,
+                                int d_model, int d_hidden, void* stream) {
+  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, num_groups, n_wgroups,
+                              group_cap, group_rows, rows_clip, d_hidden, d_model,
+                              SCMOE_EPI_BIAS_GELU, stream);
   if (rc) return rc;
-  return scmoe_grouped_gemm(hidden, dtype, w2t, b2, residual, out, num_groups, n_wgroups, group_cap,
-                            group_rows, rows_clip, d_model, d_hidden, SCMOE_EPI_BIAS, stream);
+  return scmoe_grouped_gemm(hidden, dtype, w2t, b2, residual, out, num_groups, n_wgroups,
+                            group_cap, group_rows, rows_clip, d_model, d_hidden, SCMOE_EPI_BIAS,
+                            stream);
+}
+
+extern "C" size_t scmoe_grouped_wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out,
+                                                      int splits) {
+  if (splits <= 0) splits = 64;  // the automatic choice never exceeds 64
+  return wgrad_workspace_bytes(n_wgroups, m_out, n_out, splits);
+}
+
+extern "C" int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out,
+                                   void* workspace, size_t workspace_bytes, int num_groups,
+                                   int n_wgroups, int group_cap, const int32_t* group_rows,
+                                   int rows_clip, int m_out, int n_out, int splits, void* stream) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_BF16, "wgrad runs on bf16 operands");
+  SCMOE_CHECK_ARG(num_groups >= 1 && n_wgroups >= 1 && num_groups % n_wgroups == 0,
+                  "num_groups must be a positive multiple of n_wgroups");
+  SCMOE_CHECK_ARG(group_cap >= 1 && m_out >= 1 && n_out >= 1, "bad wgrad shape");
+  if (rows_clip <= 0) rows_clip = group_cap;
+  return grouped_wgrad_bf16(a, b, out, workspace, workspace_bytes, num_groups, n_wgroups,
+                            group_cap, group_rows, rows_clip, m_out, n_out, splits,
+                            (cudaStream_t)stream);
+}
+
+extern "C" int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_cap, int cols,
+                                const int32_t* group_rows, int rows_clip, int align,
+                                void* stream) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
+  const int esz = dtype == SCMOE_BF16 ? 2 : 4;
+  SCMOE_CHECK_ARG((cols * esz) % 16 == 0 && ((uintptr_t)buf & 15) == 0,
+                  "rows must be 16-byte multiples and aligned");
+  SCMOE_CHECK_ARG(align >= 1 && num_groups >= 1, "bad zero_tails arguments");
+  if (group_cap <= 0 || !group_rows) return SCMOE_OK;
+  if (rows_clip <= 0) rows_clip = group_cap;
+  dim3 grid(32, num_groups);
+  zero_tails_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((uint4*)buf, group_cap,
+                                                            cols * esz / 16, group_rows,
+                                                            rows_clip, align);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap,
+                                    int cols, const int32_t* group_rows, int rows_clip,
+                                    float* out, void* stream) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
+  SCMOE_CHECK_ARG(num_groups >= 1 && cols >= 1, "bad colsum shape");
+  if (rows_clip <= 0) rows_clip = group_cap;
+  dim3 grid((cols + 127) / 128, num_groups);
+  if (dtype == SCMOE_BF16)
+    grouped_colsum_kernel<__nv_bfloat16><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, out);
+  else
+    grouped_colsum_kernel<float><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        (const float*)x, group_cap, cols, group_rows, rows_clip, out);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
 }

@@ -133,6 +133,20 @@ __device__ __forceinline__ float gelu_erf_fast(float x) {
   return fmaf(hx, copysignf(erf_abs, x), hx);
 }
 
+// d/dz gelu(z) = Phi(z) + z * phi(z), same erf approximation (shares exp(-z^2/2))
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  const float z = fabsf(x) * 0.70710678118654752440f;
+  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float e = ex2_approx((z * z) * -1.44269504088896340736f);  // exp(-x^2/2)
+  const float erf_v = copysignf(fmaf(-p, e, 1.0f), x);
+  return fmaf(0.5f, erf_v, 0.5f) + x * e * 0.39894228040143267794f;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

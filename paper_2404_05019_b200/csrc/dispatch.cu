@@ -20,18 +20,23 @@ template <typename T>
 __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
     const T* __restrict__ x, long long ld_x, int n_tok, int d, int k,
     const int32_t* __restrict__ indices, const int32_t* __restrict__ slots, int cap,
-    T* __restrict__ buf) {
+    const float* __restrict__ row_scale, T* __restrict__ buf) {
   constexpr int VEC = Vec16<T>::N;
   const int lane = threadIdx.x & 31;
   const long long t = (long long)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (t >= n_tok) return;
   long long dst[SCMOE_MAX_K];
+  float scl[SCMOE_MAX_K];
   int nd = 0;
 #pragma unroll
   for (int j = 0; j < SCMOE_MAX_K; ++j) {
     if (j < k) {
       const int s = slots[t * k + j];
-      if (s < cap) dst[nd++] = ((long long)indices[t * k + j] * cap + s) * d;
+      if (s < cap) {
+        dst[nd] = ((long long)indices[t * k + j] * cap + s) * d;
+        scl[nd] = row_scale ? row_scale[t * k + j] : 1.f;
+        ++nd;
+      }
     }
   }
   if (nd == 0) return;
@@ -48,7 +53,21 @@ __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
     for (int u = 0; u < 4; ++u) {
       const int cc = c + u * 32 * VEC;
       if (cc < d) {
-        for (int q = 0; q < nd; ++q) st_v4(buf + dst[q] + cc, v[u]);
+        for (int q = 0; q < nd; ++q) {
+          if (row_scale) {
+            // combine backward: d expert_out[e, slot] = w * d_out[t]
+            Vec16<T> iv, ov;
+            iv.raw = v[u];
+            float f[VEC];
+            iv.to_float(f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) f[i] *= scl[q];
+            ov.from_float(f);
+            st_v4(buf + dst[q] + cc, ov.raw);
+          } else {
+            st_v4(buf + dst[q] + cc, v[u]);
+          }
+        }
       }
     }
   }
@@ -178,9 +197,10 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 }  // namespace
 }  // namespace scmoe
 
-extern "C" int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens,
-                              int d_model, int k, const int32_t* indices, const int32_t* slots,
-                              int capacity, void* dispatch_buf, void* stream) {
+extern "C" int scmoe_dispatch_scaled(const void* x, int dtype, long long ld_x, int n_tokens,
+                                     int d_model, int k, const int32_t* indices,
+                                     const int32_t* slots, int capacity, const float* row_scale,
+                                     void* dispatch_buf, void* stream) {
   using namespace scmoe;
   SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
   SCMOE_CHECK_ARG(k >= 1 && k <= SCMOE_MAX_K, "k=%d out of range", k);
@@ -193,14 +213,21 @@ extern "C" int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_to
   const int grid = (n_tokens + WARPS - 1) / WARPS;
   if (dtype == SCMOE_BF16)
     dispatch_kernel<__nv_bfloat16><<<grid, WARPS * 32, 0, st>>>(
-        (const __nv_bfloat16*)x, ld_x, n_tokens, d_model, k, indices, slots, capacity,
+        (const __nv_bfloat16*)x, ld_x, n_tokens, d_model, k, indices, slots, capacity, row_scale,
         (__nv_bfloat16*)dispatch_buf);
   else
     dispatch_kernel<float><<<grid, WARPS * 32, 0, st>>>((const float*)x, ld_x, n_tokens, d_model, k,
-                                                        indices, slots, capacity,
+                                                        indices, slots, capacity, row_scale,
                                                         (float*)dispatch_buf);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
+}
+
+extern "C" int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens,
+                              int d_model, int k, const int32_t* indices, const int32_t* slots,
+                              int capacity, void* dispatch_buf, void* stream) {
+  return scmoe_dispatch_scaled(x, dtype, ld_x, n_tokens, d_model, k, indices, slots, capacity,
+                               nullptr, dispatch_buf, stream);
 }
 
 extern "C" int scmoe_combine(const void* se_out, const void* expert_out, const void* x_cur,

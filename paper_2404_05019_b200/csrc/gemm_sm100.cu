@@ -1,30 +1,35 @@
-// K3 / K4 — grouped bf16 GEMM on 5th-generation tensor cores (tcgen05).
+// K3 / K4 / K7 — grouped bf16 GEMMs on 5th-generation tensor cores (tcgen05).
 //
-//   out[g, r, :] = epi( a[g, r, :] . wt[g % n_wgroups, :, :]^T + bias (+ residual[g, r, :]) )
+// Forward / dgrad ("rows" mode):
+//   out[g, r, :] = epi( a[g, r, :] . B(g % W)^T ) for r < rows(g)
+// with rows(g) = min(group_rows[g], rows_clip).  B is read K-major from
+// (W, n_out, k_in) weights (forward), or MN-major from (W, k_in, n_out) — the
+// same stored weights used transposed (dgrad, K7).  Epilogues: expert_forward's
+// bias (+ exact-erf GELU, optionally storing the pre-activation) (arch.py:349-351),
+// the GELU backward dZ = acc * gelu'(z), an optional fused residual add
+// (arch.py:542, 587-588) and zero padding of rows past rows(g) ("zero_tail").
+// The routed experts read the capacity-slotted dispatch buffer (group =
+// expert, rows = kept tokens known only on the device); dense layers are one
+// group.
 //
-// for r < rows(g) = min(group_rows[g], rows_clip): the routed experts read the
-// capacity-slotted dispatch buffer (group = expert, rows = kept tokens, known
-// only on the device), the shared expert / Block-MLP is a single group.  The
-// epilogue is expert_forward's bias (+ exact-erf GELU) (arch.py:349-351),
-// optionally fused with the block's residual add (arch.py:542, 587-588).
+// Weight gradient ("wgrad" mode, K7):
+//   out[w] = sum_{g = w mod W} sum_{r < rows(g)} a[g, r, :]^T (x) b[g, r, :]
+// both operands MN-major (the token dimension is the reduction), split-K over
+// the concatenated k-blocks of the groups feeding weight group w, fp32
+// partials reduced by a second kernel.
 //
 // Structure (persistent, 384 threads per CTA, one CTA per SM):
-//   warp 0      TMA producer: 128B-swizzled A / B tiles into a shared-memory
-//               ring (full / empty mbarriers)
-//   warp 1      MMA issuer: one thread issues tcgen05.mma kind::f16, fp32
-//               accumulators in TMEM; tcgen05.commit frees ring stages and
-//               signals the epilogue
+//   warp 0      TMA producer: 128B-swizzled tiles into a shared-memory ring
+//   warp 1      MMA issuer: one thread issues tcgen05.mma kind::f16 (fp32 TMEM
+//               accumulators); tcgen05.commit frees ring stages / signals the
+//               epilogue
 //   warp 2      TMEM allocator (512 columns = two 256-column accumulators)
-//   warps 4-11  epilogue: tcgen05.ld 32x32b -> bias / GELU / residual -> bf16
-//               -> global, double-buffered against the next tile's MMAs
-// Two variants:
-//   1SM  tile 128x256, cta_group::1, 4 stages of 48 KB
-//   2SM  tile 256x256 per CTA pair (cluster of 2), cta_group::2: each CTA
-//        loads its 128 rows of A and half of B (128 rows), the leader issues
-//        M=256 MMAs that read both CTAs' shared memory and write both TMEMs;
-//        6 stages of 32 KB per CTA
-// Tiles are walked in (group, m-tile, n-tile) order with n fastest, skipping
-// m-tiles past each group's device-side row count.
+//   warps 4-11  epilogue: tcgen05.ld 32x32b (next chunk in flight) -> math ->
+//               global, double-buffered against the next tile's MMAs
+// Two shapes: 1SM 128x256 tile (cta_group::1, 4 stages x 48 KB) and 2SM 256x256
+// per CTA pair (cluster of 2, cta_group::2: each CTA loads its half of A and of
+// B, the leader's M=256 MMAs read both CTAs' smem and write both TMEMs; 6
+// stages x 32 KB).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -39,6 +44,8 @@ constexpr int THREADS = 128 + EPI_WARPS * 32;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = ACC_STAGES * BN;
 constexpr int MAX_GROUPS = 1024;
+constexpr int MN_BOX = 64;                       // MN-major TMA box: 64 (mn) x 64 (k)
+constexpr int MN_BOX_BYTES = MN_BOX * BK * 2;    // 8 KB
 
 template <bool TWO_SM>
 struct Cfg {
@@ -50,18 +57,29 @@ struct Cfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256 + (MAX_GROUPS + 1) * 4;
-  // instruction descriptor: D fp32, A/B bf16, K-major, M=TILE_M, N=256
-  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
-                                    ((uint32_t)(BN >> 3) << 17) |
-                                    ((uint32_t)(TILE_M >> 4) << 24);
 };
 
+// instruction descriptor: D fp32, A/B bf16, M = TILE_M, N = 256, operand majors
+template <bool TWO_SM, bool A_MN, bool B_MN>
+struct Idesc {
+  static constexpr uint32_t value = (1u << 4) | (1u << 7) | (1u << 10) |
+                                    ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+                                    ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(Cfg<TWO_SM>::TILE_M >> 4) << 24);
+};
+
+enum Epi { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GELU_BWD = 2 };
+
 struct Params {
-  int num_groups, n_wgroups, cap, rows_clip, N, K, epi;
+  int num_groups, n_wgroups, cap, rows_clip, N, K, epi, zero_tail;
+  int m_out, splits;                       // wgrad only
   const int32_t* group_rows;
   const float* bias;
   const __nv_bfloat16* residual;
+  const __nv_bfloat16* aux_in;             // GELU backward: pre-activation z
+  __nv_bfloat16* aux_out;                  // forward: store the pre-activation
   __nv_bfloat16* out;
+  float* out_f32;                          // wgrad partials [splits][W][m_out][N]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -105,24 +123,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// TMA tile load; in 2-SM mode the bytes land in this CTA's shared memory and
+// completion is counted on the leader CTA's barrier (peer bit cleared).
+template <bool TWO_SM>
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+  if (TWO_SM) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+        "r"(c2)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
 }
-// 2-SM TMA: bytes land in this CTA's shared memory, completion is counted on
-// the leader CTA's barrier (peer bit cleared in the cluster address).
-__device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                                int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
-      "r"(c2)
-      : "memory");
+// One operand tile of `ROWS` (M or N) x 64 (K): K-major = one box (64 k, ROWS),
+// MN-major = ROWS/64 boxes of (64 mn, 64 k), 8 KB apart.
+template <bool TWO_SM, bool MN, int ROWS>
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, uint64_t* bar, uint8_t* dst,
+                                             int k0, int mn0, int g) {
+  if (MN) {
+#pragma unroll
+    for (int i = 0; i < ROWS / MN_BOX; ++i)
+      tma_load_3d<TWO_SM>(map, bar, dst + i * MN_BOX_BYTES, mn0 + i * MN_BOX, k0, g);
+  } else {
+    tma_load_3d<TWO_SM>(map, bar, dst, k0, mn0, g);
+  }
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -147,26 +179,34 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }
 template <bool TWO_SM>
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t accumulate) {
+                                       uint32_t idesc, uint32_t accumulate) {
   if (TWO_SM) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(Cfg<true>::IDESC), "r"(accumulate));
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   } else {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(Cfg<false>::IDESC), "r"(accumulate));
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   }
 }
-// K-major operand, 128-byte swizzle: rows of 64 bf16 (128 B), 8-row groups
-// 1024 B apart (SBO), version 1 (sm_100), layout type 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// Shared-memory matrix descriptors, 128-byte swizzle, sm_100 version bits.
+// K-major: rows of 64 bf16 (128 B) along K, 8-row groups 1024 B apart (SBO).
+// MN-major: rows of 64 bf16 along MN, one per k; 8-k groups 1024 B apart (SBO),
+// 64-element MN blocks one TMA box (8 KB) apart (LBO).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kk) {
+  // advance by one UMMA K-step (16 bf16): 32 B inside a K-major row, 16 rows
+  // of 128 B in an MN-major tile
+  return MN ? sw128_desc(base + kk * 16 * 128, MN_BOX_BYTES) : sw128_desc(base + kk * 32, 16);
 }
 
 #define SCMOE_TMEM_LD32(taddr, r)                                                              \
@@ -181,41 +221,81 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
         "=r"(r[31])                                                                            \
       : "r"(taddr))
 
-struct TileCoord {
-  int g, m0, n0;
-};
-
-template <int TILE_M>
-__device__ __forceinline__ TileCoord decode_tile(int t, int n_tiles_n, const int* prefix,
-                                                 int num_groups) {
-  const int mlin = t / n_tiles_n;
-  const int nt = t - mlin * n_tiles_n;
-  int lo = 0, hi = num_groups - 1;  // largest g with prefix[g] <= mlin
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (prefix[mid] <= mlin) lo = mid;
-    else hi = mid - 1;
-  }
-  TileCoord c;
-  c.g = lo;
-  c.m0 = (mlin - prefix[lo]) * TILE_M;
-  c.n0 = nt * BN;
-  return c;
-}
-
 __device__ __forceinline__ int group_rows_of(const Params& p, int g) {
   return p.group_rows ? min(__ldg(p.group_rows + g), p.rows_clip) : p.cap;
 }
 
-// bias (+GELU) (+residual) -> bf16 for 32 consecutive columns of one row
+// One output tile: (group or weight group, row offset, column offset) and,
+// in wgrad mode, the split's k-block range.
+struct Tile {
+  int g, m0, n0, s, kb_lo, kb_hi;
+};
+
+template <int TILE_M, bool WGRAD>
+__device__ __forceinline__ Tile decode_tile(const Params& p, int t, int n_tiles_n,
+                                            const int* prefix) {
+  Tile c;
+  const int nt = t % n_tiles_n;
+  int r = t / n_tiles_n;
+  c.n0 = nt * BN;
+  if (WGRAD) {
+    const int m_tiles = (p.m_out + TILE_M - 1) / TILE_M;
+    c.m0 = (r % m_tiles) * TILE_M;
+    r /= m_tiles;
+    c.g = r % p.n_wgroups;                     // weight group
+    c.s = r / p.n_wgroups;                     // split
+    const int tot = prefix[c.g];               // k-blocks feeding weight group g
+    c.kb_lo = (int)((long long)c.s * tot / p.splits);
+    c.kb_hi = (int)((long long)(c.s + 1) * tot / p.splits);
+  } else {
+    int lo = 0, hi = p.num_groups - 1;         // largest g with prefix[g] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= r) lo = mid;
+      else hi = mid - 1;
+    }
+    c.g = lo;
+    c.m0 = (r - prefix[lo]) * TILE_M;
+    c.s = 0;
+    c.kb_lo = 0;
+    c.kb_hi = (p.K + BK - 1) / BK;
+  }
+  return c;
+}
+
+// Walk the k-blocks of a tile: in rows mode kb over K for group tc.g; in wgrad
+// mode the concatenation over source groups g = w, w+W, ... of
+// ceil(rows(g)/64) blocks each, restricted to [kb_lo, kb_hi).
+template <bool WGRAD, typename F>
+__device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc, F&& body) {
+  if (!WGRAD) {
+    for (int kb = tc.kb_lo; kb < tc.kb_hi; ++kb) body(tc.g, kb);
+    return;
+  }
+  int c = 0;
+  for (int g = tc.g; g < p.num_groups && c < tc.kb_hi; g += p.n_wgroups) {
+    const int nkb = (group_rows_of(p, g) + BK - 1) / BK;
+    const int a = max(0, tc.kb_lo - c), b = min(nkb, tc.kb_hi - c);
+    for (int kb = a; kb < b; ++kb) body(g, kb);
+    c += nkb;
+  }
+}
+
+// bias / GELU / GELU-backward / residual -> bf16 for 32 columns of one row,
+// or zeros for padding rows
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
-                                               bool row_ok, long long row_off, int n,
-                                               const float* brow) {
-  if (!row_ok || n >= p.N) return;
+                                               bool row_ok, bool pad_row, long long row_off,
+                                               int n, const float* brow) {
+  if (n >= p.N || !(row_ok || pad_row)) return;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int nn = n + u * 8;
     if (nn < p.N) {
+      if (!row_ok) {
+        st_v4(p.out + row_off + nn, make_uint4(0, 0, 0, 0));
+        if (p.aux_out) st_v4(p.aux_out + row_off + nn, make_uint4(0, 0, 0, 0));
+        continue;
+      }
       float v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
@@ -225,9 +305,21 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
         v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
         v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
       }
-      if (p.epi == SCMOE_EPI_BIAS_GELU) {
+      if (p.epi == EPI_BIAS_GELU) {
+        if (p.aux_out) {
+          Vec16<__nv_bfloat16> z;
+          z.from_float(v);
+          st_v4(p.aux_out + row_off + nn, z.raw);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
+      } else if (p.epi == EPI_GELU_BWD) {
+        Vec16<__nv_bfloat16> zv;
+        zv.raw = ld_nc_v4(p.aux_in + row_off + nn);
+        float z[8];
+        zv.to_float(z);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(z[i]);
       }
       if (p.residual) {
         Vec16<__nv_bfloat16> rv;
@@ -244,11 +336,29 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
   }
 }
 
-template <bool TWO_SM>
+// fp32 wgrad partial: 32 columns of one output row
+__device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32_t (&r)[32],
+                                                   bool row_ok, bool zero, long long row_off,
+                                                   int n) {
+  if (!row_ok || n >= p.N) return;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int nn = n + u * 4;
+    if (nn < p.N) {
+      uint4 v = zero ? make_uint4(0, 0, 0, 0)
+                     : make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
+      st_v4(p.out_f32 + row_off + nn, v);
+    }
+  }
+}
+
+template <bool TWO_SM, bool B_MN, bool WGRAD>
 __global__ void __launch_bounds__(THREADS, 1)
-    grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, const Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const Params p) {
   using C = Cfg<TWO_SM>;
+  constexpr bool A_MN = WGRAD;
+  constexpr uint32_t IDESC = Idesc<TWO_SM, A_MN, B_MN>::value;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -296,20 +406,29 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   if (warp == 3) {
-    // exclusive prefix of m-tiles per group (warp scan, 32 groups at a time)
-    int carry = 0;
-    if (lane == 0) s_prefix[0] = 0;
-    for (int base = 0; base < p.num_groups; base += 32) {
-      const int g = base + lane;
-      int v = 0;
-      if (g < p.num_groups) v = (group_rows_of(p, g) + C::TILE_M - 1) / C::TILE_M;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
+    if (WGRAD) {
+      // k-blocks feeding each weight group
+      for (int w = lane; w < p.n_wgroups; w += 32) {
+        int tot = 0;
+        for (int g = w; g < p.num_groups; g += p.n_wgroups) tot += (group_rows_of(p, g) + BK - 1) / BK;
+        s_prefix[w] = tot;
       }
-      if (g < p.num_groups) s_prefix[g + 1] = carry + v;
-      carry += __shfl_sync(0xffffffffu, v, 31);
+    } else {
+      // exclusive prefix of m-tiles per group (warp scan, 32 groups at a time)
+      int carry = 0;
+      if (lane == 0) s_prefix[0] = 0;
+      for (int base = 0; base < p.num_groups; base += 32) {
+        const int g = base + lane;
+        int v = 0;
+        if (g < p.num_groups) v = (group_rows_of(p, g) + C::TILE_M - 1) / C::TILE_M;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += u;
+        }
+        if (g < p.num_groups) s_prefix[g + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
     }
   }
   tc_fence_before();
@@ -319,37 +438,34 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *s_tmem;
 
   const int n_tiles_n = (p.N + BN - 1) / BN;
-  const int total_tiles = s_prefix[p.num_groups] * n_tiles_n;
-  const int num_kb = (p.K + BK - 1) / BK;
+  const int total_tiles =
+      WGRAD ? p.splits * p.n_wgroups * ((p.m_out + C::TILE_M - 1) / C::TILE_M) * n_tiles_n
+            : s_prefix[p.num_groups] * n_tiles_n;
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs load their own halves) =====
     int stage = 0;
     uint32_t phase = 0;
     for (int t = unit; t < total_tiles; t += n_units) {
-      const TileCoord tc = decode_tile<C::TILE_M>(t, n_tiles_n, s_prefix, p.num_groups);
-      const int wg = tc.g % p.n_wgroups;
+      const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
       const int am = tc.m0 + (int)rank * C::CTA_M;
       const int bn = tc.n0 + (int)rank * C::B_ROWS;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for_each_kblock<WGRAD>(p, tc, [&](int g, int kb) {
         if (lane == 0) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (TWO_SM) {
-            if (leader) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
-            tma_load_3d_2sm(&map_a, &full_bar[stage], smem_a + stage * C::A_BYTES, kb * BK, am, tc.g);
-            tma_load_3d_2sm(&map_b, &full_bar[stage], smem_b + stage * C::B_BYTES, kb * BK, bn, wg);
-          } else {
-            mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-            tma_load_3d(&map_a, &full_bar[stage], smem_a + stage * C::A_BYTES, kb * BK, am, tc.g);
-            tma_load_3d(&map_b, &full_bar[stage], smem_b + stage * C::B_BYTES, kb * BK, bn, wg);
-          }
+          if (leader) mbar_expect_tx(&full_bar[stage], (TWO_SM ? 2 : 1) * C::STAGE_BYTES);
+          load_operand<TWO_SM, A_MN, C::CTA_M>(&map_a, &full_bar[stage], smem_a + stage * C::A_BYTES,
+                                                kb * BK, am, g);
+          load_operand<TWO_SM, B_MN, C::B_ROWS>(&map_b, &full_bar[stage],
+                                                 smem_b + stage * C::B_BYTES, kb * BK, bn,
+                                                 WGRAD ? g : g % p.n_wgroups);
         }
         __syncwarp();
         if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
-      }
+      });
     }
   } else if (warp == 1) {
     // ===== MMA issuer (leader CTA only in 2SM mode) =====
@@ -358,6 +474,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = unit; t < total_tiles; t += n_units, ++it) {
+        const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -366,7 +483,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
         }
         __syncwarp();
-        for (int kb = 0; kb < num_kb; ++kb) {
+        bool first = true;
+        for_each_kblock<WGRAD>(p, tc, [&](int, int) {
           if (lane == 0) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
@@ -374,17 +492,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t b0 = smem_u32(smem_b + stage * C::B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              tc_mma<TWO_SM>(d_tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32),
-                             (kb | kk) != 0 ? 1u : 0u);
+              tc_mma<TWO_SM>(d_tmem, operand_desc<A_MN>(a0, kk), operand_desc<B_MN>(b0, kk), IDESC,
+                             (first && kk == 0) ? 0u : 1u);
             }
             tc_commit<TWO_SM>(&empty_bar[stage]);
           }
+          first = false;
           __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
-        }
+        });
         if (lane == 0) tc_commit<TWO_SM>(&tfull_bar[acc]);
         __syncwarp();
       }
@@ -396,16 +515,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int half = ew >> 2;    // accumulator columns [128*half, 128*half+128)
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
-      const TileCoord tc = decode_tile<C::TILE_M>(t, n_tiles_n, s_prefix, p.num_groups);
-      const int wg = tc.g % p.n_wgroups;
-      const int rows = group_rows_of(p, tc.g);
+      const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
-      const long long row_off = ((long long)tc.g * p.cap + row) * p.N;
-      const float* brow = p.bias ? p.bias + (long long)wg * p.N : nullptr;
+      bool row_ok, pad_row = false;
+      long long row_off;
+      const float* brow = nullptr;
+      if (WGRAD) {
+        row_ok = row < p.m_out;
+        row_off = (((long long)tc.s * p.n_wgroups + tc.g) * p.m_out + row) * p.N;
+      } else {
+        const int rows = group_rows_of(p, tc.g);
+        row_ok = row < rows;
+        pad_row = p.zero_tail && row < p.cap;
+        row_off = ((long long)tc.g * p.cap + row) * p.N;
+        brow = p.bias ? p.bias + (long long)(tc.g % p.n_wgroups) * p.N : nullptr;
+      }
+      const bool empty = WGRAD && tc.kb_lo >= tc.kb_hi;   // no MMA ran: write zeros
       // TMEM -> registers in 4 chunks of 32 columns, chunk c+1's tcgen05.ld in
       // flight while chunk c is processed
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
@@ -417,7 +546,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t(&cur)[32] = (c & 1) ? rb : ra;
         uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
         if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
-        epilogue_chunk(p, cur, row < rows, row_off, tc.n0 + half * 128 + c * 32, brow);
+        const int n = tc.n0 + half * 128 + c * 32;
+        if (WGRAD) epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
+        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow);
         if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == 2) {
           // the whole accumulator is in registers: hand TMEM back to the MMA warp
@@ -446,6 +577,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// sum of split-K partials: out[i] = sum_s part[s][i] (fp32), n multiple of 4
+__global__ void reduce_splits_kernel(const float4* __restrict__ part, int splits, long long n4,
+                                     float4* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 a = part[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = part[s * n4 + i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -462,36 +607,39 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D bf16 map over (k_in, rows, groups), box (64, box_rows, 1), 128B swizzle.
-int make_map(CUtensorMap* map, const void* base, int k_in, int rows, int groups, int box_rows) {
+// 3-D bf16 map over (inner, outer, groups) with box (64, box_outer, 1), 128B swizzle.
+// K-major operands: inner = k, outer = rows (box_outer = tile rows);
+// MN-major operands: inner = mn, outer = k (box_outer = 64).
+int make_map(CUtensorMap* map, const void* base, int inner, int outer, int groups, int box_outer) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable from the driver");
     return SCMOE_ERR_CUDA;
   }
-  cuuint64_t dims[3] = {(cuuint64_t)k_in, (cuuint64_t)rows, (cuuint64_t)groups};
-  cuuint64_t strides[2] = {(cuuint64_t)k_in * 2, (cuuint64_t)k_in * 2 * (cuuint64_t)rows};
-  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)groups};
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)inner * 2 * (cuuint64_t)outer};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d): k=%d rows=%d groups=%d", (int)r, k_in, rows,
-              groups);
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%d outer=%d groups=%d", (int)r, inner,
+              outer, groups);
     return SCMOE_ERR_CUDA;
   }
   return SCMOE_OK;
 }
 
-template <bool TWO_SM>
+template <bool TWO_SM, bool B_MN, bool WGRAD>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
            cudaStream_t st) {
   using C = Cfg<TWO_SM>;
   static bool attr_set = false;
+  auto kern = gemm_kernel<TWO_SM, B_MN, WGRAD>;
   if (!attr_set) {
-    SCMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<TWO_SM>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    SCMOE_CUDA_TRY(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -506,7 +654,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SCMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<TWO_SM>, ma, mb, p));
+  SCMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, p));
   return SCMOE_OK;
 }
 
@@ -515,17 +663,20 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
 // mode: 0 auto, 1 force 1-SM, 2 force 2-SM (tests / tuning)
 static int g_gemm_mode = 0;
 
-int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, const void* residual,
-                      void* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                      int rows_clip, int N, int K, int epi, cudaStream_t st) {
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias,
+                      const void* residual, const void* aux_in, void* aux_out, void* out,
+                      int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st) {
   using namespace sm100;
   SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
   SCMOE_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "bf16 GEMM needs k_in and n_out multiples of 8");
-  SCMOE_CHECK_ARG(((uintptr_t)a & 15) == 0 && ((uintptr_t)wt & 15) == 0 &&
-                      ((uintptr_t)out & 15) == 0 && ((uintptr_t)bias & 15) == 0 &&
-                      ((uintptr_t)residual & 15) == 0,
+  SCMOE_CHECK_ARG(aligned16(a) && aligned16(wt) && aligned16(out) && aligned16(bias) &&
+                      aligned16(residual) && aligned16(aux_in) && aligned16(aux_out),
                   "GEMM operands must be 16-byte aligned");
-  Params p;
+  SCMOE_CHECK_ARG(epi != EPI_GELU_BWD || aux_in, "GELU backward needs the pre-activation");
+  Params p = {};
   p.num_groups = num_groups;
   p.n_wgroups = n_wgroups;
   p.cap = cap;
@@ -533,31 +684,89 @@ int grouped_gemm_bf16(const void* a, const void* wt, const float* bias, const vo
   p.N = N;
   p.K = K;
   p.epi = epi;
+  p.zero_tail = zero_tail;
   p.group_rows = group_rows;
   p.bias = bias;
   p.residual = (const __nv_bfloat16*)residual;
+  p.aux_in = (const __nv_bfloat16*)aux_in;
+  p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
   const int sms = num_sms();
   const long long n_tiles_n = (N + BN - 1) / BN;
   const long long tiles_2sm = (long long)num_groups * ((cap + 255) / 256) * n_tiles_n;
-  bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_2sm >= sms / 2);
+  const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_2sm >= sms / 2);
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, a, K, cap, num_groups, 128);
+  int rc = make_map(&ma, a, K, cap, num_groups, Cfg<true>::CTA_M);
   if (rc) return rc;
-  rc = make_map(&mb, wt, K, N, n_wgroups, two ? BN / 2 : BN);
+  const int b_rows = two ? Cfg<true>::B_ROWS : Cfg<false>::B_ROWS;
+  rc = b_mn ? make_map(&mb, wt, N, K, n_wgroups, BK) : make_map(&mb, wt, K, N, n_wgroups, b_rows);
   if (rc) return rc;
   if (two) {
     const long long units = tiles_2sm < sms / 2 ? tiles_2sm : sms / 2;
     if (units <= 0) return SCMOE_OK;
-    rc = launch<true>(ma, mb, p, (int)units * 2, st);
+    rc = b_mn ? launch<true, true, false>(ma, mb, p, (int)units * 2, st)
+              : launch<true, false, false>(ma, mb, p, (int)units * 2, st);
   } else {
     const long long tiles = (long long)num_groups * ((cap + 127) / 128) * n_tiles_n;
     const int grid = (int)(tiles < sms ? tiles : sms);
     if (grid <= 0) return SCMOE_OK;
-    rc = launch<false>(ma, mb, p, grid, st);
+    rc = b_mn ? launch<false, true, false>(ma, mb, p, grid, st)
+              : launch<false, false, false>(ma, mb, p, grid, st);
   }
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+size_t wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out, int splits) {
+  return splits > 1 ? (size_t)splits * n_wgroups * m_out * n_out * sizeof(float) : 0;
+}
+
+int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_t ws_bytes,
+                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
+                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st) {
+  using namespace sm100;
+  SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
+  SCMOE_CHECK_ARG(m_out % 8 == 0 && n_out % 8 == 0, "wgrad needs m_out, n_out multiples of 8");
+  SCMOE_CHECK_ARG(aligned16(a) && aligned16(b) && aligned16(out) && aligned16(ws),
+                  "wgrad operands must be 16-byte aligned");
+  const int sms = num_sms();
+  const long long tiles1 =
+      (long long)n_wgroups * ((m_out + 255) / 256) * ((n_out + BN - 1) / BN);
+  if (splits <= 0) {
+    // fill the CTA pairs: split the token reduction until ~1 tile per pair
+    const long long kb_guess = ((long long)num_groups / n_wgroups) * ((cap + BK - 1) / BK);
+    long long s = (sms / 2 + tiles1 - 1) / tiles1;
+    if (s > kb_guess / 4) s = kb_guess / 4;
+    splits = (int)(s < 1 ? 1 : (s > 64 ? 64 : s));
+  }
+  SCMOE_CHECK_ARG(splits == 1 || ws_bytes >= wgrad_workspace_bytes(n_wgroups, m_out, n_out, splits),
+                  "wgrad workspace too small for %d splits", splits);
+  Params p = {};
+  p.num_groups = num_groups;
+  p.n_wgroups = n_wgroups;
+  p.cap = cap;
+  p.rows_clip = rows_clip;
+  p.N = n_out;
+  p.m_out = m_out;
+  p.splits = splits;
+  p.group_rows = group_rows;
+  p.out_f32 = splits > 1 ? (float*)ws : out;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, a, m_out, cap, num_groups, BK);
+  if (rc) return rc;
+  rc = make_map(&mb, b, n_out, cap, num_groups, BK);
+  if (rc) return rc;
+  const long long units_all = tiles1 * splits;
+  const long long units = units_all < sms / 2 ? units_all : sms / 2;
+  rc = launch<true, true, true>(ma, mb, p, (int)units * 2, st);
+  if (rc) return rc;
+  SCMOE_LAUNCH_CHECK();
+  if (splits > 1) {
+    const long long n4 = (long long)n_wgroups * m_out * n_out / 4;
+    reduce_splits_kernel<<<sms * 4, 256, 0, st>>>((const float4*)ws, splits, n4, (float4*)out);
+    SCMOE_LAUNCH_CHECK();
+  }
   return SCMOE_OK;
 }
 

@@ -169,3 +169,96 @@ def combine(expert_out: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor
 def set_gemm_mode(mode: int) -> None:
     """0 = auto, 1 = force the 1-SM tcgen05 kernel, 2 = force the 2-SM kernel."""
     check(lib().scmoe_set_gemm_mode(mode))
+
+
+# ---------------------------------------------------------------------------
+# training-side entries (K7)
+
+
+def grouped_gemm_ex(a: torch.Tensor, w: torch.Tensor, w_layout: int, out_cols: int,
+                    bias: Optional[torch.Tensor] = None, residual: Optional[torch.Tensor] = None,
+                    aux_in: Optional[torch.Tensor] = None, aux_out: Optional[torch.Tensor] = None,
+                    epilogue: int = _lib.EPI_BIAS, group_rows: Optional[torch.Tensor] = None,
+                    rows_clip: int = 0, zero_tail: bool = False,
+                    out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out[g] = epi(a[g] @ Wg + bias) with Wg = w[g % W]^T (W_NK) or w[g % W] (W_KN)."""
+    ensure_device(a)
+    a3 = a if a.dim() == 3 else a.unsqueeze(0)
+    w3 = w if w.dim() == 3 else w.unsqueeze(0)
+    G, C, K = a3.shape
+    W = w3.shape[0]
+    k_in = w3.shape[2] if w_layout == _lib.W_NK else w3.shape[1]
+    n_out = w3.shape[1] if w_layout == _lib.W_NK else w3.shape[2]
+    if k_in != K or n_out != out_cols:
+        raise ValueError(f"weight shape {tuple(w3.shape)} does not match a {tuple(a3.shape)} -> {out_cols}")
+    if out is None:
+        out = torch.empty(G, C, n_out, device=a.device, dtype=a.dtype)
+    for name, t in (("residual", residual), ("aux_in", aux_in), ("aux_out", aux_out)):
+        if t is not None:
+            _c(t, name)
+            if t.numel() != out.numel():
+                raise ValueError(f"{name} must match the output's shape")
+    check(lib().scmoe_grouped_gemm_ex(
+        ptr(_c(a3, "a")), dtype_code(a.dtype), ptr(_c(w3, "w")), w_layout, ptr(bias),
+        ptr(residual), ptr(aux_in), ptr(aux_out), ptr(out), G, W, C, ptr(group_rows), rows_clip,
+        n_out, K, epilogue, 1 if zero_tail else 0, stream_ptr(stream)))
+    return out if a.dim() == 3 else out.view(C, n_out)
+
+
+def grouped_wgrad(a: torch.Tensor, b: torch.Tensor, n_wgroups: int = 1,
+                  group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0, splits: int = 0,
+                  out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out[w] = sum_{g = w mod W} a[g, :rows(g)]^T @ b[g, :rows(g)] in fp32."""
+    ensure_device(a)
+    a3 = a if a.dim() == 3 else a.unsqueeze(0)
+    b3 = b if b.dim() == 3 else b.unsqueeze(0)
+    G, C, M = a3.shape
+    N = b3.shape[2]
+    if b3.shape[:2] != (G, C):
+        raise ValueError("a and b must share (groups, rows)")
+    if out is None:
+        out = torch.empty(n_wgroups, M, N, device=a.device, dtype=torch.float32)
+    ws_bytes = lib().scmoe_grouped_wgrad_workspace_bytes(n_wgroups, M, N, splits)
+    ws = torch.empty(max(ws_bytes, 16), device=a.device, dtype=torch.uint8)
+    check(lib().scmoe_grouped_wgrad(
+        ptr(_c(a3, "a")), ptr(_c(b3, "b")), dtype_code(a.dtype), ptr(out), ptr(ws), ws_bytes, G,
+        n_wgroups, C, ptr(group_rows), rows_clip, M, N, splits, stream_ptr(stream)))
+    return out if (a.dim() == 3 or n_wgroups > 1) else out.view(M, N)
+
+
+def zero_tails(buf: torch.Tensor, group_rows: torch.Tensor, rows_clip: int = 0, align: int = 64,
+               stream=None) -> torch.Tensor:
+    ensure_device(buf)
+    b3 = buf if buf.dim() == 3 else buf.unsqueeze(0)
+    G, C, D = b3.shape
+    check(lib().scmoe_zero_tails(ptr(_c(b3, "buf")), dtype_code(buf.dtype), G, C, D,
+                                 ptr(group_rows), rows_clip, align, stream_ptr(stream)))
+    return buf
+
+
+def grouped_colsum(x: torch.Tensor, group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
+                   stream=None) -> torch.Tensor:
+    ensure_device(x)
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    G, C, D = x3.shape
+    out = torch.empty(G, D, device=x.device, dtype=torch.float32)
+    check(lib().scmoe_grouped_colsum(ptr(_c(x3, "x")), dtype_code(x.dtype), G, C, D,
+                                     ptr(group_rows), rows_clip, ptr(out), stream_ptr(stream)))
+    return out if x.dim() == 3 else out.view(D)
+
+
+def dispatch_scaled(x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor, n_experts: int,
+                    capacity: int, row_scale: Optional[torch.Tensor],
+                    out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """dispatch with each copied row scaled by row_scale[t, j] (combine backward)."""
+    ensure_device(x)
+    T, d = x.shape
+    k = indices.shape[1]
+    if out is None:
+        out = torch.empty(n_experts, capacity, d, device=x.device, dtype=x.dtype)
+    if row_scale is not None:
+        row_scale = _c(row_scale.to(torch.float32), "row_scale")
+    check(lib().scmoe_dispatch_scaled(ptr(x), dtype_code(x.dtype), x.stride(0), T, d, k,
+                                      ptr(_c(indices, "indices")), ptr(_c(slots, "slots")),
+                                      capacity, ptr(row_scale), ptr(out), stream_ptr(stream)))
+    return out

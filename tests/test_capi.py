@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(so, n), n
     typed = {name for name, _, _ in _lib.SIGNATURES}
     assert typed == set(_declared())
-    assert so.scmoe_version() == 1
+    assert so.scmoe_version() == 2
 
 
 def test_workspace_query_is_host_only():

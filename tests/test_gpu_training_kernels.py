@@ -1,0 +1,122 @@
+"""K7 backward kernels vs torch fp64 references of the same ops (bf16 inputs,
+tolerance 2e-2 scaled by max|ref|): MN-major (transposed-weight) data
+gradients, the GELU-backward and pre-activation epilogues, zero-tail padding,
+the split-K grouped weight gradient, grouped column sums and the scaled
+dispatch used by the combine backward."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+K = L = None
+
+
+def setup_module(module):
+    global K, L
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_05019_b200 import _lib, kernels
+    K, L = kernels, _lib
+
+
+def _close(got, ref, rtol=2e-2):
+    got, ref = got.double(), ref.double()
+    bound = rtol * (ref.abs() + ref.abs().max() + 1e-12)
+    err = (got - ref).abs()
+    assert (err <= bound).all(), f"max err {err.max().item():.3g}, max ref {ref.abs().max().item():.3g}"
+
+
+def _gelu_grad(z):
+    return 0.5 * (1 + torch.erf(z / 2 ** 0.5)) + z * torch.exp(-0.5 * z * z) / (2 * torch.pi) ** 0.5
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("G,W,C,Kd,N", [(1, 1, 384, 256, 512), (4, 2, 300, 1536, 384),
+                                        (8, 8, 256, 384, 1536)])
+def test_dgrad_transposed_weights(mode, G, W, C, Kd, N):
+    """out = a @ w[g % W]  with w stored (W, k_in, n_out) — MN-major tcgen05 B."""
+    K.set_gemm_mode(mode)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(G + N)
+        a = torch.randn(G, C, Kd, device="cuda", generator=g).bfloat16()
+        w = (torch.randn(W, Kd, N, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
+        z = torch.randn(G, C, N, device="cuda", generator=g).bfloat16()
+        rows = torch.tensor([C - 37 * i for i in range(G)], device="cuda", dtype=torch.int32)
+        out = torch.full((G, C, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        K.grouped_gemm_ex(a, w, L.W_KN, N, aux_in=z, epilogue=L.EPI_GELU_BWD, group_rows=rows,
+                          rows_clip=C, zero_tail=True, out=out)
+        torch.cuda.synchronize()
+        for gi in range(G):
+            r = int(rows[gi])
+            ref = (a[gi, :r].double() @ w[gi % W].double()) * _gelu_grad(z[gi, :r].double())
+            _close(out[gi, :r], ref)
+            tail_end = min(C, ((r + (255 if mode == 2 else 127)) // (256 if mode == 2 else 128)) * (256 if mode == 2 else 128))
+            assert torch.all(out[gi, r:tail_end] == 0)
+    finally:
+        K.set_gemm_mode(0)
+
+
+def test_forward_preactivation_store():
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn(2, 200, 256, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(2, 512, 256, device="cuda", generator=g) / 16).bfloat16()
+    b = torch.randn(2, 512, device="cuda", generator=g)
+    zbuf = torch.empty(2, 200, 512, device="cuda", dtype=torch.bfloat16)
+    h = K.grouped_gemm_ex(a, w, L.W_NK, 512, bias=b, aux_out=zbuf, epilogue=L.EPI_BIAS_GELU)
+    zref = torch.einsum("gck,gnk->gcn", a.double(), w.double()) + b.double()[:, None, :]
+    _close(zbuf, zref)
+    _close(h, torch.nn.functional.gelu(zref))
+
+
+@pytest.mark.parametrize("G,W,C,M,N,splits", [(1, 1, 4096, 384, 1536, 0), (8, 8, 700, 1536, 384, 0),
+                                              (4, 2, 513, 256, 264, 3), (2, 1, 128, 64, 128, 1),
+                                              (16, 2, 300, 384, 1536, 0)])
+def test_grouped_wgrad(G, W, C, M, N, splits):
+    g = torch.Generator(device="cuda").manual_seed(G * 3 + M)
+    a = torch.randn(G, C, M, device="cuda", generator=g).bfloat16()
+    b = torch.randn(G, C, N, device="cuda", generator=g).bfloat16()
+    rows = torch.randint(1, C + 1, (G,), device="cuda", generator=g, dtype=torch.int32)
+    if G > 1:
+        rows[1] = 0
+    K.zero_tails(a, rows, C)
+    K.zero_tails(b, rows, C)
+    out = K.grouped_wgrad(a, b, n_wgroups=W, group_rows=rows, rows_clip=C, splits=splits)
+    torch.cuda.synchronize()
+    rr = rows.tolist()
+    for w in range(W):
+        ref = torch.zeros(M, N, dtype=torch.float64, device="cuda")
+        for gi in range(w, G, W):
+            r = rr[gi]
+            ref += a[gi, :r].double().t() @ b[gi, :r].double()
+        _close(out[w] if out.dim() == 3 else out, ref, rtol=1e-2)
+
+
+def test_zero_tails_and_colsum():
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(3, 300, 128, device="cuda", generator=g).bfloat16()
+    rows = torch.tensor([10, 64, 250], device="cuda", dtype=torch.int32)
+    K.zero_tails(x, rows, 300, align=64)
+    assert torch.all(x[0, 10:64] == 0) and torch.all(x[2, 250:256] == 0)
+    assert not torch.all(x[0, 64:70] == 0)          # beyond the padding: untouched
+    s = K.grouped_colsum(x, rows, 300)
+    for gi, r in enumerate(rows.tolist()):
+        torch.testing.assert_close(s[gi], x[gi, :r].float().sum(0), rtol=1e-4, atol=1e-3)
+
+
+def test_dispatch_scaled():
+    g = torch.Generator(device="cuda").manual_seed(2)
+    T, d, N, k = 500, 256, 4, 2
+    x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, d, device="cuda", generator=g)
+    quota = K.expert_quota(1.0, T, k, N)
+    dec = K.gate_topk(x, w, k, quota)
+    scale = torch.rand(T, k, device="cuda", generator=g)
+    buf = torch.zeros(N, quota, d, device="cuda", dtype=torch.bfloat16)
+    K.dispatch_scaled(x, dec.indices, dec.slots, N, quota, scale, out=buf)
+    idx, sl = dec.indices.long(), dec.slots.long()
+    kept = sl < quota
+    tt = torch.arange(T, device="cuda")[:, None].expand(T, k)
+    ref = torch.zeros(N, quota, d, device="cuda", dtype=torch.float64)
+    ref[idx[kept], sl[kept]] = x[tt[kept]].double() * scale[kept].double()[:, None]
+    _close(buf, ref, rtol=1e-2)
