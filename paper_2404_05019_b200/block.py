@@ -82,11 +82,18 @@ class Attention(nn.Module):
         if t % s:
             raise ValueError(f"{t} tokens do not split into sequences of {s}")
         b, hd = t // s, d // h
-        qkv = K.grouped_gemm(x, self.w_qkv_t, None)                        # (T, 3d)
+        train = torch.is_grad_enabled() and (self.w_qkv_t.requires_grad or x.requires_grad)
+        if train:
+            from .training import LinearFn
+            qkv = LinearFn.apply(x, self.w_qkv_t, None)
+        else:
+            qkv = K.grouped_gemm(x, self.w_qkv_t, None)                    # (T, 3d)
         q, k, v = qkv.view(b, s, 3, h, hd).permute(2, 0, 3, 1, 4).unbind(0)  # (B, H, S, hd)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal,
                                            scale=1.0 / math.sqrt(d) if h == 1 else None)
         o = o.permute(0, 2, 1, 3).reshape(t, d).contiguous()
+        if train:
+            return LinearFn.apply(o, self.w_o_t, residual)
         return K.grouped_gemm(o, self.w_o_t, None, residual=residual)
 
 
@@ -202,12 +209,31 @@ class ScMoEBlockPair(nn.Module):
             return env["x_cur"]
 
         env["h_in"] = h_in
+        train = moe.training_path()
+        if train:
+            from . import training as TR
 
         def gate():
-            env["dec"] = moe.route(src(), eps=eps, replay=replay)
+            if train:
+                with torch.no_grad():
+                    dec = moe.route(src(), eps=eps, replay=replay)
+                env["dec"] = dec
+                env["kept"] = dec.kept_counts().to(torch.int32)
+                env["w"], env["aux"] = TR.GateFn.apply(src(), moe.gate.w_gate_t, dec.logits,
+                                                       dec.indices, dec.counts, dec.weights, dec.k)
+            else:
+                env["dec"] = moe.route(src(), eps=eps, replay=replay)
 
         def encode():
             dec = env["dec"]
+            if train:
+                buf = TR.DispatchFn.apply(src(), dec.indices, dec.slots, env["kept"], moe.n_experts,
+                                          dec.capacity)
+                env["buf"] = buf
+                if use_ep:   # exchanges inline on the compute stream while training
+                    env["recv_counts"] = ep_mod.exchange_counts(env["kept"], self.ep_group)
+                    env["buf"] = TR.ExchangeFn.apply(buf, self.ep_group)
+                return
             buf = K.dispatch(src(), dec.indices, dec.slots, moe.n_experts, dec.capacity)
             env["buf"] = buf
             if use_ep:
@@ -218,6 +244,12 @@ class ScMoEBlockPair(nn.Module):
 
         def expert():
             dec = env["dec"]
+            if train:
+                e = moe.experts
+                rows = env["recv_counts"] if use_ep else env["kept"]
+                y = TR.FFNFn.apply(env["buf"], e.w1t, e.b1, e.w2t, e.b2, None, rows, dec.capacity)
+                env["y"] = TR.ExchangeFn.apply(y, self.ep_group) if use_ep else y
+                return
             if use_ep:
                 p = env["pending"]
                 st.wait_event(p.event)
@@ -234,6 +266,13 @@ class ScMoEBlockPair(nn.Module):
 
         def decode():
             dec = env["dec"]
+            if train:
+                std = self.variant == "standard"
+                env["out"] = TR.CombineFn.apply(
+                    env["y"], None if std else env["se"], env["w"], None if std else env["x_cur"],
+                    None if std else moe.w_cg, env["h_mh_cur"], dec.indices, dec.slots, env["kept"],
+                    dec.capacity, "direct_add" if std else moe.combine_mode)
+                return
             if use_ep:
                 st.wait_event(env["y_ev"])
             if self.variant == "standard":
@@ -250,12 +289,36 @@ class ScMoEBlockPair(nn.Module):
             with rec.op(name, "compute", st):
                 ops[name]()
         dec = env["dec"]
-        res = (env["out"], dec, dec.aux_loss())
+        res = (env["out"], dec, env["aux"] if train else dec.aux_loss())
         if return_taps:
             taps = {k: env[k] for k in ("h_mh_prev", "h_mlp_prev", "h_mh_cur", "x_cur")}
             taps["src"] = src()
             return res + (taps,)
         return res
+
+    # -- training ----------------------------------------------------------------
+    def train_step(self, h_in: torch.Tensor, lr: float = 0.01, aux_coeff: float = 0.01,
+                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True):
+        """One optimisation step of the reference objective (grad.py:52-67):
+        loss = mean(out) (or sum((out - target)^2) / T, LossSpec "mse") +
+        aux_coeff * aux, backward through the K7 kernels, data-parallel
+        all-reduce of the replicated parameters (N > 1), in-place SGD
+        (grad.py:330-331).  Returns the loss (device tensor, no sync)."""
+        from . import training as TR
+        for p in self.parameters():
+            p.grad = None
+        out, dec, aux = self(h_in)
+        if target is None:
+            loss = out.float().mean()
+        else:
+            loss = (out.float() - target.float()).pow(2).sum() / out.shape[0]
+        loss = loss + aux_coeff * aux
+        loss.backward()
+        if dp_group is not None or self.ep_group is not None:
+            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else self.ep_group)
+        if update:
+            TR.sgd_step(self.parameters(), lr)
+        return loss.detach()
 
     # -- adaptive scheduling ---------------------------------------------------
     def calibrate(self, h_in: torch.Tensor, repeats: int = 3) -> sched.ScheduleChoice:

@@ -222,7 +222,7 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kk) {
       : "r"(taddr))
 
 __device__ __forceinline__ int group_rows_of(const Params& p, int g) {
-  return p.group_rows ? min(__ldg(p.group_rows + g), p.rows_clip) : p.cap;
+  return p.group_rows ? max(0, min(__ldg(p.group_rows + g), p.rows_clip)) : p.cap;
 }
 
 // One output tile: (group or weight group, row offset, column offset) and,

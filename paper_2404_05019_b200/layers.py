@@ -267,6 +267,10 @@ class SharedExpert(nn.Module):
         """expert_forward(x) (+ residual, fused into the second GEMM's epilogue)."""
         if x.dtype != self.w1t.dtype:
             raise ValueError(f"input dtype {x.dtype} != expert dtype {self.w1t.dtype}")
+        if torch.is_grad_enabled() and (self.w1t.requires_grad or x.requires_grad):
+            from .training import FFNFn
+            return FFNFn.apply(x, self.w1t, self.b1, self.w2t, self.b2, residual, None,
+                               x.shape[0])
         return K.expert_ffn(x, self.w1t, self.b1, self.w2t, self.b2, hidden=hidden, out=out,
                             residual=residual, stream=stream)
 
@@ -376,6 +380,35 @@ class _RoutedMoE(nn.Module):
         from . import ep
         return ep.expert_parallel_ffn(self.experts, buf, dec, self.ep_group)
 
+    # -- training (autograd through the K7 kernels) ---------------------------
+    def training_path(self) -> bool:
+        """True when a forward must record the autograd graph."""
+        return torch.is_grad_enabled() and any(p.requires_grad for p in self.parameters())
+
+    def routed_train(self, src: torch.Tensor, dec: GateDecision):
+        """Differentiable gate weights / aux and expert output buffer."""
+        from . import training as TR
+        if self.dtype != torch.bfloat16:
+            raise NotImplementedError("backward kernels are bf16 only (the fp32 path is a "
+                                      "forward parity path)")
+        if self.noise_enabled:
+            raise NotImplementedError("training with the noisy gate is not implemented yet")
+        kept = dec.kept_counts().to(torch.int32)
+        w, aux = TR.GateFn.apply(src, self.gate.w_gate_t, dec.logits, dec.indices, dec.counts,
+                                 dec.weights, dec.k)
+        buf = TR.DispatchFn.apply(src, dec.indices, dec.slots, kept, self.n_experts, dec.capacity)
+        e = self.experts
+        if self.ep_group is None:
+            y = TR.FFNFn.apply(buf, e.w1t, e.b1, e.w2t, e.b2, None, kept, dec.capacity)
+        else:
+            from . import ep
+            recv_counts = ep.exchange_counts(kept, self.ep_group)
+            recv = TR.ExchangeFn.apply(buf, self.ep_group)
+            y_local = TR.FFNFn.apply(recv, e.w1t, e.b1, e.w2t, e.b2, None, recv_counts,
+                                     dec.capacity)
+            y = TR.ExchangeFn.apply(y_local, self.ep_group)
+        return w, aux, y, kept
+
 
 class ScMoELayer(_RoutedMoE):
     """The shortcut-connected MoE layer: combine(SE(x_cur), routed(src), x_cur)
@@ -430,6 +463,16 @@ class ScMoELayer(_RoutedMoE):
         src = x_cur if routed_src is None else routed_src
         if src.shape != x_cur.shape:
             raise ValueError("routed_src and x_cur must have the same shape")
+        if self.training_path():
+            from . import training as TR
+            with torch.no_grad():
+                dec = self.route(src, eps=eps, replay=replay, generator=generator)
+            w, aux, y, kept = self.routed_train(src, dec)
+            sh = self.shared
+            se = TR.FFNFn.apply(x_cur, sh.w1t, sh.b1, sh.w2t, sh.b2, None, None, x_cur.shape[0])
+            out = TR.CombineFn.apply(y, se, w, x_cur, self.w_cg, residual, dec.indices, dec.slots,
+                                     kept, dec.capacity, self.combine_mode)
+            return out, dec, aux
         dec = self.route(src, eps=eps, replay=replay, generator=generator)
         y = self.routed_experts(src, dec)
         se = self.shared(x_cur)
@@ -465,6 +508,14 @@ class Top2MoELayer(_RoutedMoE):
     def forward(self, x: torch.Tensor, residual: Optional[torch.Tensor] = None,
                 eps: Optional[torch.Tensor] = None, replay: Optional[MoEReplay] = None,
                 generator=None):
+        if self.training_path():
+            from . import training as TR
+            with torch.no_grad():
+                dec = self.route(x, eps=eps, replay=replay, generator=generator)
+            w, aux, y, kept = self.routed_train(x, dec)
+            out = TR.CombineFn.apply(y, None, w, None, None, residual, dec.indices, dec.slots,
+                                     kept, dec.capacity, "direct_add")
+            return out, dec, aux
         dec = self.route(x, eps=eps, replay=replay, generator=generator)
         y = self.routed_experts(x, dec)
         out = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, residual=residual)

@@ -1,0 +1,257 @@
+"""Training path (K7): autograd Functions whose forward AND backward run on
+libscmoe kernels.
+
+Semantics follow the reference's tape (scmoelab/tape.py, grad.py:52-86):
+  * routing index sets and drop masks are constants (straight-through,
+    tape.py:11-13);
+  * the objective is loss + aux_coeff * sum(aux) (grad.py:52-67, aux_coeff 0.01
+    by default, LossSpec grad.py:28-40), so the top-1 gate only receives
+    gradient through the balance loss (arch.py:436-439) — its masked-softmax
+    weight is identically 1;
+  * GELU is the exact erf GELU (tape.py:137-142).
+
+Kernels used in backward: the tcgen05 GEMM reading the stored K-major weights
+transposed (MN-major operand) with the GELU-backward epilogue (dZ = dH *
+gelu'(Z)), the split-K grouped weight-gradient GEMM, grouped column sums for
+bias gradients, the scaled dispatch (combine backward) and the combine kernel
+used as a gather-sum (dispatch backward).  Only the bf16 path has backward
+kernels; the fp32 parity path is forward-only.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+from . import kernels as K
+
+_NK, _KN = _lib.W_NK, _lib.W_KN
+
+
+def _as_param_grad(g: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+    return g.to(like.dtype).view(like.shape)
+
+
+class LinearFn(torch.autograd.Function):
+    """y = x @ wt^T (+ residual); wt is (n_out, k_in) (bias-free projection)."""
+
+    @staticmethod
+    def forward(ctx, x, wt, residual):
+        y = K.grouped_gemm(x, wt, None, residual=residual)
+        ctx.save_for_backward(x, wt)
+        ctx.has_res = residual is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, wt = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx = dwt = None
+        if ctx.needs_input_grad[0]:
+            dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1])
+        if ctx.needs_input_grad[1]:
+            dwt = _as_param_grad(K.grouped_wgrad(dy, x), wt)
+        return dx, dwt, (dy if ctx.has_res else None)
+
+
+class FFNFn(torch.autograd.Function):
+    """expert_forward (arch.py:349-351) over groups, + optional residual.
+
+    x (G, C, d) or (T, d); w1t (W, h, d), b1 (W, h), w2t (W, d, h), b2 (W, d).
+    Rows past rows(g) are zero-padded in the saved activations so the weight
+    gradients can sum whole 64-row blocks."""
+
+    @staticmethod
+    def forward(ctx, x, w1t, b1, w2t, b2, residual, group_rows, rows_clip):
+        two_d = x.dim() == 2
+        x3 = x.unsqueeze(0) if two_d else x
+        w13 = w1t.unsqueeze(0) if w1t.dim() == 2 else w1t
+        w23 = w2t.unsqueeze(0) if w2t.dim() == 2 else w2t
+        G, C, d = x3.shape
+        h = w13.shape[1]
+        z = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
+        hid = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), aux_out=z,
+                                epilogue=_lib.EPI_BIAS_GELU, group_rows=group_rows,
+                                rows_clip=rows_clip, zero_tail=group_rows is not None)
+        res3 = None if residual is None else residual.view(G, C, d)
+        y = K.grouped_gemm_ex(hid, w23, _NK, d, bias=b2.view(-1, d), residual=res3,
+                              group_rows=group_rows, rows_clip=rows_clip)
+        ctx.save_for_backward(x3, z, hid, w13, w23, group_rows)
+        ctx.meta = (two_d, rows_clip, residual is not None, b1.shape, b2.shape, w1t.shape,
+                    w2t.shape)
+        return y.view(C, d) if two_d else y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x3, z, hid, w13, w23, group_rows = ctx.saved_tensors
+        two_d, rows_clip, has_res, b1_shape, b2_shape, w1_shape, w2_shape = ctx.meta
+        G, C, d = x3.shape
+        W, h, _ = w13.shape
+        dy3 = dy.contiguous().view(G, C, d)
+        grouped = group_rows is not None
+        if grouped:
+            K.zero_tails(dy3, group_rows, rows_clip)
+        dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
+                               group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+        dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip)
+        dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
+        dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
+        db2 = K.grouped_colsum(dy3, group_rows, rows_clip)
+        db1 = K.grouped_colsum(dz, group_rows, rows_clip)
+        if W != G:   # several source groups feed one weight group (expert parallel)
+            db2 = db2.view(G // W, W, d).sum(0)
+            db1 = db1.view(G // W, W, h).sum(0)
+        return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
+                db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
+                (dy if has_res else None), None, None)
+
+
+class GateFn(torch.autograd.Function):
+    """Differentiable part of the gate: returns the kept-selection weights
+    (T, k) and aux = N * sum_i f_i P_i (arch.py:436-439, 481-485).  Routing
+    (indices, drops, counts) comes in as constants from the gate kernel."""
+
+    @staticmethod
+    def forward(ctx, src, w_gate_t, logits, indices, counts, weights, k):
+        n = logits.shape[1]
+        t = logits.shape[0]
+        f = counts.to(torch.float32) / float(t * k)
+        p = torch.softmax(logits, dim=1)
+        aux = n * (f * p.mean(0)).sum()
+        ctx.save_for_backward(src, w_gate_t, p, f, indices, weights)
+        ctx.k = k
+        return weights.clone(), aux
+
+    @staticmethod
+    def backward(ctx, d_weights, d_aux):
+        src, w_gate_t, p, f, indices, weights = ctx.saved_tensors
+        t, n = p.shape
+        dlogits = torch.zeros_like(p)
+        if d_aux is not None:
+            # d aux / d h[t, j] = (N / T) p_tj (f_j - <f, p_t>)
+            dlogits += (d_aux * n / t) * p * (f[None, :] - (p * f[None, :]).sum(1, keepdim=True))
+        if d_weights is not None and ctx.k > 1:
+            # masked softmax over the k selected logits (tape.py:161-176)
+            dw = d_weights.float()
+            dsel = weights * (dw - (weights * dw).sum(1, keepdim=True))
+            dlogits.scatter_add_(1, indices.long(), dsel)
+        d_src = (dlogits @ w_gate_t).to(src.dtype)
+        d_w = dlogits.t() @ src.float()
+        return d_src, d_w, None, None, None, None, None
+
+
+class DispatchFn(torch.autograd.Function):
+    """x_src -> capacity-slotted (E, C, d) buffer with zero-padded tails."""
+
+    @staticmethod
+    def forward(ctx, x, indices, slots, kept, n_experts, capacity):
+        buf = K.dispatch(x, indices, slots, n_experts, capacity)
+        K.zero_tails(buf, kept, capacity)
+        ctx.save_for_backward(indices, slots)
+        ctx.capacity = capacity
+        return buf
+
+    @staticmethod
+    def backward(ctx, dbuf):
+        indices, slots = ctx.saved_tensors
+        ones = torch.ones(indices.shape, device=dbuf.device, dtype=torch.float32)
+        dx = K.combine(dbuf.contiguous(), indices, slots, ones, ctx.capacity)
+        return dx, None, None, None, None, None
+
+
+class CombineFn(torch.autograd.Function):
+    """out = c_se * se + c_rt * sum_j w_j y[e_j, slot_j] (+ residual) —
+    combine (arch.py:380-392) with the routed sum (arch.py:418-433)."""
+
+    @staticmethod
+    def forward(ctx, y, se, weights, x_cur, w_cg, residual, indices, slots, kept, capacity, mode):
+        out = K.combine(y, indices, slots, weights.contiguous(), capacity, se_out=se, mode=mode,
+                        x_cur=x_cur, w_cg=w_cg, residual=residual)
+        ctx.save_for_backward(y, se, weights, x_cur, w_cg, indices, slots, kept)
+        ctx.meta = (capacity, mode, residual is not None)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        y, se, weights, x_cur, w_cg, indices, slots, kept = ctx.saved_tensors
+        capacity, mode, has_res = ctx.meta
+        dout = dout.contiguous()
+        t, k = indices.shape
+        n_exp = y.shape[0]
+        kept_sel = slots < capacity
+        d_se = d_xcur = d_wcg = None
+        c_rt = None
+        if mode == "direct_add":
+            d_se = dout if se is not None else None
+        else:
+            z = x_cur.float() @ w_cg.t()                       # (T, 1|2)
+            dse_dot = (dout.float() * se.float()).sum(1)
+            if mode == "cg1":
+                c = torch.sigmoid(z[:, 0])
+                d_se = (c[:, None] * dout.float()).to(dout.dtype)
+                dz = (dse_dot * c * (1 - c))[:, None]
+            else:
+                c = torch.softmax(z, dim=1)
+                routed = K.combine(y, indices, slots, weights.contiguous(), capacity)
+                drt_dot = (dout.float() * routed.float()).sum(1)
+                dc = torch.stack([dse_dot, drt_dot], 1)
+                dz = c * (dc - (c * dc).sum(1, keepdim=True))
+                d_se = (c[:, :1] * dout.float()).to(dout.dtype)
+                c_rt = c[:, 1]
+            d_wcg = dz.t() @ x_cur.float()
+            d_xcur = (dz @ w_cg).to(x_cur.dtype)
+        scale = weights.float() if c_rt is None else weights.float() * c_rt[:, None]
+        dy = K.dispatch_scaled(dout, indices, slots, n_exp, capacity, scale)
+        K.zero_tails(dy, kept, capacity)
+        d_weights = None
+        if k > 1:
+            # <d routed_t, y[e_j, slot_j]> for kept selections (c_rt folded in)
+            gathered = y[indices.long().clamp(max=n_exp - 1), slots.long().clamp(max=capacity - 1)]
+            dro = dout.float() if c_rt is None else dout.float() * c_rt[:, None]
+            d_weights = (gathered.float() * dro[:, None, :]).sum(-1) * kept_sel
+        return (dy, d_se, d_weights, d_xcur, d_wcg, (dout if has_res else None),
+                None, None, None, None, None)
+
+
+class ExchangeFn(torch.autograd.Function):
+    """Equal-split all-to-all of a destination-major (E, C, d) buffer; its
+    VJP is the reverse all-to-all (ep.exchange_rows is its own transpose)."""
+
+    @staticmethod
+    def forward(ctx, buf, group):
+        from . import ep
+        ctx.group = group
+        return ep.exchange_rows(buf, group)
+
+    @staticmethod
+    def backward(ctx, d):
+        from . import ep
+        return ep.exchange_rows(d.contiguous(), ctx.group), None
+
+
+def sgd_step(params, lr: float) -> None:
+    """In-place SGD (the reference's toy trainer, grad.py:330-331)."""
+    with torch.no_grad():
+        ps = [p for p in params if p.grad is not None]
+        if ps:
+            torch._foreach_add_(ps, [p.grad for p in ps], alpha=-lr)
+
+
+def allreduce_replicated_grads(module, group=None) -> None:
+    """Data-parallel all-reduce (mean) of the parameters every rank holds a
+    full copy of: everything except the sharded routed experts."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    ws = dist.get_world_size(group)
+    grads = [p.grad for n, p in module.named_parameters()
+             if p.grad is not None and ".experts." not in f".{n}"]
+    if not grads:
+        return
+    flat = torch._utils._flatten_dense_tensors(grads)
+    dist.all_reduce(flat, group=group)
+    flat.div_(ws)
+    for g, v in zip(grads, torch._utils._unflatten_dense_tensors(flat, grads)):
+        g.copy_(v)

@@ -215,12 +215,55 @@ def sched_cases(sched, distsim):
         json.dump(dict(vectors=vecs, timelines=timelines), fh)
 
 
+def grad_cases(arch, Rng):
+    """Loss and exact gradients of the reference objective (grad.backward,
+    grad.py:70-86; LossSpec mean / mse with aux_coeff 0.01) for block pairs
+    of every variant, plus the routing they were taken at."""
+    sys.path.insert(0, REF_SRC)
+    from scmoelab import grad
+    out, meta = {}, []
+    combos = [dict(variant="scmoe", shortcut_pos="pos2", combine_mode="direct_add", k_routed=1),
+              dict(variant="scmoe", shortcut_pos="pos1", combine_mode="cg1", k_routed=1),
+              dict(variant="scmoe", shortcut_pos="pos3", combine_mode="cg2", k_routed=1),
+              dict(variant="standard", k_routed=2),
+              dict(variant="shared", combine_mode="direct_add", k_routed=2)]
+    for i, kw in enumerate(combos):
+        t, d, h, n, cf = 20, 8, 16, 4, [2.0, 0.75][i % 2]
+        cfg = arch.ModelConfig(n_blocks=2, d_model=d, d_hidden=h, n_experts=n,
+                               capacity_factor=cf, **kw)
+        rng = Rng(300 + i)
+        params = arch.init_params(cfg, rng.spawn(0))
+        # non-zero biases so their gradients are exercised
+        for name, p in arch.named_parameters(params):
+            if name.endswith((".b1", ".b2")):
+                p += rng.spawn(5).normal(p.shape) * 0.1
+        tokens = rng.spawn(1).normal((t, d))
+        target = rng.spawn(2).normal((t, d)) if i % 2 else None
+        spec = grad.LossSpec(kind="mse", target=target) if target is not None else grad.LossSpec(kind="mean")
+        loss, grads, res = grad.backward(cfg, params, tokens, spec)
+        p = f"q{i}_"
+        out[p + "tokens"] = tokens
+        if target is not None:
+            out[p + "target"] = target
+        out[p + "loss"] = np.asarray(loss)
+        out[p + "idx"] = res.trace.moe[0].decision.indices.astype(np.int64)
+        out[p + "drop"] = res.trace.moe[0].decision.dropped
+        for name, arr in arch.named_parameters(params):
+            out[p + "P:" + name] = arr
+            out[p + "G:" + name] = grads[name]
+        meta.append(dict(t=t, d=d, h=h, n=n, cf=cf, seed=300 + i, mse=target is not None, **kw))
+    np.savez_compressed(os.path.join(HERE, "grad_cases.npz"), **out)
+    with open(os.path.join(HERE, "grad_cases.json"), "w") as fh:
+        json.dump(meta, fh, indent=0)
+
+
 def main():
     arch, distsim, gating, sched, Rng = _import_reference()
     gating_cases(gating, Rng)
     layer_and_pair_cases(arch, Rng)
     cfg1_case(arch, Rng)
     sched_cases(sched, distsim)
+    grad_cases(arch, Rng)
     print("golden vectors written to", HERE)
 
 

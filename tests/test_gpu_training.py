@@ -1,0 +1,121 @@
+"""Training step (K7) parity: gradients of the reference objective
+(loss + 0.01 * aux, grad.py:52-67) from the bf16 GPU backward vs the float64
+gradient oracle (oracle/grad_oracle.py, itself pinned to the reference's tape
+gradients), at the same bf16-rounded parameters and inputs, with the GPU's
+routing pinned (straight-through, tape.py:11-13).
+
+Tolerance: |g_gpu - g_ref| <= rtol * (|g_ref| + max|g_ref|) per parameter
+tensor with rtol = 5e-2 — the bf16 backward stacks several bf16 roundings of
+activations and gradients on top of the forward's 2e-2 budget.
+"""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import grad_oracle as G
+from oracle import scmoe_oracle as O
+
+pytestmark = pytest.mark.gpu
+P = None
+RTOL = 5e-2
+
+
+def setup_module(module):
+    global P
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2404_05019_b200 as pkg
+    P = pkg
+
+
+def _expert_items(prefix, w1t, b1, w2t, b2):
+    return {prefix + ".w1": w1t.t(), prefix + ".b1": b1.reshape(1, -1),
+            prefix + ".w2": w2t.t(), prefix + ".b2": b2.reshape(1, -1)}
+
+
+def _ref_view(blk, grad=False):
+    """Module tensors (or their .grad) under the reference's names/shapes."""
+    g = (lambda t: t.grad) if grad else (lambda t: t.detach())
+    d = blk.attn_prev.d_model
+    out = {}
+    for bi, att in ((0, blk.attn_prev), (1, blk.attn_cur)):
+        qkv = g(att.w_qkv_t)
+        for j, nm in enumerate(("w_q", "w_k", "w_v")):
+            out[f"block{bi}.attn.{nm}"] = qkv[j * d:(j + 1) * d].t()
+        out[f"block{bi}.attn.w_o"] = g(att.w_o_t).t()
+    m = blk.mlp_prev
+    out.update(_expert_items("block0.mlp", g(m.w1t), g(m.b1), g(m.w2t), g(m.b2)))
+    moe = blk.moe
+    e = moe.experts
+    for i in range(e.n_experts):
+        out.update(_expert_items(f"block1.moe.expert{i}", g(e.w1t)[i], g(e.b1)[i], g(e.w2t)[i],
+                                 g(e.b2)[i]))
+    if hasattr(moe, "shared"):
+        s = moe.shared
+        out.update(_expert_items("block1.moe.shared", g(s.w1t), g(s.b1), g(s.w2t), g(s.b2)))
+        if moe.w_cg is not None:
+            out["block1.moe.cg.w"] = g(moe.w_cg)
+    out["block1.moe.gate.w_gate"] = g(moe.gate.w_gate_t).t()
+    return {k: v.double().cpu().numpy() for k, v in out.items()}
+
+
+@pytest.mark.parametrize("variant,pos,mode,k,cf,mse", [
+    ("scmoe", "pos2", "direct_add", 1, 1.0, False), ("scmoe", "pos1", "cg1", 1, 2.0, True),
+    ("scmoe", "pos3", "cg2", 1, 0.75, False), ("standard", None, "direct_add", 2, 1.0, True),
+    ("shared", None, "direct_add", 2, 2.0, False)])
+def test_block_pair_gradients(variant, pos, mode, k, cf, mse):
+    T, d, h, N = 256, 128, 256, 4
+    pp = O.init_pair(d, h, N, O.Rng(17).spawn(0), variant=variant, k=k, combine_mode=mode)
+    cfg = SimpleNamespace(d_model=d, d_hidden=h, n_experts=N, variant=variant, shortcut_pos=pos,
+                          k_routed=k, combine_mode=mode, capacity_factor=cf, noise_enabled=False,
+                          pre_layernorm=False)
+    prev = SimpleNamespace(attn=pp.attn_prev, feed=pp.mlp_prev)
+    cur = SimpleNamespace(attn=pp.attn_cur, feed=pp.moe)
+    blk = P.ScMoEBlockPair.from_reference(cfg, prev, cur, dtype=torch.bfloat16)
+    with torch.no_grad():                       # non-zero biases exercise the bias grads
+        for prm in (blk.mlp_prev.b1, blk.moe.experts.b2):
+            prm.copy_(torch.randn_like(prm) * 0.1)
+    blk.requires_grad_(True)
+    x = torch.as_tensor(O.Rng(17).spawn(1).normal((T, d)), device="cuda").bfloat16()
+    target = torch.randn(T, d, device="cuda").bfloat16() if mse else None
+    params0 = _ref_view(blk)                    # bf16-rounded parameters, float64
+    out, dec, aux = blk(x)
+    loss = (out.float().mean() if target is None
+            else (out.float() - target.float()).pow(2).sum() / T) + 0.01 * aux
+    loss.backward()
+    torch.cuda.synchronize()
+    ref_loss, ref_grads = G.pair_grads(
+        params0, x.double().cpu().numpy(), variant=variant, pos=pos, n_experts=N, k=k,
+        combine_mode=mode, pinned_indices=dec.indices.long().cpu().numpy(),
+        pinned_dropped=dec.dropped.cpu().numpy(),
+        target=None if target is None else target.double().cpu())
+    assert float(loss) == pytest.approx(ref_loss, rel=2e-2, abs=1e-3)
+    got = _ref_view(blk, grad=True)
+    for name, ref in ref_grads.items():
+        if name not in got:
+            continue
+        gv = got[name]
+        bound = RTOL * (np.abs(ref) + np.abs(ref).max() + 1e-30)
+        worst = float((np.abs(gv - ref) / bound).max())
+        assert worst <= 1.0, f"{variant}/{mode} grad {name}: worst err/bound {worst:.3g}"
+
+
+def test_train_step_reduces_loss_and_updates():
+    """A few SGD steps of the reference objective on a fixed target lower the
+    loss (the reference's toy trainer, grad.py:296-333)."""
+    T, d, h, N = 512, 128, 256, 4
+    blk = P.ScMoEBlockPair(d, h, N, variant="scmoe", shortcut_pos="pos2", n_heads=2, seq_len=128,
+                           capacity_factor=1.25, dtype=torch.bfloat16,
+                           generator=torch.Generator(device="cuda").manual_seed(5))
+    blk.requires_grad_(True)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    target = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    w_before = blk.moe.experts.w1t.detach().clone()
+    losses = [float(blk.train_step(x, lr=0.05, target=target)) for _ in range(8)]
+    assert losses[-1] < losses[0]
+    assert not torch.equal(w_before, blk.moe.experts.w1t.detach())
+    assert all(np.isfinite(losses))
