@@ -248,6 +248,52 @@ def timed(fn, steps, ws, recorder_factory=None):
     return max_over_ranks(ms, ws), recs
 
 
+def bench_training(args, ws, rank, group):
+    """configs[1]: SwinV2-MoE-S stage-3 ScMoE block pair (d 384, h 1536, 12 heads,
+    12x12 windows = 144 tokens, 128 images = 18432 tokens per GPU, one expert
+    per GPU, cf 1.25, pos2, direct add), one bf16 training step = forward +
+    loss (mean + 0.01 aux, grad.py:52-67) + backward through the K7 kernels +
+    replicated-grad all-reduce + SGD.  Top-2 needs >= 2 experts, so the
+    same-box top-2 step is measured from N = 2 GPUs up."""
+    import torch
+    import paper_2404_05019_b200 as P
+    w = WORKLOADS["swinv2s"]
+    T = w["seq"] * w["seqs"]
+    n_exp = max(ws, 1)
+    common = dict(n_heads=w["heads"], seq_len=w["seq"], causal=False, dtype=torch.bfloat16,
+                  capacity_factor=w["cf"], ep_group=group)
+
+    def make(variant, k):
+        gen = torch.Generator(device="cuda").manual_seed(4321 + rank)
+        blk = P.ScMoEBlockPair(w["d"], w["h"], n_exp, variant=variant, k_routed=k,
+                               shortcut_pos=w["pos"] if variant == "scmoe" else None,
+                               generator=gen, **common)
+        return blk.requires_grad_(True)
+
+    gen = torch.Generator(device="cuda").manual_seed(77 + rank)
+    x = torch.randn(T, w["d"], device="cuda", generator=gen).bfloat16()
+    res = {"workload": w["name"].replace("(configs[1] shape, fwd)", "(configs[1])"),
+           "d_model": w["d"], "d_hidden": w["h"], "n_experts": n_exp, "tokens_per_gpu": T,
+           "capacity_factor": w["cf"], "step": "fwd + bwd + SGD (bf16)"}
+    sc = make("scmoe", 1)
+    for _ in range(args.warmup):
+        sc.train_step(x, lr=1e-4)
+    ms, _ = timed(lambda r: sc.train_step(x, lr=1e-4), args.steps, ws)
+    res.update(value=ws * T / (ms * 1e-3), unit="tokens/s", ms_per_step=ms)
+    if n_exp >= 2:
+        t2 = make("standard", 2)
+        for _ in range(args.warmup):
+            t2.train_step(x, lr=1e-4)
+        ms2, _ = timed(lambda r: t2.train_step(x, lr=1e-4), args.steps, ws)
+        res["top2"] = {"value": ws * T / (ms2 * 1e-3), "ms_per_step": ms2}
+        res["speedup_vs_top2"] = ms2 / ms
+    else:
+        res["top2"] = None
+        res["note"] = "one expert per GPU: top-2 routing needs >= 2 GPUs"
+    del sc
+    return res
+
+
 def run_ours(args):
     import torch
     import paper_2404_05019_b200 as P
@@ -274,11 +320,11 @@ def run_ours(args):
             t2(x)
         torch.cuda.synchronize()
 
-        # ---- ScMoE block pair, device-timed, clocks sampled ----------------
-        with Clocks(local) as clk:
-            ms_sc, recs = timed(lambda r: sc(x, recorder=r), args.steps, ws,
-                                recorder_factory=lambda: Recorder())
-        clocks = clk.summary()
+        # ---- ScMoE block pair, device-timed; clocks sampled over every
+        # timed region below (nvidia-smi, 200 ms) -----------------------------
+        clk = Clocks(local).__enter__()
+        ms_sc, recs = timed(lambda r: sc(x, recorder=r), args.steps, ws,
+                            recorder_factory=lambda: Recorder())
         # ---- top-2 baseline, same box, same kernels -------------------------
         ms_t2, recs2 = timed(lambda r: t2(x, recorder=r), args.steps, ws,
                              recorder_factory=lambda: Recorder())
@@ -309,6 +355,11 @@ def run_ours(args):
             torch.cuda.synchronize()
             barrier(ws)
             e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+
+    # ---- configs[1]: SwinV2-MoE-S stage-3 ScMoE block, bf16 training step ----
+    training = None if args.no_training else bench_training(args, ws, rank, group)
+    clk.__exit__(None, None, None)
+    clocks = clk.summary()
 
     # spans -> per-op durations, overlap, dominant-kernel roofline
     spans = [r.spans() for r in recs]
@@ -367,6 +418,7 @@ def run_ours(args):
                      "flops_per_launch": flops_per_launch, "peak_source": peak_src},
         "clocks": clocks,
         "gpu_launches": args.steps * 13,
+        "training": training,
     }
     if e2e_ms is not None:
         line["e2e"] = {"value": ws * T / (e2e_ms * 1e-3), "unit": "tokens/s",
@@ -395,6 +447,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gpt3xl")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-training", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--cpu-reps", type=int, default=3)
