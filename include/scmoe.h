@@ -157,9 +157,12 @@ int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out, voi
 int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_cap, int cols,
                      const int32_t* group_rows, int rows_clip, int align, void* stream);
 
-/* out[g, c] = sum_{r < rows(g)} x[g, r, c] in fp32 (bias gradients) */
+/* out[g, c] = sum_{r < rows(g)} x[g, r, c] in fp32 (bias gradients), two
+ * deterministic passes through a caller-owned workspace */
+size_t scmoe_grouped_colsum_workspace_bytes(int num_groups, int group_cap, int cols);
 int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap, int cols,
-                         const int32_t* group_rows, int rows_clip, float* out, void* stream);
+                         const int32_t* group_rows, int rows_clip, float* out,
+                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */

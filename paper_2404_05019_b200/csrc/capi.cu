@@ -55,26 +55,43 @@ __global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs
     base[i] = make_uint4(0, 0, 0, 0);
 }
 
-// out[g, c] = sum_{r < rows(g)} x[g, r, c]  (fp32), bf16 or fp32 input
+// Column sums over the valid rows of each group, two deterministic passes:
+// pass 1: block (group, row chunk of COLSUM_ROWS, 256-column tile) -> partial
+//         sums (each thread one column, 8 rows in flight, coalesced rows);
+// pass 2: fixed-order sum of the chunk partials.
+constexpr int COLSUM_ROWS = 128;
+
 template <typename T>
-__global__ void grouped_colsum_kernel(const T* __restrict__ x, int cap, int cols,
+__global__ void colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
                                       const int32_t* __restrict__ group_rows, int rows_clip,
-                                      float* __restrict__ out) {
-  const int g = blockIdx.y;
+                                      int n_chunks, float* __restrict__ part) {
+  const int g = blockIdx.z;
+  const int chunk = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
-  const int rows = group_rows ? min(group_rows[g], rows_clip) : cap;
-  const T* p = x + (long long)g * cap * cols + c;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  int r = 0;
-  for (; r + 4 <= rows; r += 4) {
-    s0 += to_f32(p[(long long)r * cols]);
-    s1 += to_f32(p[(long long)(r + 1) * cols]);
-    s2 += to_f32(p[(long long)(r + 2) * cols]);
-    s3 += to_f32(p[(long long)(r + 3) * cols]);
+  const int rows = group_rows ? max(0, min(group_rows[g], rows_clip)) : cap;
+  const int r0 = chunk * COLSUM_ROWS, r1 = min(rows, r0 + COLSUM_ROWS);
+  const T* p = x + ((long long)g * cap) * cols + c;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += to_f32(p[(long long)(r + u) * cols]);
   }
-  for (; r < rows; ++r) s0 += to_f32(p[(long long)r * cols]);
-  out[(long long)g * cols + c] = (s0 + s1) + (s2 + s3);
+  for (; r < r1; ++r) s[0] += to_f32(p[(long long)r * cols]);
+  part[((long long)g * n_chunks + chunk) * cols + c] =
+      ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ part, int n_chunks, int cols,
+                                    int n_groups, float* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)n_groups * cols) return;
+  const int g = (int)(i / cols), c = (int)(i - (long long)g * cols);
+  const float* p = part + (long long)g * n_chunks * cols + c;
+  float s = 0.f;
+  for (int k = 0; k < n_chunks; ++k) s += p[(long long)k * cols];
+  out[i] = s;
 }
 
 }  // namespace
@@ -192,19 +209,35 @@ extern "C" int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_
   return SCMOE_OK;
 }
 
+extern "C" size_t scmoe_grouped_colsum_workspace_bytes(int num_groups, int group_cap, int cols) {
+  const size_t chunks = (size_t)((group_cap + COLSUM_ROWS - 1) / COLSUM_ROWS);
+  return chunks * (size_t)num_groups * (size_t)cols * sizeof(float);
+}
+
 extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap,
                                     int cols, const int32_t* group_rows, int rows_clip,
-                                    float* out, void* stream) {
+                                    float* out, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
   SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
-  SCMOE_CHECK_ARG(num_groups >= 1 && cols >= 1, "bad colsum shape");
+  SCMOE_CHECK_ARG(num_groups >= 1 && cols >= 1 && group_cap >= 1, "bad colsum shape");
+  SCMOE_CHECK_ARG(workspace_bytes >= scmoe_grouped_colsum_workspace_bytes(num_groups, group_cap,
+                                                                          cols),
+                  "colsum workspace too small");
   if (rows_clip <= 0) rows_clip = group_cap;
-  dim3 grid((cols + 127) / 128, num_groups);
+  const int n_chunks = (group_cap + COLSUM_ROWS - 1) / COLSUM_ROWS;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((cols + 255) / 256, n_chunks, num_groups);
+  float* part = (float*)workspace;
   if (dtype == SCMOE_BF16)
-    grouped_colsum_kernel<__nv_bfloat16><<<grid, 128, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, out);
+    colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, n_chunks, part);
   else
-    grouped_colsum_kernel<float><<<grid, 128, 0, (cudaStream_t)stream>>>(
-        (const float*)x, group_cap, cols, group_rows, rows_clip, out);
+    colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)x, group_cap, cols,
+                                                       group_rows, rows_clip, n_chunks, part);
+  SCMOE_LAUNCH_CHECK();
+  const long long n = (long long)num_groups * cols;
+  colsum_final_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n_chunks, cols,
+                                                                   num_groups, out);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

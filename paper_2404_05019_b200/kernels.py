@@ -242,8 +242,11 @@ def grouped_colsum(x: torch.Tensor, group_rows: Optional[torch.Tensor] = None, r
     x3 = x if x.dim() == 3 else x.unsqueeze(0)
     G, C, D = x3.shape
     out = torch.empty(G, D, device=x.device, dtype=torch.float32)
+    ws_bytes = lib().scmoe_grouped_colsum_workspace_bytes(G, C, D)
+    ws = torch.empty(ws_bytes, device=x.device, dtype=torch.uint8)
     check(lib().scmoe_grouped_colsum(ptr(_c(x3, "x")), dtype_code(x.dtype), G, C, D,
-                                     ptr(group_rows), rows_clip, ptr(out), stream_ptr(stream)))
+                                     ptr(group_rows), rows_clip, ptr(out), ptr(ws), ws_bytes,
+                                     stream_ptr(stream)))
     return out if x.dim() == 3 else out.view(D)
 
 
