@@ -449,3 +449,95 @@ def allclose_scaled(a, b, rtol: float) -> Tuple[bool, float]:
     bound = np.where(bound == 0, 1e-300, bound)
     worst = float(np.max(np.abs(a - b) / bound)) if b.size else 0.0
     return worst <= 1.0, worst
+
+
+# ---------------------------------------------------------------------------
+# whole model (scmoelab/arch.py:167-196 init, 553-665 model_forward)
+
+
+@dataclass
+class BlockP:
+    attn: Attention
+    feed: object          # Expert (Block-MLP) or Layer (Block-MoE)
+
+
+def init_model(n_blocks: int, d: int, h: int, n_experts: int, rng: Rng,
+               moe_frequency: str = "every-second-block", variant: str = "scmoe", k: int = 1,
+               combine_mode: str = "direct_add", noise_enabled: bool = False):
+    """init_params draw order for any block count (arch.py:167-196): per block
+    attention (4 x (d,d)), then the feed: Block-MLP (W1, W2) or the MoE layer
+    (N experts, shared, W_gate, W_noise, W_cg).  MoE blocks are the odd ones
+    (every-second-block) or all (every-block), arch.py:193-196."""
+    s = 1.0 / np.sqrt(d)
+
+    def expert():
+        w1 = rng.normal((d, h)) * s
+        w2 = rng.normal((h, d)) * s
+        return Expert(w1, np.zeros((1, h)), w2, np.zeros((1, d)))
+
+    blocks = []
+    for i in range(n_blocks):
+        attn = Attention(*(rng.normal((d, d)) * s for _ in range(4)))
+        is_moe = moe_frequency == "every-block" or i % 2 == 1
+        if is_moe:
+            experts = [expert() for _ in range(n_experts)]
+            shared = expert() if variant in ("shared", "scmoe") else None
+            wg = rng.normal((d, n_experts)) * s
+            wn = rng.normal((d, n_experts)) * s
+            w_cg = None
+            if combine_mode != "direct_add":
+                w_cg = rng.normal((1 if combine_mode == "cg1" else 2, d)) * s
+            feed = Layer(experts, Gate(wg, wn, k, noise_enabled), combine_mode, w_cg, shared)
+        else:
+            feed = expert()
+        blocks.append(BlockP(attn, feed))
+    return blocks
+
+
+def model_forward(blocks, tokens, variant: str, pos: Optional[str], capacity_factor: float,
+                  k: int, moe_frequency: str = "every-second-block",
+                  first_layer_pos1: bool = False, pre_layernorm: bool = False,
+                  pinned=None):
+    """arch.model_forward (arch.py:553-665) value mode; `pinned` is an optional
+    list of (indices, dropped) per MoE layer.  Returns (out, decisions, auxes)."""
+    d = tokens.shape[1]
+    feed = layer_norm if pre_layernorm else (lambda z: z)
+    h = np.asarray(tokens, dtype=np.float64)
+    decs, auxes = [], []
+
+    def moe_call(layer, x_cur, src, j):
+        kw = {}
+        if pinned is not None:
+            kw = dict(pinned_indices=pinned[j][0], pinned_dropped=pinned[j][1])
+        if variant == "scmoe":
+            return moe_shared(x_cur, layer, capacity_factor, k, routed_src=src, **kw)
+        if variant == "shared":
+            return moe_shared(x_cur, layer, capacity_factor, k, **kw)
+        return moe_standard(x_cur, layer, capacity_factor, k, **kw)
+
+    if moe_frequency == "every-second-block":
+        for pair in range(len(blocks) // 2):
+            prev_b, cur_b = blocks[2 * pair], blocks[2 * pair + 1]
+            h_in = h
+            h_mh_prev = h_in + attention_forward(feed(h_in), prev_b.attn, d)
+            h_mlp_prev = h_mh_prev + expert_forward(feed(h_mh_prev), prev_b.feed)
+            h_mh_cur = h_mlp_prev + attention_forward(feed(h_mlp_prev), cur_b.attn, d)
+            x_cur = feed(h_mh_cur)
+            p = "pos1" if (variant == "scmoe" and first_layer_pos1 and pair == 0) else pos
+            src = {"pos1": h_mlp_prev, "pos2": h_mh_prev, "pos3": h_in}.get(p, x_cur) \
+                if variant == "scmoe" else x_cur
+            f, dec, aux = moe_call(cur_b.feed, x_cur, src, pair)
+            decs.append(dec)
+            auxes.append(aux)
+            h = h_mh_cur + f
+    else:
+        for i, b in enumerate(blocks):
+            h_in = h
+            h_mh = h_in + attention_forward(feed(h_in), b.attn, d)
+            x_cur = feed(h_mh)
+            src = h_in if variant == "scmoe" else x_cur
+            f, dec, aux = moe_call(b.feed, x_cur, src, i)
+            decs.append(dec)
+            auxes.append(aux)
+            h = h_mh + f
+    return h, decs, auxes

@@ -10,3 +10,5 @@ from . import sched, timeline, ep
 __all__ = ["CapacityConfig", "ConfigError", "GateDecision", "MoEReplay", "RoutedExperts",
            "ScMoELayer", "SharedExpert", "Top1Gate", "Top2MoELayer", "expert_quota",
            "Attention", "ScMoEBlockPair", "sched", "timeline", "ep"]
+from .block import ScMoEBlock, ScMoEModel
+__all__ += ["ScMoEBlock", "ScMoEModel"]

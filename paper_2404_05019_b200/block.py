@@ -100,6 +100,8 @@ class Attention(nn.Module):
 class ScMoEBlockPair(nn.Module):
     """Block-MLP followed by a Block-MoE (ScMoE / shared-expert / top-k)."""
 
+    _PAIR = True        # ScMoEBlock (every-block placement) drops the Block-MLP half
+
     def __init__(self, d_model: int, d_hidden: int, n_experts: int, variant: str = "scmoe",
                  shortcut_pos: Optional[str] = "pos2", k_routed: int = 1,
                  combine_mode: str = "direct_add", capacity_factor: float = 2.0,
@@ -118,9 +120,12 @@ class ScMoEBlockPair(nn.Module):
         self.variant, self.shortcut_pos = variant, shortcut_pos
         self.pre_layernorm = pre_layernorm
         self.dtype = dtype
+        if not self._PAIR and variant == "scmoe" and shortcut_pos != "pos1":
+            raise ConfigError("every-block shortcut placement supports pos1 only")  # arch.py:72-74
         kw = dict(dtype=dtype, device=device, generator=generator)
-        self.attn_prev = Attention(d_model, n_heads, seq_len, causal, **kw)
-        self.mlp_prev = SharedExpert(d_model, d_hidden, **kw)
+        if self._PAIR:
+            self.attn_prev = Attention(d_model, n_heads, seq_len, causal, **kw)
+            self.mlp_prev = SharedExpert(d_model, d_hidden, **kw)
         self.attn_cur = Attention(d_model, n_heads, seq_len, causal, **kw)
         if variant == "standard":
             self.moe = Top2MoELayer(d_model, d_hidden, n_experts, k_routed=k_routed,
@@ -138,17 +143,19 @@ class ScMoEBlockPair(nn.Module):
     # -- construction from the reference's parameter tree --------------------
     @classmethod
     def from_reference(cls, cfg, prev_blk, cur_blk, dtype=torch.bfloat16, device=None,
-                       n_heads: int = 1, seq_len=None, causal=False, ep_group=None):
-        """cfg: reference ModelConfig; prev_blk/cur_blk: BlockParams of one pair."""
-        import numpy as np
+                       n_heads: int = 1, seq_len=None, causal=False, ep_group=None,
+                       shortcut_pos: Optional[str] = None):
+        """cfg: reference ModelConfig; prev_blk/cur_blk: BlockParams of one pair
+        (prev_blk is ignored by the single-block ScMoEBlock)."""
         m = cls(cfg.d_model, cfg.d_hidden, cfg.n_experts, variant=cfg.variant,
-                shortcut_pos=cfg.shortcut_pos, k_routed=cfg.k_routed,
+                shortcut_pos=shortcut_pos or cfg.shortcut_pos, k_routed=cfg.k_routed,
                 combine_mode=cfg.combine_mode, capacity_factor=cfg.capacity_factor,
                 noise_enabled=cfg.noise_enabled, pre_layernorm=cfg.pre_layernorm,
                 n_heads=n_heads, seq_len=seq_len, causal=causal, dtype=dtype, device=device,
                 ep_group=ep_group)
-        m.attn_prev.load_reference(prev_blk.attn)
-        m.mlp_prev.load_reference(prev_blk.feed)
+        if cls._PAIR:
+            m.attn_prev.load_reference(prev_blk.attn)
+            m.mlp_prev.load_reference(prev_blk.feed)
         m.attn_cur.load_reference(cur_blk.attn)
         cap = CapacityConfig(cfg.capacity_factor)
         layer = cur_blk.feed
@@ -171,10 +178,13 @@ class ScMoEBlockPair(nn.Module):
 
     def order(self):
         if self.variant == "scmoe":
-            return sched.issue_order(self.shortcut_pos, self.slot if self.slot is not None else 0)
-        o = sched.sequential_order()
-        if self.variant == "standard":
-            o.remove("shared")
+            o = sched.issue_order(self.shortcut_pos, self.slot if self.slot is not None else 0)
+        else:
+            o = sched.sequential_order()
+            if self.variant == "standard":
+                o.remove("shared")
+        if not self._PAIR:
+            o = [n for n in o if n not in ("attn_prev", "mlp_prev")]
         return o
 
     # -- forward -------------------------------------------------------------
@@ -209,6 +219,10 @@ class ScMoEBlockPair(nn.Module):
             return env["x_cur"]
 
         env["h_in"] = h_in
+        if not self._PAIR:
+            # every-block: the block input plays the preceding block's output
+            # (src = h_in, arch.py:640) and attention reads it directly
+            env["h_mh_prev"] = env["h_mlp_prev"] = h_in
         train = moe.training_path()
         if train:
             from . import training as TR
@@ -333,7 +347,8 @@ class ScMoEBlockPair(nn.Module):
             self.forward(h_in, recorder=rec)
             for k, v in rec.durations().items():
                 durs[k] = min(durs.get(k, float("inf")), v)
-        window = list(sched.WINDOW_OPS[self.shortcut_pos])
+        window = [n for n in sched.WINDOW_OPS[self.shortcut_pos]
+                  if self._PAIR or n not in ("attn_prev", "mlp_prev")]
         comm_d = durs.get("dispatch", 0.0)
         comm_c = durs.get("combine", 0.0)
         expert_ms = durs.get("expert", 0.0)
@@ -346,3 +361,117 @@ class ScMoEBlockPair(nn.Module):
         self.slot = choice.slot
         self.last_costs = cv
         return choice
+
+
+class ScMoEBlock(ScMoEBlockPair):
+    """One Transformer block whose feed is the MoE layer — the every-block
+    placement (moe_frequency "every-block", arch.py:632-663):
+
+        h_mh = h_in + Attn(feed(h_in));  out = h_mh + MoE(feed(h_mh), src)
+
+    with src = h_in (ScMoE pos1, the previous block's output), else feed(h_mh).
+    The gate and dispatch of the ScMoE variant only need h_in, so they are
+    issued before the attention and the all-to-alls overlap attention + SE."""
+
+    _PAIR = False
+
+    def __init__(self, d_model: int, d_hidden: int, n_experts: int, variant: str = "scmoe",
+                 shortcut_pos: Optional[str] = "pos1", **kw):
+        super().__init__(d_model, d_hidden, n_experts, variant=variant,
+                         shortcut_pos=shortcut_pos, **kw)
+
+
+class ScMoEModel(nn.Module):
+    """The reference's model (arch.model_forward, arch.py:553-665) on the GPU:
+    n_blocks Transformer blocks with the MoE feed every second block (block
+    pairs, ScMoEBlockPair) or every block (ScMoEBlock).  Constructor fields
+    are ModelConfig's (arch.py:39-54); `first_layer_pos1` routes the first
+    pair from pos1 (arch.py:594-595).  forward -> (out, decisions, auxes)."""
+
+    def __init__(self, n_blocks: int, d_model: int, d_hidden: int, n_experts: int,
+                 k_routed: int = 1, moe_frequency: str = "every-second-block",
+                 variant: str = "standard", shortcut_pos: Optional[str] = None,
+                 combine_mode: str = "direct_add", capacity_factor: float = 2.0,
+                 noise_enabled: bool = False, first_layer_pos1: bool = False,
+                 pre_layernorm: bool = False, n_heads: int = 1, seq_len: Optional[int] = None,
+                 causal: bool = False, dtype=torch.bfloat16, device=None, generator=None,
+                 ep_group=None, _build: bool = True):
+        super().__init__()
+        if moe_frequency not in ("every-second-block", "every-block"):
+            raise ConfigError(f"unknown moe_frequency {moe_frequency!r}")
+        if moe_frequency == "every-second-block" and n_blocks % 2:
+            raise ConfigError("every-second-block placement needs an even block count")
+        if variant == "scmoe" and moe_frequency == "every-block" and shortcut_pos != "pos1":
+            raise ConfigError("every-block shortcut placement supports pos1 only")
+        self.moe_frequency, self.variant = moe_frequency, variant
+        kw = dict(k_routed=k_routed, combine_mode=combine_mode, capacity_factor=capacity_factor,
+                  noise_enabled=noise_enabled, pre_layernorm=pre_layernorm, n_heads=n_heads,
+                  seq_len=seq_len, causal=causal, dtype=dtype, device=device,
+                  generator=generator, ep_group=ep_group)
+        blocks = []
+        if _build:
+            if moe_frequency == "every-second-block":
+                for pair in range(n_blocks // 2):
+                    pos = shortcut_pos
+                    if variant == "scmoe" and first_layer_pos1 and pair == 0:
+                        pos = "pos1"
+                    blocks.append(ScMoEBlockPair(d_model, d_hidden, n_experts, variant=variant,
+                                                 shortcut_pos=pos, **kw))
+            else:
+                for _ in range(n_blocks):
+                    blocks.append(ScMoEBlock(d_model, d_hidden, n_experts, variant=variant,
+                                             shortcut_pos=shortcut_pos, **kw))
+        self.blocks = nn.ModuleList(blocks)
+
+    @classmethod
+    def from_reference(cls, cfg, params, dtype=torch.bfloat16, device=None, n_heads: int = 1,
+                       seq_len=None, causal=False, ep_group=None):
+        """cfg: reference ModelConfig; params: ModelParams (arch.py:150-151)."""
+        m = cls(cfg.n_blocks, cfg.d_model, cfg.d_hidden, cfg.n_experts, k_routed=cfg.k_routed,
+                moe_frequency=cfg.moe_frequency, variant=cfg.variant,
+                shortcut_pos=cfg.shortcut_pos, combine_mode=cfg.combine_mode,
+                capacity_factor=cfg.capacity_factor, noise_enabled=cfg.noise_enabled,
+                first_layer_pos1=cfg.first_layer_pos1, pre_layernorm=cfg.pre_layernorm,
+                n_heads=n_heads, seq_len=seq_len, causal=causal, dtype=dtype, device=device,
+                ep_group=ep_group, _build=False)
+        kw = dict(dtype=dtype, device=device, n_heads=n_heads, seq_len=seq_len, causal=causal,
+                  ep_group=ep_group)
+        blocks = list(params.blocks)
+        if cfg.moe_frequency == "every-second-block":
+            for pair in range(cfg.n_blocks // 2):
+                pos = "pos1" if (cfg.variant == "scmoe" and cfg.first_layer_pos1 and pair == 0) \
+                    else None
+                m.blocks.append(ScMoEBlockPair.from_reference(
+                    cfg, blocks[2 * pair], blocks[2 * pair + 1], shortcut_pos=pos, **kw))
+        else:
+            for b in blocks:
+                m.blocks.append(ScMoEBlock.from_reference(cfg, None, b, **kw))
+        return m
+
+    def forward(self, tokens: torch.Tensor, replay=None):
+        h = tokens
+        decs, auxes = [], []
+        for i, blk in enumerate(self.blocks):
+            h, dec, aux = blk(h, replay=None if replay is None else replay[i])
+            decs.append(dec)
+            auxes.append(aux)
+        return h, decs, auxes
+
+    def train_step(self, tokens: torch.Tensor, lr: float = 0.01, aux_coeff: float = 0.01,
+                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True):
+        """grad.compute_loss (mean / mse + aux_coeff * sum aux) + SGD."""
+        from . import training as TR
+        for p in self.parameters():
+            p.grad = None
+        out, _, auxes = self(tokens)
+        loss = out.float().mean() if target is None else \
+            (out.float() - target.float()).pow(2).sum() / out.shape[0]
+        for a in auxes:
+            loss = loss + aux_coeff * a
+        loss.backward()
+        ep = self.blocks[0].ep_group if len(self.blocks) else None
+        if dp_group is not None or ep is not None:
+            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else ep)
+        if update:
+            TR.sgd_step(self.parameters(), lr)
+        return loss.detach()

@@ -61,26 +61,47 @@ __global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs
 // pass 2: fixed-order sum of the chunk partials.
 constexpr int COLSUM_ROWS = 128;
 
+// each thread owns one 16-byte column vector (8 bf16 / 4 fp32) and keeps 4
+// row loads in flight; cols must be a multiple of the vector width
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
                                       const int32_t* __restrict__ group_rows, int rows_clip,
                                       int n_chunks, float* __restrict__ part) {
+  constexpr int VEC = Vec16<T>::N;
   const int g = blockIdx.z;
   const int chunk = blockIdx.y;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (c >= cols) return;
   const int rows = group_rows ? max(0, min(group_rows[g], rows_clip)) : cap;
   const int r0 = chunk * COLSUM_ROWS, r1 = min(rows, r0 + COLSUM_ROWS);
   const T* p = x + ((long long)g * cap) * cols + c;
-  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float s[4][VEC] = {};
   int r = r0;
-  for (; r + 8 <= r1; r += 8) {
+  for (; r + 4 <= r1; r += 4) {
+    uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] += to_f32(p[(long long)(r + u) * cols]);
+    for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(p + (long long)(r + u) * cols);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      Vec16<T> w;
+      w.raw = v[u];
+      float f[VEC];
+      w.to_float(f);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) s[u][i] += f[i];
+    }
   }
-  for (; r < r1; ++r) s[0] += to_f32(p[(long long)r * cols]);
-  part[((long long)g * n_chunks + chunk) * cols + c] =
-      ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  for (; r < r1; ++r) {
+    Vec16<T> w;
+    w.raw = ld_nc_v4(p + (long long)r * cols);
+    float f[VEC];
+    w.to_float(f);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) s[0][i] += f[i];
+  }
+  float* o = part + ((long long)g * n_chunks + chunk) * cols + c;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) o[i] = (s[0][i] + s[1][i]) + (s[2][i] + s[3][i]);
 }
 
 __global__ void colsum_final_kernel(const float* __restrict__ part, int n_chunks, int cols,
@@ -224,15 +245,20 @@ extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, in
                                                                           cols),
                   "colsum workspace too small");
   if (rows_clip <= 0) rows_clip = group_cap;
+  const int vec = dtype == SCMOE_BF16 ? 8 : 4;
+  SCMOE_CHECK_ARG(cols % vec == 0 && ((uintptr_t)x & 15) == 0,
+                  "colsum needs 16-byte aligned rows (cols multiple of %d)", vec);
   const int n_chunks = (group_cap + COLSUM_ROWS - 1) / COLSUM_ROWS;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid((cols + 255) / 256, n_chunks, num_groups);
+  const int vecs = cols / vec;
+  const int threads = vecs < 128 ? ((vecs + 31) / 32) * 32 : 128;
+  dim3 grid((vecs + threads - 1) / threads, n_chunks, num_groups);
   float* part = (float*)workspace;
   if (dtype == SCMOE_BF16)
-    colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+    colsum_partial_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
         (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, n_chunks, part);
   else
-    colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)x, group_cap, cols,
+    colsum_partial_kernel<float><<<grid, threads, 0, st>>>((const float*)x, group_cap, cols,
                                                        group_rows, rows_clip, n_chunks, part);
   SCMOE_LAUNCH_CHECK();
   const long long n = (long long)num_groups * cols;

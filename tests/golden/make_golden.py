@@ -257,8 +257,39 @@ def grad_cases(arch, Rng):
         json.dump(meta, fh, indent=0)
 
 
+def model_cases(arch, Rng):
+    """Whole-model forwards (arch.forward, arch.py:553-675): stacks of pairs
+    with first_layer_pos1, every-block placement (pos1, every variant)."""
+    out, meta = {}, []
+    combos = [dict(n_blocks=4, variant="scmoe", shortcut_pos="pos2", first_layer_pos1=True),
+              dict(n_blocks=4, variant="scmoe", shortcut_pos="pos3", combine_mode="cg1"),
+              dict(n_blocks=3, variant="scmoe", shortcut_pos="pos1", moe_frequency="every-block"),
+              dict(n_blocks=2, variant="standard", k_routed=2, moe_frequency="every-block"),
+              dict(n_blocks=3, variant="shared", moe_frequency="every-block", combine_mode="cg2",
+                   pre_layernorm=True)]
+    for i, kw in enumerate(combos):
+        t, d, h, n = 24, 8, 16, 4
+        cfg = arch.ModelConfig(d_model=d, d_hidden=h, n_experts=n, capacity_factor=1.0, **kw)
+        rng = Rng(500 + i)
+        params = arch.init_params(cfg, rng.spawn(0))
+        tokens = rng.spawn(1).normal((t, d))
+        o, trace = arch.forward(cfg, params, tokens)
+        p = f"m{i}_"
+        out[p + "tokens"] = tokens
+        out[p + "out"] = o
+        for j, m in enumerate(trace.moe):
+            out[p + f"idx{j}"] = m.decision.indices.astype(np.int64)
+            out[p + f"drop{j}"] = m.decision.dropped
+            out[p + f"aux{j}"] = np.asarray(m.aux_loss)
+        meta.append(dict(t=t, d=d, h=h, n=n, cf=1.0, seed=500 + i, n_moe=len(trace.moe), **kw))
+    np.savez_compressed(os.path.join(HERE, "model_cases.npz"), **out)
+    with open(os.path.join(HERE, "model_cases.json"), "w") as fh:
+        json.dump(meta, fh, indent=0)
+
+
 def main():
     arch, distsim, gating, sched, Rng = _import_reference()
+    model_cases(arch, Rng)
     gating_cases(gating, Rng)
     layer_and_pair_cases(arch, Rng)
     cfg1_case(arch, Rng)

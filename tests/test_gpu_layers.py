@@ -261,3 +261,59 @@ def test_host_stream_runner_matches_direct_forward():
     torch.cuda.synchronize()
     for x, o in zip(xs, outs):
         assert torch.equal(o, blk(x.cuda())[0].cpu())
+
+
+@pytest.mark.parametrize("kw", [
+    dict(n_blocks=4, variant="scmoe", shortcut_pos="pos2", first_layer_pos1=True),
+    dict(n_blocks=3, variant="scmoe", shortcut_pos="pos1", moe_frequency="every-block"),
+    dict(n_blocks=2, variant="standard", k_routed=2, moe_frequency="every-block"),
+    dict(n_blocks=2, variant="shared", combine_mode="cg2", moe_frequency="every-block",
+         pre_layernorm=True),
+    dict(n_blocks=2, variant="scmoe", shortcut_pos="pos3", combine_mode="cg1")])
+def test_model_matches_oracle_fp32(kw):
+    """ScMoEModel (arch.model_forward on the GPU): pair stacks, first_layer_pos1,
+    every-block placement, pre-LN — fp32 rtol 1e-4 with routing pinned."""
+    T, d, h, N, cf = 256, 128, 256, 4, 1.0
+    freq = kw.get("moe_frequency", "every-second-block")
+    k = kw.get("k_routed", 1)
+    blocks = O.init_model(kw["n_blocks"], d, h, N, O.Rng(21).spawn(0), moe_frequency=freq,
+                          variant=kw["variant"], k=k, combine_mode=kw.get("combine_mode", "direct_add"))
+    cfg = SimpleNamespace(n_blocks=kw["n_blocks"], d_model=d, d_hidden=h, n_experts=N, k_routed=k,
+                          moe_frequency=freq, variant=kw["variant"],
+                          shortcut_pos=kw.get("shortcut_pos"),
+                          combine_mode=kw.get("combine_mode", "direct_add"), capacity_factor=cf,
+                          noise_enabled=False, first_layer_pos1=kw.get("first_layer_pos1", False),
+                          pre_layernorm=kw.get("pre_layernorm", False))
+    model = P.ScMoEModel.from_reference(cfg, SimpleNamespace(blocks=blocks), dtype=torch.float32)
+    tokens = O.Rng(21).spawn(1).normal((T, d))
+    out, decs, auxes = model(_t(tokens, torch.float32))
+    torch.cuda.synchronize()
+    pinned = [(dd.indices.long().cpu().numpy(), dd.dropped.cpu().numpy()) for dd in decs]
+    ref, rdecs, rauxes = O.model_forward(blocks, tokens, kw["variant"], kw.get("shortcut_pos"), cf,
+                                         k, moe_frequency=freq,
+                                         first_layer_pos1=kw.get("first_layer_pos1", False),
+                                         pre_layernorm=kw.get("pre_layernorm", False),
+                                         pinned=pinned)
+    _check(out.double().cpu().numpy(), ref, 1e-4, f"model {kw}")
+    for a, ra in zip(auxes, rauxes):
+        assert float(a) == pytest.approx(ra, rel=1e-4, abs=1e-5)
+    free = O.model_forward(blocks, tokens, kw["variant"], kw.get("shortcut_pos"), cf, k,
+                           moe_frequency=freq, first_layer_pos1=kw.get("first_layer_pos1", False),
+                           pre_layernorm=kw.get("pre_layernorm", False))[1]
+    for dd, fd in zip(decs, free):
+        assert (dd.indices.long().cpu().numpy() == fd.indices).mean() > 0.97
+
+
+def test_every_block_training_step():
+    """configs[3]-style every-block ScMoE (pos1) trains through the K7 kernels."""
+    model = P.ScMoEModel(2, 128, 256, 4, moe_frequency="every-block", variant="scmoe",
+                         shortcut_pos="pos1", n_heads=2, seq_len=128, capacity_factor=2.0,
+                         dtype=torch.bfloat16,
+                         generator=torch.Generator(device="cuda").manual_seed(3))
+    model.requires_grad_(True)
+    x = torch.randn(256, 128, device="cuda").bfloat16()
+    tgt = torch.randn(256, 128, device="cuda").bfloat16()
+    losses = [float(model.train_step(x, lr=2e-3, target=tgt)) for _ in range(6)]
+    assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
+    for p in model.parameters():
+        assert p.grad is not None
