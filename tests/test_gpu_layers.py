@@ -315,5 +315,6 @@ def test_every_block_training_step():
     tgt = torch.randn(256, 128, device="cuda").bfloat16()
     losses = [float(model.train_step(x, lr=2e-3, target=tgt)) for _ in range(6)]
     assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
-    for p in model.parameters():
-        assert p.grad is not None
+    for blk in model.blocks:
+        for p in (blk.attn_cur.w_qkv_t, blk.moe.experts.w1t, blk.moe.shared.b2, blk.moe.gate.w_gate_t):
+            assert p.grad is not None and torch.isfinite(p.grad.float()).all()
