@@ -72,12 +72,16 @@ int scmoe_device_check(int device);
  *   counts[e]    = pre-drop selections of expert e   (int32, overwritten)
  *   prob_sum[e]  = sum_t softmax(logits[t,:])[e]     (fp32, overwritten)
  * w_gate_t / w_noise_t are (N, d) fp32 (transposed gate weights); w_noise_t
- * and eps are NULL when noise is disabled.  x is (T, d) with row stride
+ * and eps are NULL when noise is disabled.  exclude (T,) int32 or NULL: an
+ * expert per token that must not be selected — DGMoE's distinct-expert
+ * constraint (arch.py:447-460): the top-1 over the remaining experts is the
+ * runner-up exactly when the best expert clashes.  x is (T, d) with row stride
  * ld_x elements, dtype SCMOE_F32 or SCMOE_BF16.  N <= 64, 1 <= k <= min(N, 8).
  */
 size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts);
 int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                     const float* w_gate_t, const float* w_noise_t, const float* eps,
+                    const int32_t* exclude,
                     int n_tokens, int d_model, int n_experts, int k, int quota,
                     float* logits, int32_t* indices, float* weights, int32_t* slots,
                     uint8_t* dropped, int32_t* counts, float* prob_sum,

@@ -541,3 +541,59 @@ def model_forward(blocks, tokens, variant: str, pos: Optional[str], capacity_fac
             auxes.append(aux)
             h = h_mh + f
     return h, decs, auxes
+
+
+# ---------------------------------------------------------------------------
+# DGMoE: dual top-1 gating with the distinct-expert constraint
+# (scmoelab/arch.py:447-460 dual_routing, 507-533 moe_dual_gating)
+
+
+def dual_routing(h_cur, h_prev, constraint: bool, capacity_factor: float):
+    """(dec_cur, dec_prev): top-1 on the preceding representation with
+    capacity; on the current one the top-1, replaced by the runner-up when it
+    equals the preceding pick (constraint on), then capacity."""
+    h_cur = np.asarray(h_cur, dtype=np.float64)
+    n, t = h_prev.shape[1], h_prev.shape[0]
+    dec_prev = apply_capacity(select_topk(h_prev, 1), capacity_factor, n, t)
+    top2 = topk_indices(h_cur, 2)
+    idx = top2[:, :1].copy()
+    if constraint:
+        clash = idx[:, 0] == dec_prev.indices[:, 0]
+        idx[clash, 0] = top2[clash, 1]
+    dec_cur = decision_from_indices(h_cur, idx, np.zeros((t, 1), dtype=bool))
+    return apply_capacity(dec_cur, capacity_factor, n, t), dec_prev
+
+
+def moe_dual_gating(x_cur, x_prev, layer: Layer, capacity_factor: float, constraint: bool,
+                    pinned=None):
+    """routed_sum(x_cur, w_cur) + routed_sum(x_prev, w_prev); aux from the
+    current gating (arch.py:507-533).  pinned = ((idx_cur, drop_cur),
+    (idx_prev, drop_prev)) replays the routing."""
+    h_prev, _ = gate_logits(x_prev, layer.gate)
+    h_cur, _ = gate_logits(x_cur, layer.gate)
+    if pinned is not None:
+        dec_cur = decision_from_indices(h_cur, pinned[0][0], pinned[0][1])
+        dec_prev = decision_from_indices(h_prev, pinned[1][0], pinned[1][1])
+    else:
+        dec_cur, dec_prev = dual_routing(h_cur, h_prev, constraint, capacity_factor)
+
+    def wmat(h, dec):
+        return row_softmax(np.where(dec.support_mask(), h, NEG_INF)) * dec.keep_mask()
+
+    out = routed_sum_dense(x_cur, layer.experts, wmat(h_cur, dec_cur)) + \
+        routed_sum_dense(x_prev, layer.experts, wmat(h_prev, dec_prev))
+    return out, dec_cur, dec_prev, load_balance_loss(dec_cur, h_cur.shape[1])
+
+
+def dgmoe_pair_forward(p: PairParams, h_in, capacity_factor: float, constraint: bool = True,
+                       pre_layernorm: bool = False, pinned=None):
+    """Block pair with the DGMoE feed; the preceding gating reads h_mh_prev
+    (arch.py:606-609).  Returns (out, dec_cur, dec_prev, aux)."""
+    d = h_in.shape[1]
+    feed = layer_norm if pre_layernorm else (lambda z: z)
+    h_mh_prev = h_in + attention_forward(feed(h_in), p.attn_prev, d)
+    h_mlp_prev = h_mh_prev + expert_forward(feed(h_mh_prev), p.mlp_prev)
+    h_mh_cur = h_mlp_prev + attention_forward(feed(h_mlp_prev), p.attn_cur, d)
+    x_cur = feed(h_mh_cur)
+    f, dc, dp, aux = moe_dual_gating(x_cur, h_mh_prev, p.moe, capacity_factor, constraint, pinned)
+    return h_mh_cur + f, dc, dp, aux

@@ -11,4 +11,5 @@ __all__ = ["CapacityConfig", "ConfigError", "GateDecision", "MoEReplay", "Routed
            "ScMoELayer", "SharedExpert", "Top1Gate", "Top2MoELayer", "expert_quota",
            "Attention", "ScMoEBlockPair", "sched", "timeline", "ep"]
 from .block import ScMoEBlock, ScMoEModel
-__all__ += ["ScMoEBlock", "ScMoEModel"]
+from .layers import DGMoELayer
+__all__ += ["ScMoEBlock", "ScMoEModel", "DGMoELayer"]

@@ -36,11 +36,11 @@ from torch import nn
 from . import ep as ep_mod
 from . import kernels as K
 from . import sched
-from .layers import (CapacityConfig, ConfigError, MoEReplay, ScMoELayer, SharedExpert,
-                     Top2MoELayer, _as_tensor, _normal_)
+from .layers import (CapacityConfig, ConfigError, DGMoELayer, MoEReplay, ScMoELayer,
+                     SharedExpert, Top2MoELayer, _as_tensor, _normal_)
 from .timeline import Recorder
 
-VARIANTS = ("scmoe", "shared", "standard")
+VARIANTS = ("scmoe", "shared", "standard", "dgmoe")
 POSITIONS = ("pos1", "pos2", "pos3")
 
 
@@ -107,7 +107,7 @@ class ScMoEBlockPair(nn.Module):
                  combine_mode: str = "direct_add", capacity_factor: float = 2.0,
                  noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
                  seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
-                 device=None, generator=None, ep_group=None):
+                 device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True):
         super().__init__()
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
@@ -131,6 +131,12 @@ class ScMoEBlockPair(nn.Module):
             self.moe = Top2MoELayer(d_model, d_hidden, n_experts, k_routed=k_routed,
                                     capacity_factor=capacity_factor, noise_enabled=noise_enabled,
                                     ep_group=ep_group, **kw)
+        elif variant == "dgmoe":
+            if not self._PAIR:
+                raise ConfigError("dual gating is defined on block pairs only")  # arch.py:78-79
+            self.moe = DGMoELayer(d_model, d_hidden, n_experts, capacity_factor=capacity_factor,
+                                  dgmoe_constraint=dgmoe_constraint, noise_enabled=noise_enabled,
+                                  ep_group=ep_group, **kw)
         else:
             self.moe = ScMoELayer(d_model, d_hidden, n_experts, k_routed=k_routed,
                                   combine_mode=combine_mode, capacity_factor=capacity_factor,
@@ -152,7 +158,7 @@ class ScMoEBlockPair(nn.Module):
                 combine_mode=cfg.combine_mode, capacity_factor=cfg.capacity_factor,
                 noise_enabled=cfg.noise_enabled, pre_layernorm=cfg.pre_layernorm,
                 n_heads=n_heads, seq_len=seq_len, causal=causal, dtype=dtype, device=device,
-                ep_group=ep_group)
+                ep_group=ep_group, dgmoe_constraint=getattr(cfg, "dgmoe_constraint", True))
         if cls._PAIR:
             m.attn_prev.load_reference(prev_blk.attn)
             m.mlp_prev.load_reference(prev_blk.feed)
@@ -162,6 +168,9 @@ class ScMoEBlockPair(nn.Module):
         if cfg.variant == "standard":
             ref = Top2MoELayer.from_reference(layer, cap, k=cfg.k_routed, dtype=dtype,
                                               device=device, ep_group=ep_group)
+        elif cfg.variant == "dgmoe":
+            ref = DGMoELayer.from_reference(layer, cap, constraint=m.moe.constraint, dtype=dtype,
+                                            device=device)
         else:
             ref = ScMoELayer.from_reference(layer, cap, dtype=dtype, device=device,
                                             ep_group=ep_group)
@@ -177,6 +186,8 @@ class ScMoEBlockPair(nn.Module):
         return self._comm_stream
 
     def order(self):
+        if self.variant == "dgmoe":
+            return ["attn_prev", "mlp_prev", "attn_cur", "dual"]
         if self.variant == "scmoe":
             o = sched.issue_order(self.shortcut_pos, self.slot if self.slot is not None else 0)
         else:
@@ -297,13 +308,21 @@ class ScMoEBlockPair(nn.Module):
                                        se_out=env["se"], mode=moe.combine_mode, x_cur=env["x_cur"],
                                        w_cg=moe.w_cg, residual=env["h_mh_cur"])
 
+        def dual():
+            # DGMoE: preceding gating on h_mh_prev, current on x_cur (arch.py:606-609)
+            out, dc, dp, aux = moe(env["x_cur"], env["h_mh_prev"], residual=env["h_mh_cur"])
+            env["out"], env["dec"], env["aux"] = out, (dc, dp), aux
+
         ops = dict(attn_prev=attn_prev, mlp_prev=mlp_prev, attn_cur=attn_cur, gate=gate,
-                   encode=encode, expert=expert, shared=shared, decode=decode)
+                   encode=encode, expert=expert, shared=shared, decode=decode, dual=dual)
         for name in self.order():
             with rec.op(name, "compute", st):
                 ops[name]()
         dec = env["dec"]
-        res = (env["out"], dec, env["aux"] if train else dec.aux_loss())
+        if self.variant == "dgmoe":
+            res = (env["out"], dec, env["aux"])       # decision = (current, preceding)
+        else:
+            res = (env["out"], dec, env["aux"] if train else dec.aux_loss())
         if return_taps:
             taps = {k: env[k] for k in ("h_mh_prev", "h_mlp_prev", "h_mh_cur", "x_cur")}
             taps["src"] = src()
@@ -395,7 +414,7 @@ class ScMoEModel(nn.Module):
                  noise_enabled: bool = False, first_layer_pos1: bool = False,
                  pre_layernorm: bool = False, n_heads: int = 1, seq_len: Optional[int] = None,
                  causal: bool = False, dtype=torch.bfloat16, device=None, generator=None,
-                 ep_group=None, _build: bool = True):
+                 ep_group=None, dgmoe_constraint: bool = True, _build: bool = True):
         super().__init__()
         if moe_frequency not in ("every-second-block", "every-block"):
             raise ConfigError(f"unknown moe_frequency {moe_frequency!r}")
@@ -408,6 +427,8 @@ class ScMoEModel(nn.Module):
                   noise_enabled=noise_enabled, pre_layernorm=pre_layernorm, n_heads=n_heads,
                   seq_len=seq_len, causal=causal, dtype=dtype, device=device,
                   generator=generator, ep_group=ep_group)
+        if variant == "dgmoe":
+            kw["dgmoe_constraint"] = dgmoe_constraint
         blocks = []
         if _build:
             if moe_frequency == "every-second-block":

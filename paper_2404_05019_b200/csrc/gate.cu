@@ -54,7 +54,8 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
 template <typename T, int NMAX, bool NOISE>
 __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
     const T* __restrict__ x, long long ld_x, const float* __restrict__ wg_t,
-    const float* __restrict__ wn_t, const float* __restrict__ eps, int n_tok, int d,
+    const float* __restrict__ wn_t, const float* __restrict__ eps,
+    const int32_t* __restrict__ exclude, int n_tok, int d,
     int N, int k, int quota, int dc_max, float* __restrict__ logits,
     int32_t* __restrict__ indices, float* __restrict__ weights, int32_t* __restrict__ slots,
     uint8_t* __restrict__ dropped, int32_t* __restrict__ counts, float* __restrict__ prob_sum,
@@ -203,7 +204,14 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
       for (int e = 0; e < NMAX; ++e)
         if (e < N) logits[(long long)t * N + e] = h[e];
     }
-    // top-k: repeated argmax with strict '>' (lowest index wins ties)
+    // top-k: repeated argmax with strict '>' (lowest index wins ties).  An
+    // excluded expert (DGMoE distinct-expert constraint, arch.py:453-457) is
+    // skipped, so the pick becomes the runner-up exactly when it would clash.
+    uint64_t blocked = 0;
+    if (exclude && valid) {
+      const int ex = exclude[t];
+      if (ex >= 0 && ex < N) blocked = 1ull << ex;
+    }
     uint64_t selmask = 0;
 #pragma unroll
     for (int j = 0; j < SCMOE_MAX_K; ++j) {
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
         float bv = 0.f;
 #pragma unroll
         for (int e = 0; e < NMAX; ++e) {
-          if (e < N && !((selmask >> e) & 1ull)) {
+          if (e < N && !(((selmask | blocked) >> e) & 1ull)) {
             if (bi < 0 || gt_nan_last(h[e], bv)) {
               bi = e;
               bv = h[e];
@@ -350,7 +358,8 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
 
 template <typename T, int NMAX>
 int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
-                const float* eps, int T_, int d, int N, int k, int quota, float* logits,
+                const float* eps, const int32_t* excl, int T_, int d, int N, int k, int quota,
+                float* logits,
                 int32_t* idx, float* w, int32_t* slots, uint8_t* drop, int32_t* counts,
                 float* prob_sum, uint8_t* ws, cudaStream_t st) {
   const int tiles = (T_ + TOK - 1) / TOK;
@@ -370,13 +379,13 @@ int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
   if (noise) {
     auto kern = gate_topk_kernel<T, NMAX, true>;
     SCMOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, T_, d, N, k, quota, dc,
+    kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, excl, T_, d, N, k, quota, dc,
                                        logits, idx, w, slots, drop, counts, prob_sum, ctrs,
                                        status, psum, tiles);
   } else {
     auto kern = gate_topk_kernel<T, NMAX, false>;
     SCMOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, T_, d, N, k, quota, dc,
+    kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, excl, T_, d, N, k, quota, dc,
                                        logits, idx, w, slots, drop, counts, prob_sum, ctrs,
                                        status, psum, tiles);
   }
@@ -386,13 +395,13 @@ int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
 
 template <typename T>
 int dispatch_nmax(const void* x, long long ld_x, const float* wg, const float* wn,
-                  const float* eps, int T_, int d, int N, int k, int quota, float* logits,
-                  int32_t* idx, float* w, int32_t* slots, uint8_t* drop, int32_t* counts,
-                  float* prob_sum, uint8_t* ws, cudaStream_t st) {
-#define SCMOE_GATE_CASE(NM)                                                                   \
-  if (N <= NM)                                                                                \
-    return launch_gate<T, NM>(x, ld_x, wg, wn, eps, T_, d, N, k, quota, logits, idx, w, slots, \
-                              drop, counts, prob_sum, ws, st);
+                  const float* eps, const int32_t* excl, int T_, int d, int N, int k, int quota,
+                  float* logits, int32_t* idx, float* w, int32_t* slots, uint8_t* drop,
+                  int32_t* counts, float* prob_sum, uint8_t* ws, cudaStream_t st) {
+#define SCMOE_GATE_CASE(NM)                                                                    \
+  if (N <= NM)                                                                                 \
+    return launch_gate<T, NM>(x, ld_x, wg, wn, eps, excl, T_, d, N, k, quota, logits, idx, w,  \
+                              slots, drop, counts, prob_sum, ws, st);
   SCMOE_GATE_CASE(4)
   SCMOE_GATE_CASE(8)
   SCMOE_GATE_CASE(16)
@@ -413,6 +422,7 @@ extern "C" size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts) {
 
 extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                                const float* w_gate_t, const float* w_noise_t, const float* eps,
+                               const int32_t* exclude,
                                int n_tokens, int d_model, int n_experts, int k, int quota,
                                float* logits, int32_t* indices, float* weights, int32_t* slots,
                                uint8_t* dropped, int32_t* counts, float* prob_sum,
@@ -430,15 +440,16 @@ extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                   "d_model and ld_x must be multiples of %d", vec);
   SCMOE_CHECK_ARG(((uintptr_t)x & 15) == 0, "x must be 16-byte aligned");
   SCMOE_CHECK_ARG((w_noise_t == nullptr) == (eps == nullptr), "w_noise and eps go together");
+  SCMOE_CHECK_ARG(!exclude || k < n_experts, "an excluded expert needs k < n_experts");
   SCMOE_CHECK_ARG(workspace_bytes >= scmoe_gate_workspace_bytes(n_tokens, n_experts),
                   "gate workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)workspace;
   if (x_dtype == SCMOE_BF16)
-    return dispatch_nmax<__nv_bfloat16>(x, ld_x, w_gate_t, w_noise_t, eps, n_tokens, d_model,
-                                        n_experts, k, quota, logits, indices, weights, slots,
-                                        dropped, counts, prob_sum, ws, st);
-  return dispatch_nmax<float>(x, ld_x, w_gate_t, w_noise_t, eps, n_tokens, d_model, n_experts, k,
-                              quota, logits, indices, weights, slots, dropped, counts, prob_sum,
-                              ws, st);
+    return dispatch_nmax<__nv_bfloat16>(x, ld_x, w_gate_t, w_noise_t, eps, exclude, n_tokens,
+                                        d_model, n_experts, k, quota, logits, indices, weights,
+                                        slots, dropped, counts, prob_sum, ws, st);
+  return dispatch_nmax<float>(x, ld_x, w_gate_t, w_noise_t, eps, exclude, n_tokens, d_model,
+                              n_experts, k, quota, logits, indices, weights, slots, dropped,
+                              counts, prob_sum, ws, st);
 }

@@ -43,7 +43,7 @@ class GateOut:
 
 def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
               w_noise_t: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
-              stream=None) -> GateOut:
+              exclude: Optional[torch.Tensor] = None, stream=None) -> GateOut:
     """K1/K1b: logits, top-k, masked-softmax weights and capacity slots."""
     ensure_device(x)
     if x.dim() != 2 or x.stride(1) != 1:
@@ -64,9 +64,11 @@ def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
     ws = torch.empty(ws_bytes, device=dev, dtype=torch.uint8)
     if eps is not None:
         eps = _c(eps.to(torch.float32), "eps")
+    if exclude is not None:
+        exclude = _c(exclude.to(torch.int32).reshape(-1), "exclude")
     check(lib().scmoe_gate_topk(
         ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")),
-        ptr(w_noise_t), ptr(eps), T, d, N, k, quota,
+        ptr(w_noise_t), ptr(eps), ptr(exclude), T, d, N, k, quota,
         ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
         ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
     return GateOut(logits, indices, weights, slots, dropped, counts, prob_sum, quota)

@@ -520,3 +520,81 @@ class Top2MoELayer(_RoutedMoE):
         y = self.routed_experts(x, dec)
         out = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, residual=residual)
         return out, dec, dec.aux_loss()
+
+
+class DGMoELayer(_RoutedMoE):
+    """Dual-gating MoE (paper App. A.2, Eq. 20): two top-1 gatings with the
+    same gate, one over the preceding-layer representation and one over the
+    current one; with `dgmoe_constraint` a token whose current pick equals its
+    preceding pick takes the current runner-up (arch.py:447-460, 507-533).
+    out = routed(x_cur; dec_cur) + routed(x_prev; dec_prev), aux from the
+    current gating.  Both dispatches share one (2N, C, d) buffer, so the two
+    expert passes are a single grouped GEMM over 2N groups."""
+
+    def __init__(self, d_model: int, d_hidden: int, n_experts: int,
+                 capacity_factor: float = 2.0, dgmoe_constraint: bool = True,
+                 noise_enabled: bool = False, dtype=torch.bfloat16, device=None,
+                 generator: Optional[torch.Generator] = None, ep_group=None):
+        if n_experts < 2:
+            raise ConfigError("dual gating needs at least 2 experts")
+        if ep_group is not None:
+            raise NotImplementedError("DGMoE under expert parallelism is not implemented")
+        super().__init__(d_model, d_hidden, n_experts, 1, capacity_factor, noise_enabled,
+                         dtype, device, generator, ep_group)
+        self.constraint = dgmoe_constraint
+
+    @classmethod
+    def from_reference(cls, layer, capacity=None, constraint: bool = True, dtype=torch.bfloat16,
+                       device=None):
+        d, n = np.asarray(layer.gate.w_gate).shape
+        h = np.asarray(layer.experts[0].w1).shape[1]
+        cf = capacity.capacity_factor if capacity is not None else 2.0
+        m = cls(d, h, n, capacity_factor=cf, dgmoe_constraint=constraint,
+                noise_enabled=bool(layer.gate.noise_enabled), dtype=dtype, device=device)
+        m._load_reference_common(layer)
+        return m
+
+    def route_dual(self, x_cur, x_prev, eps=None, eps_prev=None):
+        dec_prev = self.gate(x_prev, eps=eps_prev)
+        g = self.gate
+        quota = g.quota(x_cur.shape[0])
+        excl = dec_prev.indices[:, 0] if self.constraint else None
+        o = K.gate_topk(x_cur, g.w_gate_t, 1, quota,
+                        w_noise_t=g.w_noise_t if g.noise_enabled else None,
+                        eps=eps if g.noise_enabled else None, exclude=excl)
+        dec_cur = GateDecision(o.logits, o.indices, o.weights, o.dropped.bool(), o.slots, o.counts,
+                               o.prob_sum, quota, quota, eps if g.noise_enabled else None)
+        return dec_cur, dec_prev
+
+    def forward(self, x_cur: torch.Tensor, x_prev: torch.Tensor,
+                residual: Optional[torch.Tensor] = None, eps=None, eps_prev=None):
+        """(out, dec_cur, dec_prev, aux) — moe_dual_gating (arch.py:507-533)."""
+        n, cap = self.n_experts, self.gate.quota(x_cur.shape[0])
+        train = self.training_path()
+        with torch.no_grad():
+            dec_cur, dec_prev = self.route_dual(x_cur, x_prev, eps, eps_prev)
+        idx = torch.cat([dec_cur.indices, dec_prev.indices + n], dim=1).contiguous()
+        slots = torch.cat([dec_cur.slots, dec_prev.slots], dim=1).contiguous()
+        e = self.experts
+        if train:
+            from . import training as TR
+            w_cur, aux = TR.GateFn.apply(x_cur, self.gate.w_gate_t, dec_cur.logits,
+                                         dec_cur.indices, dec_cur.counts, dec_cur.weights, 1)
+            kc, kp = dec_cur.kept_counts().int(), dec_prev.kept_counts().int()
+            buf = torch.cat([TR.DispatchFn.apply(x_cur, dec_cur.indices, dec_cur.slots, kc, n, cap),
+                             TR.DispatchFn.apply(x_prev, dec_prev.indices, dec_prev.slots, kp, n,
+                                                 cap)])
+            rows = torch.cat([kc, kp])
+            y = TR.FFNFn.apply(buf, e.w1t, e.b1, e.w2t, e.b2, None, rows, cap)
+            w = torch.cat([w_cur, dec_prev.weights], dim=1)
+            out = TR.CombineFn.apply(y, None, w, None, None, residual, idx, slots,
+                                     rows, cap, "direct_add")
+            return out, dec_cur, dec_prev, aux
+        buf = torch.empty(2 * n, cap, x_cur.shape[1], device=x_cur.device, dtype=x_cur.dtype)
+        K.dispatch(x_cur, dec_cur.indices, dec_cur.slots, n, cap, out=buf[:n])
+        K.dispatch(x_prev, dec_prev.indices, dec_prev.slots, n, cap, out=buf[n:])
+        rows = torch.cat([dec_cur.counts, dec_prev.counts])
+        y = self.experts(buf, rows, cap)
+        w = torch.cat([dec_cur.weights, dec_prev.weights], dim=1).contiguous()
+        out = K.combine(y, idx, slots, w, cap, residual=residual)
+        return out, dec_cur, dec_prev, dec_cur.aux_loss()

@@ -113,6 +113,8 @@ def layer_and_pair_cases(arch, Rng):
                        k_routed=1, noise_enabled=True))
     combos.append(dict(variant="scmoe", shortcut_pos="pos1", combine_mode="direct_add",
                        k_routed=1, pre_layernorm=True))
+    combos.append(dict(variant="dgmoe", shortcut_pos="pos2", k_routed=1))
+    combos.append(dict(variant="dgmoe", shortcut_pos="pos2", k_routed=1, dgmoe_constraint=False))
     for i, kw in enumerate(combos):
         t, d, h, n = 24, 8, 16, 4
         cf = [2.0, 1.0, 0.5][i % 3]
@@ -125,6 +127,16 @@ def layer_and_pair_cases(arch, Rng):
         res = arch.model_forward(cfg, params, tokens, rng=noise_rng)
         m = res.trace.moe[0]
         p = f"c{i}_"
+        if m.decision_prev is not None:
+            out[p + "idx_prev"] = m.decision_prev.indices.astype(np.int64)
+            out[p + "drop_prev"] = m.decision_prev.dropped
+            out[p + "out"] = np.asarray(res.output)
+            out[p + "idx"] = m.decision.indices.astype(np.int64)
+            out[p + "drop"] = m.decision.dropped
+            out[p + "tokens"] = tokens
+            out[p + "aux"] = np.asarray(m.aux_loss)
+            meta.append(dict(t=t, d=d, h=h, n=n, cf=cf, seed=100 + i, **kw))
+            continue
         out[p + "tokens"] = tokens
         out[p + "out"] = np.asarray(res.output)
         out[p + "idx"] = m.decision.indices.astype(np.int64)

@@ -39,7 +39,7 @@ def test_workspace_query_is_host_only():
 
 def test_argument_errors_do_not_touch_the_gpu():
     so = _lib.load_library()
-    rc = so.scmoe_gate_topk(None, 1, 8, None, None, None, 0, 8, 4, 1, 1, None, None, None,
+    rc = so.scmoe_gate_topk(None, 1, 8, None, None, None, None, 0, 8, 4, 1, 1, None, None, None,
                             None, None, None, None, None, 0, None)
     assert rc == _lib.SCMOE_ERR_ARG
     assert b"n_tokens" in so.scmoe_last_error()
