@@ -107,8 +107,12 @@ class ScMoEBlockPair(nn.Module):
                  combine_mode: str = "direct_add", capacity_factor: float = 2.0,
                  noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
                  seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
-                 device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True):
+                 device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True,
+                 chunks: int = 1):
         super().__init__()
+        if chunks < 1:
+            raise ConfigError("chunks must be >= 1")
+        self.chunks = chunks
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
         if variant == "scmoe" and shortcut_pos not in POSITIONS:
@@ -237,6 +241,9 @@ class ScMoEBlockPair(nn.Module):
         train = moe.training_path()
         if train:
             from . import training as TR
+        # chunked pipelining (standard_pipeline / scmoe_overlap_pipeline,
+        # distsim.py:277-300, 358-364): forward only
+        chunks = self.chunks if not train else 1
 
         def gate():
             if train:
@@ -248,9 +255,57 @@ class ScMoEBlockPair(nn.Module):
                                                        dec.indices, dec.counts, dec.weights, dec.k)
             else:
                 env["dec"] = moe.route(src(), eps=eps, replay=replay)
+                if chunks > 1:
+                    env["cr"] = ep_mod.chunk_routing(env["dec"], chunks)
+
+        def encode_chunked():
+            # chunk-major buffer (chunks, E, Cc, d): chunk c's exchange is contiguous
+            idx2, slot2, cc, rows = env["cr"]
+            buf = K.dispatch(src(), idx2, slot2, chunks * moe.n_experts, cc)
+            env["buf"] = buf.view(chunks, moe.n_experts, cc, -1)
+            if use_ep:
+                cs.wait_stream(st)
+                env["pending"] = []
+                for c in range(chunks):
+                    with rec.op(f"dispatch{c}", "comm", cs):
+                        env["pending"].append(ep_mod.dispatch_exchange(
+                            env["buf"][c], rows[c].contiguous(), cc, self.ep_group, cs))
+
+        def expert_chunked():
+            idx2, slot2, cc, rows = env["cr"]
+            y = torch.empty_like(env["buf"])
+            evs = []
+            for c in range(chunks):
+                if use_ep:
+                    p = env["pending"][c]
+                    st.wait_event(p.event)
+                    yc = moe.experts(p.recv, p.recv_counts, cc)
+                    cs.wait_stream(st)
+                    with rec.op(f"combine{c}", "comm", cs):
+                        _, ev = ep_mod.combine_exchange(yc, self.ep_group, cs, out=y[c])
+                    evs.append(ev)
+                else:
+                    moe.experts(env["buf"][c], rows[c].contiguous(), cc, out=y[c])
+            env["y"] = y.view(chunks * moe.n_experts, cc, -1)
+            env["y_evs"] = evs
+
+        def decode_chunked():
+            dec = env["dec"]
+            idx2, slot2, cc, rows = env["cr"]
+            for ev in env.get("y_evs", []):
+                st.wait_event(ev)
+            if self.variant == "standard":
+                env["out"] = K.combine(env["y"], idx2, slot2, dec.weights, cc,
+                                       residual=env["h_mh_cur"])
+            else:
+                env["out"] = K.combine(env["y"], idx2, slot2, dec.weights, cc, se_out=env["se"],
+                                       mode=moe.combine_mode, x_cur=env["x_cur"], w_cg=moe.w_cg,
+                                       residual=env["h_mh_cur"])
 
         def encode():
             dec = env["dec"]
+            if chunks > 1:
+                return encode_chunked()
             if train:
                 buf = TR.DispatchFn.apply(src(), dec.indices, dec.slots, env["kept"], moe.n_experts,
                                           dec.capacity)
@@ -269,6 +324,8 @@ class ScMoEBlockPair(nn.Module):
 
         def expert():
             dec = env["dec"]
+            if chunks > 1:
+                return expert_chunked()
             if train:
                 e = moe.experts
                 rows = env["recv_counts"] if use_ep else env["kept"]
@@ -291,6 +348,8 @@ class ScMoEBlockPair(nn.Module):
 
         def decode():
             dec = env["dec"]
+            if chunks > 1:
+                return decode_chunked()
             if train:
                 std = self.variant == "standard"
                 env["out"] = TR.CombineFn.apply(

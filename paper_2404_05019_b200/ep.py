@@ -70,18 +70,38 @@ def dispatch_exchange(buf: torch.Tensor, kept_counts: torch.Tensor, capacity: in
 
 
 def combine_exchange(expert_out: torch.Tensor, group=None,
-                     comm_stream: Optional[torch.cuda.Stream] = None):
+                     comm_stream: Optional[torch.cuda.Stream] = None,
+                     out: Optional[torch.Tensor] = None):
     """Return the expert outputs to the ranks that own the tokens; returns
     (buffer, event-or-None)."""
     if comm_stream is None:
-        return exchange_rows(expert_out, group), None
+        return exchange_rows(expert_out, group, out), None
     comm_stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(comm_stream):
-        back = exchange_rows(expert_out, group)
+        back = exchange_rows(expert_out, group, out)
         ev = torch.cuda.Event()
         ev.record(comm_stream)
     expert_out.record_stream(comm_stream)
     return back, ev
+
+
+def chunk_routing(dec, n_chunks: int):
+    """Chunked pipelining (distsim.py:277-300): split every expert's capacity
+    C into n_chunks slices of Cc = ceil(C / n_chunks) slots and renumber
+    selections into a chunk-major (n_chunks * E, Cc) buffer, so chunk c's
+    dispatch / combine exchange is one contiguous (E, Cc, d) block.
+    Returns (indices', slots', Cc, rows) with rows (n_chunks, E) the kept rows
+    of every expert in every chunk."""
+    n_exp, cap = dec.n_experts, dec.capacity
+    cc = (cap + n_chunks - 1) // n_chunks
+    s = dec.slots.long()
+    kept = s < cap
+    chunk = torch.div(s, cc, rounding_mode="floor").clamp(max=n_chunks - 1)
+    idx2 = (chunk * n_exp + dec.indices.long()).to(torch.int32).contiguous()
+    slot2 = torch.where(kept, s - chunk * cc, torch.full_like(s, cc)).to(torch.int32).contiguous()
+    base = torch.arange(n_chunks, device=s.device)[:, None] * cc
+    rows = (dec.kept_counts().long()[None, :] - base).clamp(min=0, max=cc).to(torch.int32)
+    return idx2, slot2, cc, rows
 
 
 def expert_parallel_ffn(experts, buf: torch.Tensor, dec, group=None) -> torch.Tensor:
