@@ -1,0 +1,79 @@
+"""The expert-parallel path over a real NCCL communicator of one rank: the
+side-stream all-to-alls, cross-stream events, chunked exchanges and the
+comm-span recording all run on the GPU (a one-rank all-to-all is a local
+copy), and the results must equal the single-GPU path bit for bit.  The
+multi-rank exchange logic itself is covered over gloo in test_ep_gloo.py."""
+
+import os
+import socket
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+P = None
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def setup_module(module):
+    global P
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import torch.distributed as dist
+    import paper_2404_05019_b200 as pkg
+    P = pkg
+    if not dist.is_initialized():
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+
+
+def teardown_module(module):
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant,chunks", [("scmoe", 1), ("scmoe", 2), ("standard", 1),
+                                            ("standard", 3)])
+def test_ep_path_equals_local(variant, chunks):
+    import torch.distributed as dist
+    from paper_2404_05019_b200.timeline import Recorder, comm_overlap_fraction
+    T, d, h, N = 1024, 256, 512, 8
+    kw = dict(variant=variant, k_routed=1 if variant == "scmoe" else 2,
+              shortcut_pos="pos2" if variant == "scmoe" else None, n_heads=4, seq_len=256,
+              capacity_factor=1.25, dtype=torch.bfloat16, chunks=chunks)
+    loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2), **kw)
+    epb = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2),
+                           ep_group=dist.group.WORLD, **kw)
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    with torch.no_grad():
+        a, _, _ = loc(x)
+        rec = Recorder()
+        b, _, _ = epb(x, recorder=rec)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    spans = rec.spans()
+    comm = [s for s in spans if s.stream == "comm"]
+    assert len(comm) == 2 * chunks          # dispatch + combine per chunk
+    assert 0.0 <= comm_overlap_fraction(spans) <= 1.0
+
+
+def test_ep_calibrate_and_train_step():
+    import torch.distributed as dist
+    blk = P.ScMoEBlockPair(256, 512, 8, variant="scmoe", shortcut_pos="pos2", n_heads=4,
+                           seq_len=256, dtype=torch.bfloat16, ep_group=dist.group.WORLD,
+                           generator=torch.Generator(device="cuda").manual_seed(3))
+    x = torch.randn(1024, 256, device="cuda").bfloat16()
+    with torch.no_grad():
+        ch = blk.calibrate(x)
+    assert 0 <= ch.slot <= 3 and blk.last_costs.t_disp >= 0
+    blk.requires_grad_(True)
+    l0 = float(blk.train_step(x, lr=1e-3))
+    l1 = float(blk.train_step(x, lr=1e-3))
+    assert l1 < l0
