@@ -228,6 +228,28 @@ def grouped_wgrad(a: torch.Tensor, b: torch.Tensor, n_wgroups: int = 1,
     return out if (a.dim() == 3 or n_wgroups > 1) else out.view(M, N)
 
 
+_ONES = {}
+
+
+def bias_grad(dy: torch.Tensor, n_wgroups: int = 1, group_rows: Optional[torch.Tensor] = None,
+              rows_clip: int = 0, stream=None) -> torch.Tensor:
+    """Bias gradient sum_{g = w mod W} sum_{r < rows(g)} dy[g, r, :] as the
+    tensor-core weight gradient 1^T dy (K7 wgrad with an all-ones (C, 8)
+    operand): dy is read once, split-K across the GPU, the zero-padded tails
+    of dy keep the partial last 64-row block exact.  Returns (W, N) fp32."""
+    ensure_device(dy)
+    d3 = dy if dy.dim() == 3 else dy.unsqueeze(0)
+    G, C, N = d3.shape
+    key = (d3.device, d3.dtype, G, C)
+    ones = _ONES.get(key)
+    if ones is None:
+        ones = torch.ones(G, C, 8, device=d3.device, dtype=d3.dtype)
+        _ONES[key] = ones
+    out = grouped_wgrad(ones, d3, n_wgroups=n_wgroups, group_rows=group_rows,
+                        rows_clip=rows_clip, stream=stream)
+    return out.view(n_wgroups, 8, N)[:, 0, :]
+
+
 def zero_tails(buf: torch.Tensor, group_rows: torch.Tensor, rows_clip: int = 0, align: int = 64,
                stream=None) -> torch.Tensor:
     ensure_device(buf)

@@ -98,11 +98,10 @@ class FFNFn(torch.autograd.Function):
         dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip)
         dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
         dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
-        db2 = K.grouped_colsum(dy3, group_rows, rows_clip)
-        db1 = K.grouped_colsum(dz, group_rows, rows_clip)
-        if W != G:   # several source groups feed one weight group (expert parallel)
-            db2 = db2.view(G // W, W, d).sum(0)
-            db1 = db1.view(G // W, W, h).sum(0)
+        # bias gradients as 1^T dy on the tensor cores (sums the source groups
+        # of each weight group like the weight gradients)
+        db2 = K.bias_grad(dy3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
+        db1 = K.bias_grad(dz, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
                 (dy if has_res else None), None, None)

@@ -120,3 +120,15 @@ def test_dispatch_scaled():
     ref = torch.zeros(N, quota, d, device="cuda", dtype=torch.float64)
     ref[idx[kept], sl[kept]] = x[tt[kept]].double() * scale[kept].double()[:, None]
     _close(buf, ref, rtol=1e-2)
+
+
+@pytest.mark.parametrize("G,W,C,N", [(1, 1, 18432, 384), (8, 8, 700, 1536), (4, 2, 300, 264)])
+def test_bias_grad_tensor_core(G, W, C, N):
+    g = torch.Generator(device="cuda").manual_seed(C)
+    dy = torch.randn(G, C, N, device="cuda", generator=g).bfloat16()
+    rows = torch.randint(1, C + 1, (G,), device="cuda", generator=g, dtype=torch.int32)
+    K.zero_tails(dy, rows, C)
+    out = K.bias_grad(dy, n_wgroups=W, group_rows=rows, rows_clip=C)
+    for w in range(W):
+        ref = sum(dy[gi, :int(rows[gi])].double().sum(0) for gi in range(w, G, W))
+        _close(out[w], ref, rtol=1e-3)
