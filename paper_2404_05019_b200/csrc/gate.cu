@@ -376,15 +376,25 @@ int launch_gate(const void* x, long long ld_x, const float* wg, const float* wn,
   int dc = ((d + LB - 1) / LB) * LB;
   while (dc > LB && per_col * dc > 65536) dc -= LB;
   const size_t smem = per_col * dc;
+  // raise the dynamic-smem limit once per instantiation (never inside a
+  // CUDA-graph capture of a later call)
+  static size_t smem_set[2] = {0, 0};
+  if (smem > smem_set[noise ? 1 : 0]) {
+    if (noise)
+      SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_kernel<T, NMAX, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    else
+      SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_kernel<T, NMAX, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    smem_set[noise ? 1 : 0] = 160 * 1024;
+  }
   if (noise) {
     auto kern = gate_topk_kernel<T, NMAX, true>;
-    SCMOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, excl, T_, d, N, k, quota, dc,
                                        logits, idx, w, slots, drop, counts, prob_sum, ctrs,
                                        status, psum, tiles);
   } else {
     auto kern = gate_topk_kernel<T, NMAX, false>;
-    SCMOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<tiles, THREADS, smem, st>>>((const T*)x, ld_x, wg, wn, eps, excl, T_, d, N, k, quota, dc,
                                        logits, idx, w, slots, drop, counts, prob_sum, ctrs,
                                        status, psum, tiles);
