@@ -275,16 +275,24 @@ def bench_training(args, ws, rank, group):
     res = {"workload": w["name"].replace("(configs[1] shape, fwd)", "(configs[1])"),
            "d_model": w["d"], "d_hidden": w["h"], "n_experts": n_exp, "tokens_per_gpu": T,
            "capacity_factor": w["cf"], "step": "fwd + bwd + SGD (bf16)"}
+    from paper_2404_05019_b200.runtime import CapturedStep
+    use_graphs = ws == 1 and not args.no_graphs
+
+    def step_fn(blk):
+        if use_graphs:   # forward + backward + SGD captured as one CUDA graph
+            g = CapturedStep(lambda xx: blk.train_step(xx, lr=1e-4), [x], warmup=args.warmup)
+            return lambda r: g.replay()
+        for _ in range(args.warmup):
+            blk.train_step(x, lr=1e-4)
+        return lambda r: blk.train_step(x, lr=1e-4)
+
     sc = make("scmoe", 1)
-    for _ in range(args.warmup):
-        sc.train_step(x, lr=1e-4)
-    ms, _ = timed(lambda r: sc.train_step(x, lr=1e-4), args.steps, ws)
-    res.update(value=ws * T / (ms * 1e-3), unit="tokens/s", ms_per_step=ms)
+    ms, _ = timed(step_fn(sc), args.steps, ws)
+    res.update(value=ws * T / (ms * 1e-3), unit="tokens/s", ms_per_step=ms,
+               cuda_graph=use_graphs)
     if n_exp >= 2:
         t2 = make("standard", 2)
-        for _ in range(args.warmup):
-            t2.train_step(x, lr=1e-4)
-        ms2, _ = timed(lambda r: t2.train_step(x, lr=1e-4), args.steps, ws)
+        ms2, _ = timed(step_fn(t2), args.steps, ws)
         res["top2"] = {"value": ws * T / (ms2 * 1e-3), "ms_per_step": ms2}
         res["speedup_vs_top2"] = ms2 / ms
     else:
@@ -323,11 +331,25 @@ def run_ours(args):
         # ---- ScMoE block pair, device-timed; clocks sampled over every
         # timed region below (nvidia-smi, 200 ms) -----------------------------
         clk = Clocks(local).__enter__()
-        ms_sc, recs = timed(lambda r: sc(x, recorder=r), args.steps, ws,
-                            recorder_factory=lambda: Recorder())
-        # ---- top-2 baseline, same box, same kernels -------------------------
-        ms_t2, recs2 = timed(lambda r: t2(x, recorder=r), args.steps, ws,
-                             recorder_factory=lambda: Recorder())
+        # eager steps with a CUDA event around every op (op_ms, overlap,
+        # the roofline kernel's launch time)
+        ms_sc_eager, recs = timed(lambda r: sc(x, recorder=r), args.steps, ws,
+                                  recorder_factory=lambda: Recorder())
+        ms_t2_eager, _ = timed(lambda r: t2(x), args.steps, ws)
+        # the same steps captured once into CUDA graphs and replayed (one
+        # launch per step; single GPU — NCCL runs stay eager)
+        from paper_2404_05019_b200.runtime import CapturedStep, HostStreamRunner
+        use_graphs = ws == 1 and not args.no_graphs
+
+        def fwd(blk):
+            return lambda xx: blk(xx)[0]
+
+        if use_graphs:
+            g_sc, g_t2 = CapturedStep(fwd(sc), [x]), CapturedStep(fwd(t2), [x])
+            ms_sc, _ = timed(lambda r: g_sc.replay(), args.steps, ws)
+            ms_t2, _ = timed(lambda r: g_t2.replay(), args.steps, ws)
+        else:
+            ms_sc, ms_t2 = ms_sc_eager, ms_t2_eager
         # ---- layer-only numbers ---------------------------------------------
         src = x.clone()
         ms_layer_sc, _ = timed(lambda r: sc.moe(x, src), args.steps, ws)
@@ -337,13 +359,13 @@ def run_ours(args):
         # every step copies its input from pinned host memory and its output
         # back; HostStreamRunner overlaps step i's compute with the H2D of
         # step i+1 and the D2H of step i-1 (two copy engines, full duplex PCIe)
-        from paper_2404_05019_b200.runtime import HostStreamRunner
         h_host = torch.empty(T, d, dtype=dtype, pin_memory=True)
         h_host.copy_(x.cpu())
         o_host = [torch.empty(T, d, dtype=dtype, pin_memory=True) for _ in range(2)]
         e2e_ms = None
         if not args.no_e2e:
-            runner = HostStreamRunner(lambda xd: sc(xd))
+            runner = HostStreamRunner([g_sc, CapturedStep(fwd(sc), [x])] if use_graphs
+                                      else (lambda xd: sc(xd)))
             runner.run([h_host] * 3, [o_host[i % 2] for i in range(3)])
             torch.cuda.synchronize()
             barrier(ws)
@@ -406,6 +428,11 @@ def run_ours(args):
                    "combine": w["combine"], "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
         "speedup_vs_top2": ms_t2 / ms_sc,
+        "cuda_graph": use_graphs,
+        "eager": {"ms_per_step": ms_sc_eager, "value": ws * T / (ms_sc_eager * 1e-3),
+                  "top2_ms_per_step": ms_t2_eager,
+                  "note": "same steps without graph capture; op_ms / roofline / comm come "
+                          "from these per-op CUDA events"},
         "top2": {"value": t2_value, "unit": "tokens/s", "ms_per_step": ms_t2},
         "layer_only": {"scmoe_ms": ms_layer_sc, "top2_ms": ms_layer_t2,
                        "speedup": ms_layer_t2 / ms_layer_sc},
@@ -448,6 +475,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gpt3xl")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-training", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--cpu-reps", type=int, default=3)
