@@ -65,13 +65,13 @@ def log(*a):
 # distributed plumbing
 
 
-def dist_setup():
+def dist_setup(force_dist: bool = False):
     import torch
     import torch.distributed as dist
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or force_dist:
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -276,7 +276,7 @@ def bench_training(args, ws, rank, group):
            "d_model": w["d"], "d_hidden": w["h"], "n_experts": n_exp, "tokens_per_gpu": T,
            "capacity_factor": w["cf"], "step": "fwd + bwd + SGD (bf16)"}
     from paper_2404_05019_b200.runtime import CapturedStep
-    use_graphs = ws == 1 and not args.no_graphs
+    use_graphs = group is None and not args.no_graphs
 
     def step_fn(blk):
         if use_graphs:   # forward + backward + SGD captured as one CUDA graph
@@ -307,11 +307,14 @@ def run_ours(args):
     import paper_2404_05019_b200 as P
     from paper_2404_05019_b200.timeline import Recorder, comm_overlap_fraction, exposed_comm_ms
 
-    ws, rank, local = dist_setup()
+    ws, rank, local = dist_setup(args.force_ep)
     w = WORKLOADS[args.workload]
     dtype = torch.bfloat16
     group = None
-    if ws > 1:
+    if ws > 1 or args.force_ep:
+        # --force-ep runs the expert-parallel code path (NCCL exchanges on the
+        # side stream, max-over-ranks timing) even on one rank — a smoke test
+        # of the multi-GPU bench on a single GPU
         import torch.distributed as dist
         group = dist.group.WORLD
     T = w["seq"] * w["seqs"]
@@ -339,7 +342,7 @@ def run_ours(args):
         # the same steps captured once into CUDA graphs and replayed (one
         # launch per step; single GPU — NCCL runs stay eager)
         from paper_2404_05019_b200.runtime import CapturedStep, HostStreamRunner
-        use_graphs = ws == 1 and not args.no_graphs
+        use_graphs = group is None and not args.no_graphs
 
         def fwd(blk):
             return lambda xx: blk(xx)[0]
@@ -460,8 +463,8 @@ def run_ours(args):
                                           f"fp64 oracle of the same block pair", "blas": blas}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -476,6 +479,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-training", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--force-ep", action="store_true",
+                    help="expert-parallel code path even on one rank (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--cpu-reps", type=int, default=3)
