@@ -37,6 +37,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL prints its version banner on stdout at communicator init; stdout must
+# carry the single JSON line only
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 WORKLOADS = {
     # BASELINE.json configs[2]
