@@ -168,6 +168,13 @@ int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap
                          const int32_t* group_rows, int rows_clip, float* out,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* Expert migration (offload.py:109-182 made real): dst[j] = src[ids[j]] for
+ * j < min(*n_rows, max_rows), rows of row_bytes.  src may be pinned host
+ * memory (read over the host link by the kernel, no host synchronisation:
+ * the activated-expert list and its length stay on the device). */
+int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_t* ids,
+                      const int32_t* n_rows, int max_rows, void* dst, void* stream);
+
 /* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);

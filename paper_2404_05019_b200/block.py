@@ -146,6 +146,8 @@ class ScMoEBlockPair(nn.Module):
                                   combine_mode=combine_mode, capacity_factor=capacity_factor,
                                   noise_enabled=noise_enabled, ep_group=ep_group, **kw)
         self.ep_group = ep_group
+        self.offload = None
+        self.offload_mode = "none"
         self.slot: Optional[int] = None
         self.last_costs: Optional[sched.CostVector] = None
         self._comm_stream: Optional[torch.cuda.Stream] = None
@@ -244,6 +246,9 @@ class ScMoEBlockPair(nn.Module):
         # chunked pipelining (standard_pipeline / scmoe_overlap_pipeline,
         # distsim.py:277-300, 358-364): forward only
         chunks = self.chunks if not train else 1
+        off = self.offload if not train else None
+        if off is not None and (use_ep or chunks > 1):
+            raise NotImplementedError("expert offload is a single-GPU, unchunked inference mode")
 
         def gate():
             if train:
@@ -257,6 +262,25 @@ class ScMoEBlockPair(nn.Module):
                 env["dec"] = moe.route(src(), eps=eps, replay=replay)
                 if chunks > 1:
                     env["cr"] = ep_mod.chunk_routing(env["dec"], chunks)
+                if off is not None:
+                    # activated experts -> device slots; async migration starts
+                    # here, at the (shortcut) gate point
+                    env["plan"] = off.plan(env["dec"])
+                    if self.offload_mode == "async":
+                        env["bufs"], env["mig_ev"] = off.migrate_async(env["plan"])
+
+        def encode_offload():
+            dec, plan = env["dec"], env["plan"]
+            env["buf"] = K.dispatch(src(), plan.slot_idx, dec.slots, plan.n_slots, dec.capacity)
+
+        def expert_offload():
+            dec, plan = env["dec"], env["plan"]
+            if self.offload_mode == "async":
+                st.wait_event(env["mig_ev"])
+                bufs = env["bufs"]
+            else:
+                bufs = off.migrate(plan)
+            env["y"] = off.ffn(env["buf"], plan, bufs, dec.capacity)
 
         def encode_chunked():
             # chunk-major buffer (chunks, E, Cc, d): chunk c's exchange is contiguous
@@ -306,6 +330,8 @@ class ScMoEBlockPair(nn.Module):
             dec = env["dec"]
             if chunks > 1:
                 return encode_chunked()
+            if off is not None:
+                return encode_offload()
             if train:
                 buf = TR.DispatchFn.apply(src(), dec.indices, dec.slots, env["kept"], moe.n_experts,
                                           dec.capacity)
@@ -326,6 +352,8 @@ class ScMoEBlockPair(nn.Module):
             dec = env["dec"]
             if chunks > 1:
                 return expert_chunked()
+            if off is not None:
+                return expert_offload()
             if train:
                 e = moe.experts
                 rows = env["recv_counts"] if use_ep else env["kept"]
@@ -359,11 +387,12 @@ class ScMoEBlockPair(nn.Module):
                 return
             if use_ep:
                 st.wait_event(env["y_ev"])
+            cidx = env["plan"].slot_idx if off is not None else dec.indices
             if self.variant == "standard":
-                env["out"] = K.combine(env["y"], dec.indices, dec.slots, dec.weights, dec.capacity,
+                env["out"] = K.combine(env["y"], cidx, dec.slots, dec.weights, dec.capacity,
                                        residual=env["h_mh_cur"])
             else:
-                env["out"] = K.combine(env["y"], dec.indices, dec.slots, dec.weights, dec.capacity,
+                env["out"] = K.combine(env["y"], cidx, dec.slots, dec.weights, dec.capacity,
                                        se_out=env["se"], mode=moe.combine_mode, x_cur=env["x_cur"],
                                        w_cg=moe.w_cg, residual=env["h_mh_cur"])
 
@@ -387,6 +416,24 @@ class ScMoEBlockPair(nn.Module):
             taps["src"] = src()
             return res + (taps,)
         return res
+
+    # -- memory-limited inference -----------------------------------------------
+    def enable_offload(self, mode: str = "async") -> "ScMoEBlockPair":
+        """Move the routed experts to pinned host memory (offload.py).  "async"
+        starts the migration at the gate point (needs the ScMoE shortcut
+        routing to overlap anything), "blocking" right before the expert
+        computation, "none" keeps them resident."""
+        from .offload import MODES, ExpertOffload
+        if mode not in MODES:
+            raise ConfigError(f"unknown offload mode {mode!r}")
+        if mode == "none":
+            return self
+        if self.variant == "dgmoe" or self.ep_group is not None:
+            raise ConfigError("expert offload supports single-GPU ScMoE / shared / top-k layers")
+        if self.offload is None:
+            self.offload = ExpertOffload(self.moe.experts, self.moe.k_routed)
+        self.offload_mode = mode
+        return self
 
     # -- training ----------------------------------------------------------------
     def train_step(self, h_in: torch.Tensor, lr: float = 0.01, aux_coeff: float = 0.01,

@@ -104,6 +104,29 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, int cap, int cols
   for (int i = 0; i < VEC; ++i) o[i] = (s[0][i] + s[1][i]) + (s[2][i] + s[3][i]);
 }
 
+// dst[j] = src[ids[j]] for j < min(*n_rows, max_rows); rows of row_bytes
+// (multiple of 16).  src may be pinned host memory (UVA-mapped): this is the
+// expert-migration copy, 8 x 16-byte loads in flight per thread over PCIe.
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_vecs,
+                                   const int32_t* __restrict__ ids,
+                                   const int32_t* __restrict__ n_rows, int max_rows,
+                                   uint4* __restrict__ dst) {
+  const int j = blockIdx.y;
+  if (j >= max_rows || j >= *n_rows) return;
+  const uint4* s = src + (long long)ids[j] * row_vecs;
+  uint4* d = dst + (long long)j * row_vecs;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < row_vecs; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = s[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[i + u * stride] = v[u];
+  }
+  for (; i < row_vecs; i += stride) d[i] = s[i];
+}
+
 __global__ void colsum_final_kernel(const float* __restrict__ part, int n_chunks, int cols,
                                     int n_groups, float* __restrict__ out) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -264,6 +287,22 @@ extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, in
   const long long n = (long long)num_groups * cols;
   colsum_final_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n_chunks, cols,
                                                                    num_groups, out);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_t* ids,
+                                 const int32_t* n_rows, int max_rows, void* dst, void* stream) {
+  SCMOE_CHECK_ARG(row_bytes % 16 == 0 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0,
+                  "gather rows must be 16-byte multiples and aligned");
+  SCMOE_CHECK_ARG(max_rows >= 0 && ids && n_rows, "bad gather arguments");
+  if (max_rows == 0 || row_bytes == 0) return SCMOE_OK;
+  const long long vecs = (long long)(row_bytes / 16);
+  long long per_row = (vecs + 256 * 8 - 1) / (256 * 8);
+  if (per_row > 64) per_row = 64;   // ~64 CTAs per row saturate the host link
+  dim3 grid((unsigned)per_row, (unsigned)max_rows);
+  gather_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, vecs, ids, n_rows,
+                                                            max_rows, (uint4*)dst);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

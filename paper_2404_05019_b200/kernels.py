@@ -228,6 +228,19 @@ def grouped_wgrad(a: torch.Tensor, b: torch.Tensor, n_wgroups: int = 1,
     return out if (a.dim() == 3 or n_wgroups > 1) else out.view(M, N)
 
 
+def gather_rows(src: torch.Tensor, ids: torch.Tensor, n_rows: torch.Tensor, max_rows: int,
+                out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out[j] = src[ids[j]] for j < min(n_rows, max_rows); src may be pinned
+    host memory (the kernel reads it over the host link)."""
+    ensure_device(out)
+    if src.is_cuda is False and not src.is_pinned():
+        raise ValueError("host-side source rows must be in pinned memory")
+    row_bytes = src[0].numel() * src.element_size()
+    check(lib().scmoe_gather_rows(ptr(_c(src, "src")), row_bytes, ptr(_c(ids, "ids")),
+                                  ptr(n_rows), max_rows, ptr(_c(out, "out")), stream_ptr(stream)))
+    return out
+
+
 _ONES = {}
 
 
