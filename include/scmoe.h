@@ -77,8 +77,12 @@ int scmoe_device_check(int device);
  * constraint (arch.py:447-460): the top-1 over the remaining experts is the
  * runner-up exactly when the best expert clashes.  x is (T, d) with row stride
  * ld_x elements, dtype SCMOE_F32 or SCMOE_BF16.  N <= 64, 1 <= k <= min(N, 8).
+ * bf16 tokens without noise and N <= 16 take the tensor-core logit path
+ * (mma.sync on a 3-part bf16 split of the fp32 weights, fp32 accumulate).
+ * The workspace (size from scmoe_gate_workspace_bytes) holds the tile
+ * counters, per-tile status words and the split-weight blob.
  */
-size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts);
+size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts, int d_model);
 int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                     const float* w_gate_t, const float* w_noise_t, const float* eps,
                     const int32_t* exclude,

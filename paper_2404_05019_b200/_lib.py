@@ -30,7 +30,7 @@ SIGNATURES = [
     ("scmoe_version", _i, []),
     ("scmoe_last_error", ctypes.c_char_p, []),
     ("scmoe_device_check", _i, [_i]),
-    ("scmoe_gate_workspace_bytes", _sz, [_i, _i]),
+    ("scmoe_gate_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_gate_topk", _i, [_vp, _i, _ll, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                              _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     ("scmoe_dispatch", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),

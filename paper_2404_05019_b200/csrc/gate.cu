@@ -18,19 +18,30 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace scmoe {
+
+int make_map_2d(CUtensorMap* map, const void* base, int inner, int outer,
+                long long row_stride_bytes, int box_outer);   // gemm_sm100.cu
+
 namespace {
 
 constexpr int TOK = 64;        // tokens per CTA
 constexpr int TPT = 4;         // threads per token in phase 1
 constexpr int THREADS = TOK * TPT;
-constexpr int ROUTE_WARPS = TOK / 32;
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
 constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 constexpr size_t CTR_BYTES = 256;
+
+// workspace = [counters | per-tile status (or tile counts) | per-tile prob partials]
+__host__ __device__ inline size_t gate_ws_bytes(int n_tok, int n_exp) {
+  const size_t tiles = (size_t)((n_tok + 63) / 64);
+  return (CTR_BYTES + 2 * tiles * (size_t)n_exp * 4 + 15) & ~(size_t)15;
+}
 
 __device__ __forceinline__ bool gt_nan_last(float a, float b) {
   // a ranks above b: larger value; NaN ranks below everything (numpy sorts
@@ -51,6 +62,265 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Barrier over the first NTHR threads of the CTA (the routing threads; the
+// tensor-core kernel's producer warp does not take part).
+template <int NTHR, int BAR = 1>
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTHR) : "memory");
+}
+
+// Phase 2, shared by both logit kernels, in two halves so the tensor-core
+// kernel can run the look-back of tile i after the logits of tile i+1:
+//   route_publish — one thread per token: top-k (strict '>', lowest index
+//     wins ties), weights, full-softmax partials, per-expert ballots -> ranks
+//     inside the tile; publishes the tile's per-expert AGGREGATE at once;
+//   route_finish  — decoupled look-back over the (flag | count) words of the
+//     earlier tiles -> exclusive count = capacity slot base; slots / drops;
+//     the last tile reduces the per-tile probability partials in a fixed order.
+template <int NMAX, int TOK_>
+struct RouteState {            // survives between publish and finish (shared memory)
+  int tile;
+  uint32_t agg[NMAX];
+  int8_t sel[TOK_][SCMOE_MAX_K];
+  int32_t lr[TOK_][SCMOE_MAX_K];   // rank of the selection inside its tile
+};
+
+// LOCAL = true (tensor-core gate): no look-back at all — the in-tile rank of
+// every selection goes to `slots` and the tile's per-expert count to
+// status[tile][e]; gate_slots_kernel adds the prefix over earlier tiles.
+template <int NMAX, int TOK_, int THREADS_, int BASE = 0, int BAR = 1, bool LOCAL = false>
+__device__ __forceinline__ void route_publish(
+    const float (*s_logit)[NMAX + 1], RouteState<NMAX, TOK_>& rs, int tile,
+    const int32_t* __restrict__ exclude, int n_tok, int N, int k, float* __restrict__ logits,
+    int32_t* __restrict__ indices, float* __restrict__ weights, int32_t* __restrict__ counts,
+    uint32_t* __restrict__ status, float* __restrict__ psum, int32_t* __restrict__ slots = nullptr) {
+  constexpr int RW = TOK_ / 32;
+  __shared__ int s_wcnt[RW][NMAX];
+  __shared__ float s_wprob[RW][NMAX];
+  const int tid = (int)threadIdx.x - BASE;
+  const int warp = tid >> 5, lane = tid & 31;
+  int sel[SCMOE_MAX_K];
+  int rank[SCMOE_MAX_K];
+  const int t = tile * TOK_ + tid;
+  const bool valid = (tid < TOK_) && (t < n_tok);
+  if (tid < TOK_) {
+    float h[NMAX];
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tid][e] : 0.f;
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e)
+        if (e < N) logits[(long long)t * N + e] = h[e];
+    }
+    // top-k: repeated argmax with strict '>' (lowest index wins ties).  An
+    // excluded expert (DGMoE distinct-expert constraint, arch.py:453-457) is
+    // skipped, so the pick becomes the runner-up exactly when it would clash.
+    uint64_t blocked = 0;
+    if (exclude && valid) {
+      const int ex = exclude[t];
+      if (ex >= 0 && ex < N) blocked = 1ull << ex;
+    }
+    uint64_t selmask = 0;
+    float selv[SCMOE_MAX_K];
+#pragma unroll
+    for (int j = 0; j < SCMOE_MAX_K; ++j) {
+      sel[j] = 0;
+      selv[j] = 0.f;
+      rank[j] = 0;
+      if (j < k) {
+        int bi = -1;
+        float bv = 0.f;
+#pragma unroll
+        for (int e = 0; e < NMAX; ++e) {
+          if (e < N && !(((selmask | blocked) >> e) & 1ull)) {
+            if (bi < 0 || gt_nan_last(h[e], bv)) {
+              bi = e;
+              bv = h[e];
+            }
+          }
+        }
+        sel[j] = bi;
+        selv[j] = bv;
+        selmask |= 1ull << bi;
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < SCMOE_MAX_K; ++j) {
+        if (j < k) {
+          const long long o = (long long)t * k + j;
+          indices[o] = sel[j];
+          // softmax over the kept logits, stabilised by the top logit
+          float den = 0.f;
+#pragma unroll
+          for (int q = 0; q < SCMOE_MAX_K; ++q)
+            if (q < k) den += expf(selv[q] - selv[0]);
+          weights[o] = (k == 1) ? 1.0f : expf(selv[j] - selv[0]) / den;
+        }
+      }
+    }
+    // full-softmax probabilities for the balance-loss mean (arch.py:484-485)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e)
+      if (e < N) mx = fmaxf(mx, h[e]);
+    float ex[NMAX];
+    float den = 0.f;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) {
+      ex[e] = (e < N) ? expf(h[e] - mx) : 0.f;
+      den += ex[e];
+    }
+    const float inv = 1.f / den;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) {
+      if (e < N) {
+        const bool mine = valid && ((selmask >> e) & 1ull);
+        const unsigned b = __ballot_sync(0xffffffffu, mine);
+        const float p = warp_sum(valid ? ex[e] * inv : 0.f);
+        if (lane == 0) {
+          s_wcnt[warp][e] = __popc(b);
+          s_wprob[warp][e] = p;
+        }
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < SCMOE_MAX_K; ++j)
+            if (j < k && sel[j] == e) rank[j] = __popc(b & lt);
+        }
+      }
+    }
+  }
+  consumer_sync<THREADS_, BAR>();
+
+  // per-expert tile aggregate and within-tile warp offsets; publish the
+  // aggregate at once so later tiles can make progress
+  if (tid < N) {
+    const int e = tid;
+    uint32_t run = 0;
+    float psum_tile = 0.f;
+#pragma unroll
+    for (int w = 0; w < RW; ++w) {
+      const int c = s_wcnt[w][e];
+      s_wcnt[w][e] = (int)run;
+      run += (uint32_t)c;
+      psum_tile += s_wprob[w][e];
+    }
+    psum[(size_t)tile * N + e] = psum_tile;
+    if (LOCAL) {
+      status[(size_t)tile * N + e] = run;
+    } else {
+      rs.agg[e] = run;
+      st_volatile_u32(status + (size_t)tile * N + e, (tile == 0 ? FLAG_INC : FLAG_AGG) | run);
+      if (run) atomicAdd(&counts[e], (int)run);
+      __threadfence();
+    }
+  }
+  if (!LOCAL && tid == 0) rs.tile = tile;
+  consumer_sync<THREADS_, BAR>();
+  if (valid) {
+#pragma unroll
+    for (int j = 0; j < SCMOE_MAX_K; ++j) {
+      if (j < k) {
+        const int lr = s_wcnt[warp][sel[j]] + rank[j];
+        if (LOCAL) {
+          slots[(long long)t * k + j] = lr;
+        } else {
+          rs.sel[tid][j] = (int8_t)sel[j];
+          rs.lr[tid][j] = lr;
+        }
+      }
+    }
+  }
+}
+
+template <int NMAX, int TOK_, int THREADS_, int BASE = 0, int BAR = 1>
+__device__ __forceinline__ void route_finish(
+    RouteState<NMAX, TOK_>& rs, int n_tok, int N, int k, int quota, int32_t* __restrict__ slots,
+    uint8_t* __restrict__ dropped, float* __restrict__ prob_sum, uint32_t* __restrict__ ctrs,
+    uint32_t* __restrict__ status, const float* __restrict__ psum, int num_tiles) {
+  __shared__ uint32_t s_excl[NMAX];
+  __shared__ int s_last;
+  const int tid = (int)threadIdx.x - BASE;
+  const int warp = tid >> 5, lane = tid & 31;
+  consumer_sync<THREADS_, BAR>();     // publish's shared state is complete
+  const int tile = rs.tile;
+  // decoupled look-back, one warp per expert, 32 predecessor tiles per step:
+  // lane l reads tile (j - l); the nearest INCLUSIVE word ends the walk, every
+  // word before it must at least carry its AGGREGATE.  Tiles finish phase 1 at
+  // about the same time, so a one-tile-per-step walk would serialise ~T/TOK
+  // dependent loads.
+  for (int e = warp; e < N; e += THREADS_ / 32) {
+    const uint32_t agg = rs.agg[e];
+    uint32_t excl = 0;
+    if (tile > 0) {
+      int j = tile - 1;
+      while (true) {
+        const int jj = j - lane;
+        const uint32_t v = jj >= 0 ? ld_volatile_u32(status + (size_t)jj * N + e) : FLAG_INC;
+        const uint32_t f = v & ~VAL_MASK;
+        const unsigned inc = __ballot_sync(0xffffffffu, f == FLAG_INC);
+        const unsigned not_ready = __ballot_sync(0xffffffffu, f == 0);
+        const int first = inc ? __ffs(inc) - 1 : 31;              // last lane that counts
+        const unsigned span = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if (not_ready & span) continue;                          // retry the same window
+        uint32_t part = (lane <= first) ? (v & VAL_MASK) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (inc) break;
+        j -= 32;
+      }
+      if (lane == 0) st_volatile_u32(status + (size_t)tile * N + e, FLAG_INC | (excl + agg));
+    }
+    __syncwarp();
+    if (lane == 0) s_excl[e] = excl;
+  }
+  consumer_sync<THREADS_, BAR>();
+
+  const int t = tile * TOK_ + tid;
+  if (tid < TOK_ && t < n_tok) {
+#pragma unroll
+    for (int j = 0; j < SCMOE_MAX_K; ++j) {
+      if (j < k) {
+        const int slot = (int)s_excl[rs.sel[tid][j]] + rs.lr[tid][j];
+        const long long o = (long long)t * k + j;
+        slots[o] = slot;
+        dropped[o] = slot >= quota ? 1 : 0;
+      }
+    }
+  }
+
+  // the last tile to finish reduces the per-tile probability sums
+  if (tid == 0) {
+    const uint32_t prev = atomicAdd(&ctrs[1], 1u);
+    s_last = (prev == (uint32_t)num_tiles - 1u);
+  }
+  consumer_sync<THREADS_, BAR>();
+  if (s_last) {
+    // all THREADS_ threads: thread (e, p) sums tiles p, p + P, ... (independent
+    // loads in flight), then the P partials are added in order — a fixed
+    // summation order, so prob_sum is deterministic
+    constexpr int P = THREADS_ / NMAX;
+    __shared__ float s_red[P][NMAX];
+    __threadfence();
+    const int e = tid % NMAX, p = tid / NMAX;
+    if (p < P) {
+      float s = 0.f;
+      if (e < N)
+        for (int j = p; j < num_tiles; j += P) s += __ldcg(psum + (size_t)j * N + e);
+      s_red[p][e] = s;
+    }
+    consumer_sync<THREADS_, BAR>();
+    if (tid < N) {
+      float s = 0.f;
+#pragma unroll 1
+      for (int q = 0; q < P; ++q) s += s_red[q][tid];
+      prob_sum[tid] = s;
+    }
+  }
+}
+
 template <typename T, int NMAX, bool NOISE>
 __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
     const T* __restrict__ x, long long ld_x, const float* __restrict__ wg_t,
@@ -64,11 +334,7 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
   extern __shared__ float4 dyn_smem4[];
   float* wsm = reinterpret_cast<float*>(dyn_smem4);  // [(1+NOISE)][N][dc_max]
   __shared__ float s_logit[TOK][NMAX + 1];
-  __shared__ int s_wcnt[ROUTE_WARPS][NMAX];
-  __shared__ float s_wprob[ROUTE_WARPS][NMAX];
-  __shared__ uint32_t s_excl[NMAX];
   __shared__ uint32_t s_tile;
-  __shared__ int s_last;
 
   constexpr int VEC = Vec16<T>::N;
   const int tid = threadIdx.x;
@@ -188,172 +454,415 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
   }
   __syncthreads();
 
-  // ---------------- phase 2: routing, one thread per token -----------------
-  const int warp = tid >> 5, lane = tid & 31;
-  int sel[SCMOE_MAX_K];
-  float selv[SCMOE_MAX_K];
-  int rank[SCMOE_MAX_K];
-  const int t = tile * TOK + tid;
-  const bool valid = (tid < TOK) && (t < n_tok);
-  if (tid < TOK) {
-    float h[NMAX];
-#pragma unroll
-    for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tid][e] : 0.f;
-    if (valid) {
-#pragma unroll
-      for (int e = 0; e < NMAX; ++e)
-        if (e < N) logits[(long long)t * N + e] = h[e];
+  __shared__ RouteState<NMAX, TOK> rs;
+  route_publish<NMAX, TOK, THREADS>(s_logit, rs, tile, exclude, n_tok, N, k, logits, indices,
+                                    weights, counts, status, psum);
+  route_finish<NMAX, TOK, THREADS>(rs, n_tok, N, k, quota, slots, dropped, prob_sum, ctrs, status,
+                                   psum, num_tiles);
+}
+
+// ---------------------------------------------------------------------------
+// K1 tensor-core variant (bf16 tokens, no noise, N <= 16, d >= 64).
+//
+// Logits run on mma.sync.m16n8k16 (bf16 x bf16 -> fp32).  The fp32 gate
+// weights are split into three bf16 parts w = w0 + w1 + w2 (8 + 8 +
+// 8 mantissa bits: the whole fp32 mantissa), each multiplied exactly, so the
+// logits keep fp32-level accuracy while the FMA pipe no longer bounds the pass
+// over x.
+//
+// Persistent and warp-specialised, one CTA per SM, tiles of TOK tokens
+// assigned round-robin (no cross-tile dependency: gate_slots_kernel adds the
+// capacity-slot prefix over tiles afterwards).
+//   producer warp  — per stage, KC/64 TMA boxes of TOK rows x 64 columns
+//                    (cp.async.bulk.tensor.2d, 128B swizzle, OOB rows/columns
+//                    zero-filled) plus the matching slice of the split-weight
+//                    blob (gate_split_weights_kernel; one 1-D bulk copy),
+//                    completion on the stage's "full" mbarrier.  Per-row 1-D copies of x were measured
+//                    issue-bound (~1.8 TB/s at 512 B per copy); boxes are not;
+//   8 MMA warps    — warp w takes m16 tile w%4 and half w/4 of the stage's k16
+//                    steps: ldmatrix.x4 A fragments, B fragments as 8-byte
+//                    shared loads, one accumulator chain per weight part; the two
+//                    halves' partial logits are summed in a fixed order into a
+//                    double-buffered logits tile;
+//   4 routing warps — route_publish(LOCAL) per tile (top-k, weights, in-tile
+//                    ranks, per-expert tile counts, softmax partials), off the
+//                    MMA warps' critical path.
+constexpr int GT_KC = 256;                       // columns per stage (4 TMA boxes)
+constexpr int GT_BOXB = TOK * 128;               // one 64-col x TOK-row box, 128B swizzle
+constexpr int GT_XB = (GT_KC / 64) * GT_BOXB;    // x part of a stage
+constexpr int GT_GROUP_B = 3072;                 // split-weight blob bytes per 64 columns per n8 tile
+constexpr int GT_CONSUMERS = 8;                  // MMA warps 0..7
+constexpr int GT_PRODUCER = GT_CONSUMERS;        // warp 8
+constexpr int GT_ROUTERS = 4;                    // routing warps 9..12
+constexpr int GT_ROUTE_BASE = (GT_CONSUMERS + 1) * 32;
+constexpr int GT_THREADS = (GT_CONSUMERS + 1 + GT_ROUTERS) * 32;
+
+template <int NT> struct GateTC {
+  static constexpr int STAGES = NT == 1 ? 4 : 3;
+  static constexpr int BLOBB = (GT_KC / 64) * GT_GROUP_B * NT;
+  static constexpr int STAGEB = GT_XB + BLOBB;
+  static constexpr int SMEM = STAGES * STAGEB + 1024;   // + alignment slack (swizzle atoms)
+  static_assert(STAGEB % 1024 == 0, "stages must stay 1024-byte aligned");
+};
+
+__device__ __forceinline__ void mma_bf16_16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+  return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void ldmatrix_x4(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+
+// Split fp32 gate weights (N, d) into the blob the tensor-core kernel stages:
+// per 64-column group [nt][part 3][k16 step 4][lane 32] x uint2, lane
+// (g = lane/4, c = lane%4) of step s holding the mma B fragment
+//   (w[n][k0+2c], w[n][k0+2c+1]), (w[n][k0+2c+8], w[n][k0+2c+9]),
+// n = nt*8 + g, k0 = 64*group + 16*s.  Experts >= N and columns >= d are zero.
+// (Splitting on the fly inside the MMA warps was measured ~1.5x slower.)
+template <int NT>
+__global__ void gate_split_weights_kernel(const float* __restrict__ wg_t, int d, int N, int ngrp,
+                                          uint2* __restrict__ blob) {
+  const int total = ngrp * NT * 4 * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ln = i & 31, st = (i >> 5) & 3, rest = i >> 7;
+    const int nt = rest % NT, gg = rest / NT;
+    const int n = nt * 8 + (ln >> 2);
+    const int k0 = gg * 64 + st * 16 + 2 * (ln & 3);
+    float w[4] = {0.f, 0.f, 0.f, 0.f};
+    if (n < N) {     // d % 8 == 0: pairs (k0, k0+1) and (k0+8, k0+9) are all-in or all-out
+      const float* row = wg_t + (long long)n * d;
+      if (k0 < d) {
+        w[0] = row[k0];
+        w[1] = row[k0 + 1];
+      }
+      if (k0 + 8 < d) {
+        w[2] = row[k0 + 8];
+        w[3] = row[k0 + 9];
+      }
     }
-    // top-k: repeated argmax with strict '>' (lowest index wins ties).  An
-    // excluded expert (DGMoE distinct-expert constraint, arch.py:453-457) is
-    // skipped, so the pick becomes the runner-up exactly when it would clash.
-    uint64_t blocked = 0;
-    if (exclude && valid) {
-      const int ex = exclude[t];
-      if (ex >= 0 && ex < N) blocked = 1ull << ex;
+    __nv_bfloat16 p[3][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      p[0][q] = __float2bfloat16_rn(w[q]);
+      const float r1 = w[q] - __bfloat162float(p[0][q]);
+      p[1][q] = __float2bfloat16_rn(r1);
+      p[2][q] = __float2bfloat16_rn(r1 - __bfloat162float(p[1][q]));
     }
-    uint64_t selmask = 0;
 #pragma unroll
-    for (int j = 0; j < SCMOE_MAX_K; ++j) {
-      sel[j] = 0;
-      selv[j] = 0.f;
-      rank[j] = 0;
-      if (j < k) {
-        int bi = -1;
-        float bv = 0.f;
+    for (int part = 0; part < 3; ++part)
+      blob[(((size_t)(gg * NT + nt) * 3 + part) * 4 + st) * 32 + ln] =
+          make_uint2(pack_bf16(p[part][0], p[part][1]), pack_bf16(p[part][2], p[part][3]));
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
+    const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ blob,
+    const int32_t* __restrict__ exclude, int n_tok, int d, int N, int k, int quota,
+    float* __restrict__ logits, int32_t* __restrict__ indices, float* __restrict__ weights,
+    int32_t* __restrict__ slots, uint8_t* __restrict__ dropped, int32_t* __restrict__ counts,
+    float* __restrict__ prob_sum, uint32_t* __restrict__ ctrs, uint32_t* __restrict__ status,
+    float* __restrict__ psum, int num_tiles) {
+  using C = GateTC<NT>;
+  constexpr int NMAX = NT * 8;
+  constexpr int S = C::STAGES;
+  extern __shared__ __align__(128) uint8_t gsm_raw[];
+  uint8_t* gsm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
+  __shared__ float s_logit[2][TOK][NMAX + 1];     // MMA warps -> routing warps
+  __shared__ float s_part[2][TOK][NMAX + 1];
+  __shared__ __align__(8) uint64_t full_bar[S], empty_bar[S], lfull_bar[2], lempty_bar[2];
+  __shared__ int s_stage_tile[S], s_logit_tile[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkc = (d + GT_KC - 1) / GT_KC;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], GT_CONSUMERS);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&lfull_bar[i], GT_CONSUMERS);
+      mbar_init(&lempty_bar[i], GT_ROUTERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp > GT_PRODUCER) {
+    // ---------------- routing warps ----------------
+    // per tile: top-k, weights, in-tile ranks and per-expert tile counts (no
+    // cross-tile dependency; gate_slots_kernel adds the tile prefix)
+    __shared__ RouteState<NMAX, TOK> rs;
+    constexpr int RT = GT_ROUTERS * 32;
+    for (uint32_t n = 0;; ++n) {
+      const int b = n & 1;
+      mbar_wait(&lfull_bar[b], (n >> 1) & 1);
+      const int tile = s_logit_tile[b];
+      if (tile < 0) break;
+      route_publish<NMAX, TOK, RT, GT_ROUTE_BASE, 2, true>(s_logit[b], rs, tile, exclude, n_tok, N,
+                                                           k, logits, indices, weights, counts,
+                                                           status, psum, slots);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lempty_bar[b]);   // publish read s_logit[b] before its barrier
+    }
+    return;
+  }
+
+  if (warp == GT_PRODUCER) {
+    // ---------------- producer warp ----------------
+    // static round-robin tiles (no cross-tile dependency in this kernel)
+    uint32_t it = 0;
+    for (int tile = blockIdx.x;; tile += gridDim.x) {
+      const bool live = tile < num_tiles;
+      const int row0 = tile * TOK;
+      for (int kc = 0; kc < (live ? nkc : 1); ++kc, ++it) {
+        const int s = it % S;
+        mbar_wait(&empty_bar[s], ((it / S) & 1) ^ 1);
+        if (!live) {
+          if (lane == 0) {
+            s_stage_tile[s] = -1;
+            mbar_arrive(&full_bar[s]);
+          }
+          break;
+        }
+        const int c0 = kc * GT_KC;
+        const int nbox = (min(GT_KC, d - c0) + 63) / 64;
+        const uint32_t blobb = (uint32_t)nbox * GT_GROUP_B * NT;
+        uint8_t* st = gsm + (size_t)s * C::STAGEB;
+        if (lane == 0) {
+          s_stage_tile[s] = tile;
+          mbar_expect_tx(&full_bar[s], (uint32_t)nbox * GT_BOXB + blobb);
+          bulk_g2s(st + GT_XB, blob + (size_t)(c0 / 64) * GT_GROUP_B * NT, blobb, &full_bar[s]);
+          for (int b = 0; b < nbox; ++b)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3}], [%4];"
+                ::"r"(smem_u32(st + b * GT_BOXB)), "l"(&xmap), "r"(c0 + 64 * b), "r"(row0),
+                  "r"(smem_u32(&full_bar[s]))
+                : "memory");
+        }
+        __syncwarp();
+      }
+      if (!live) break;
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int mt = warp & 3, kh = warp >> 2;
+  const int g = lane >> 2, c = lane & 3;
+  // ldmatrix.x4 lane address: matrices (rows 0-7 | 8-15) x (k 0-7 | 8-15);
+  // 128B swizzle: 16-byte chunk q of box row r sits at chunk q ^ (r % 8)
+  const int lrow = mt * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+  const int lhi = lane >> 4;
+  uint32_t it = 0;
+  for (uint32_t n = 0;; ++n) {
+    float acc[3][NT][4];
 #pragma unroll
-        for (int e = 0; e < NMAX; ++e) {
-          if (e < N && !(((selmask | blocked) >> e) & 1ull)) {
-            if (bi < 0 || gt_nan_last(h[e], bv)) {
-              bi = e;
-              bv = h[e];
-            }
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][nt][q] = 0.f;
+    int tile = -1;
+    for (int kc = 0; kc < nkc; ++kc, ++it) {
+      const int s = it % S;
+      mbar_wait(&full_bar[s], (it / S) & 1);
+      tile = s_stage_tile[s];
+      if (tile < 0) break;
+      const uint8_t* st = gsm + (size_t)s * C::STAGEB;
+      const int nsteps = (min(GT_KC, d - kc * GT_KC) + 63) / 64 * 4;
+      const int half = nsteps / 2;                       // whole boxes: a multiple of 4
+      const uint32_t abase = smem_u32(st) + lrow * 128;
+      const uint2* bl = reinterpret_cast<const uint2*>(st + GT_XB);
+      for (int j = kh * half; j < (kh + 1) * half; ++j) {
+        uint32_t a[4];
+        const int q = ((j & 3) * 2 + lhi) ^ (lrow & 7);
+        ldmatrix_x4(a, abase + (j >> 2) * GT_BOXB + q * 16);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            const uint2 b = bl[((((j >> 2) * NT + nt) * 3 + p) * 4 + (j & 3)) * 32 + lane];
+            mma_bf16_16816(acc[p][nt], a[0], a[1], a[2], a[3], b.x, b.y);
           }
         }
-        sel[j] = bi;
-        selv[j] = bv;
-        selmask |= 1ull << bi;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+    const int b = n & 1;
+    mbar_wait(&lempty_bar[b], ((n >> 1) & 1) ^ 1);      // routing done with buffer b
+    if (tile >= 0) {
+      // partial logits, smallest weight part first; C fragment rows g / g+8,
+      // experts nt*8 + 2c + {0,1}
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int e = nt * 8 + 2 * c;
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = (acc[2][nt][q] + acc[1][nt][q]) + acc[0][nt][q];
+        s_part[kh][mt * 16 + g][e] = v[0];
+        s_part[kh][mt * 16 + g][e + 1] = v[1];
+        s_part[kh][mt * 16 + g + 8][e] = v[2];
+        s_part[kh][mt * 16 + g + 8][e + 1] = v[3];
+      }
+      consumer_sync<GT_CONSUMERS * 32>();
+      for (int i = tid; i < TOK * NMAX; i += GT_CONSUMERS * 32) {
+        const int t = i / NMAX, e = i % NMAX;
+        s_logit[b][t][e] = s_part[0][t][e] + s_part[1][t][e];
       }
     }
-    // full-softmax probabilities for the balance-loss mean (arch.py:484-485)
-    float mx = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < NMAX; ++e)
-      if (e < N) mx = fmaxf(mx, h[e]);
-    float ex[NMAX];
-    float den = 0.f;
-#pragma unroll
-    for (int e = 0; e < NMAX; ++e) {
-      ex[e] = (e < N) ? expf(h[e] - mx) : 0.f;
-      den += ex[e];
-    }
-    const float inv = 1.f / den;
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int e = 0; e < NMAX; ++e) {
-      if (e < N) {
-        const bool mine = valid && ((selmask >> e) & 1ull);
-        const unsigned b = __ballot_sync(0xffffffffu, mine);
-        const float p = warp_sum(valid ? ex[e] * inv : 0.f);
-        if (lane == 0) {
-          s_wcnt[warp][e] = __popc(b);
-          s_wprob[warp][e] = p;
-        }
-        if (mine) {
-#pragma unroll
-          for (int j = 0; j < SCMOE_MAX_K; ++j)
-            if (j < k && sel[j] == e) rank[j] = __popc(b & lt);
-        }
-      }
-    }
+    if (tid == 0) s_logit_tile[b] = tile;
+    consumer_sync<GT_CONSUMERS * 32>();   // s_part reads done before the next tile's writes
+    if (lane == 0) mbar_arrive(&lfull_bar[b]);
+    if (tile < 0) break;
   }
-  __syncthreads();
+}
 
-  // per-expert tile aggregate and within-tile warp offsets; publish the
-  // aggregate at once so later tiles can make progress
-  if (tid < N) {
-    const int e = tid;
-    uint32_t run = 0;
-    float psum_tile = 0.f;
-#pragma unroll
-    for (int w = 0; w < ROUTE_WARPS; ++w) {
-      const int c = s_wcnt[w][e];
-      s_wcnt[w][e] = (int)run;
-      run += (uint32_t)c;
-      psum_tile += s_wprob[w][e];
-    }
-    s_excl[e] = run;  // temporarily: this tile's aggregate
-    st_volatile_u32(status + (size_t)tile * N + e, (tile == 0 ? FLAG_INC : FLAG_AGG) | run);
-    if (run) atomicAdd(&counts[e], (int)run);
-    psum[(size_t)tile * N + e] = psum_tile;
-    __threadfence();
-  }
+// Second pass of the tensor-core gate.  Tile b's capacity-slot base for
+// expert e is the sum of the tile counts of tiles < b.  Every CTA loads the
+// whole (tiles, N) count table into shared memory with coalesced loads and
+// scans it (one warp per expert column, a warp-wide exclusive scan over
+// per-lane runs), then rewrites the in-tile ranks of its tiles (round robin)
+// into capacity slots and drop flags.  CTA 0 writes counts[] and prob_sum[]
+// (fixed summation order: deterministic).
+template <int NMAX>
+__global__ void __launch_bounds__(256) gate_slots_kernel(
+    const int32_t* __restrict__ indices, int32_t* __restrict__ slots, uint8_t* __restrict__ dropped,
+    const uint32_t* __restrict__ tile_counts, const float* __restrict__ psum,
+    int32_t* __restrict__ counts, float* __restrict__ prob_sum, int n_tok, int N, int k, int quota,
+    int num_tiles) {
+  extern __shared__ uint32_t s_tab[];          // [N][num_tiles + 1] -> exclusive prefix
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ent = num_tiles * N, ld = num_tiles + 1;   // padded rows: conflict-free
+  for (int m = tid; m < ent; m += 256) s_tab[(m % N) * ld + m / N] = tile_counts[m];
   __syncthreads();
-  // decoupled look-back, one warp per expert, 32 predecessor tiles per step:
-  // lane l reads tile (j - l); the nearest INCLUSIVE word ends the walk, every
-  // word before it must at least carry its AGGREGATE.  Tiles finish phase 1 at
-  // about the same time, so a one-tile-per-step walk would serialise ~T/TOK
-  // dependent loads.
-  for (int e = warp; e < N; e += THREADS / 32) {
-    const uint32_t agg = s_excl[e];
-    uint32_t excl = 0;
-    if (tile > 0) {
-      int j = tile - 1;
-      while (true) {
-        const int jj = j - lane;
-        const uint32_t v = jj >= 0 ? ld_volatile_u32(status + (size_t)jj * N + e) : FLAG_INC;
-        const uint32_t f = v & ~VAL_MASK;
-        const unsigned inc = __ballot_sync(0xffffffffu, f == FLAG_INC);
-        const unsigned not_ready = __ballot_sync(0xffffffffu, f == 0);
-        const int first = inc ? __ffs(inc) - 1 : 31;              // last lane that counts
-        const unsigned span = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
-        if (not_ready & span) continue;                          // retry the same window
-        uint32_t part = (lane <= first) ? (v & VAL_MASK) : 0u;
+  // one warp per expert row: 32 consecutive tiles per round, warp inclusive
+  // scan, running carry
+  for (int e = warp; e < N; e += 8) {
+    uint32_t carry = 0;
+    uint32_t* row = s_tab + e * ld;
+    for (int j0 = 0; j0 < num_tiles; j0 += 32) {
+      const int j = j0 + lane;
+      const uint32_t v = j < num_tiles ? row[j] : 0u;
+      uint32_t incl = v;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        excl += part;
-        if (inc) break;
-        j -= 32;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
       }
-      if (lane == 0) st_volatile_u32(status + (size_t)tile * N + e, FLAG_INC | (excl + agg));
+      if (j < num_tiles) row[j] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    __syncwarp();
-    if (lane == 0) s_excl[e] = excl;
+    if (blockIdx.x == 0 && lane == 0) counts[e] = (int)carry;
   }
   __syncthreads();
-
-  if (valid) {
-#pragma unroll
-    for (int j = 0; j < SCMOE_MAX_K; ++j) {
-      if (j < k) {
-        const int e = sel[j];
-        const int slot = (int)s_excl[e] + s_wcnt[warp][e] + rank[j];
-        const long long o = (long long)t * k + j;
-        indices[o] = e;
-        slots[o] = slot;
-        dropped[o] = slot >= quota ? 1 : 0;
-        // softmax over the kept logits, stabilised by the top logit
-        float den = 0.f;
-#pragma unroll
-        for (int q = 0; q < SCMOE_MAX_K; ++q)
-          if (q < k) den += expf(selv[q] - selv[0]);
-        weights[o] = (k == 1) ? 1.0f : expf(selv[j] - selv[0]) / den;
-      }
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int i = tid; i < TOK * k; i += 256) {
+      const long long t = (long long)tile * TOK + i / k;
+      if (t >= n_tok) break;
+      const long long o = t * k + i % k;
+      const int slot = (int)s_tab[indices[o] * ld + tile] + slots[o];
+      slots[o] = slot;
+      dropped[o] = slot >= quota ? 1 : 0;
     }
   }
+  if (blockIdx.x == 0) {
+    constexpr int P = 256 / NMAX;
+    __shared__ float s_ps[P][NMAX];
+    const int e = tid % NMAX, p = tid / NMAX;
+    float ps = 0.f;
+    if (e < N)
+      for (int j = p; j < num_tiles; j += P) ps += psum[(size_t)j * N + e];
+    s_ps[p][e] = ps;
+    __syncthreads();
+    if (tid < N) {
+      float fs = 0.f;
+      for (int q = 0; q < P; ++q) fs += s_ps[q][tid];
+      prob_sum[tid] = fs;
+    }
+  }
+}
 
-  // the last tile to finish reduces the per-tile probability sums in order
-  if (tid == 0) {
-    const uint32_t prev = atomicAdd(&ctrs[1], 1u);
-    s_last = (prev == (uint32_t)num_tiles - 1u);
+constexpr int GT_SLOTS_SMEM_MAX = 200 * 1024;   // count table in shared memory
+
+template <int NT>
+int launch_gate_tc(const void* x, long long ld_x, const float* wg, const int32_t* excl, int T_,
+                   int d, int N, int k, int quota, float* logits, int32_t* idx, float* w,
+                   int32_t* slots, uint8_t* drop, int32_t* counts, float* prob_sum, uint8_t* ws,
+                   cudaStream_t st) {
+  using C = GateTC<NT>;
+  const int tiles = (T_ + TOK - 1) / TOK;
+  const int ngrp = (d + 63) / 64;
+  uint32_t* tile_counts = reinterpret_cast<uint32_t*>(ws + CTR_BYTES);
+  float* psum = reinterpret_cast<float*>(ws + CTR_BYTES + (size_t)tiles * N * 4);
+  uint8_t* blob = ws + gate_ws_bytes(T_, N);
+  const size_t tab = (size_t)(tiles + 1) * N * 4;
+  if (tab > (size_t)GT_SLOTS_SMEM_MAX) {
+    set_error("tensor-core gate: %d tokens x %d experts exceed the slot pass's table", T_, N);
+    return SCMOE_ERR_UNSUPPORTED;
   }
-  __syncthreads();
-  if (s_last && tid < N) {
-    __threadfence();
-    float s = 0.f;
-    for (int j = 0; j < num_tiles; ++j) s += __ldcg(psum + (size_t)j * N + tid);
-    prob_sum[tid] = s;
+  {
+    const int total = ngrp * NT * 128;
+    gate_split_weights_kernel<NT><<<(total + 255) / 256, 256, 0, st>>>(wg, d, N, ngrp,
+                                                                       (uint2*)blob);
+    SCMOE_LAUNCH_CHECK();
   }
+  static bool attr_set = false;   // once per instantiation, never inside a graph capture
+  if (!attr_set) {
+    SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_tc_kernel<NT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_slots_kernel<NT * 8>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        GT_SLOTS_SMEM_MAX));
+    attr_set = true;
+  }
+  CUtensorMap xmap;
+  const int rc = make_map_2d(&xmap, x, d, T_, ld_x * 2, TOK);
+  if (rc != SCMOE_OK) return rc;
+  const int grid = min(tiles, num_sms());
+  gate_topk_tc_kernel<NT><<<grid, GT_THREADS, C::SMEM, st>>>(
+      xmap, blob, excl, T_, d, N, k, quota, logits, idx, w, slots, drop, counts, prob_sum, nullptr,
+      tile_counts, psum, tiles);
+  SCMOE_LAUNCH_CHECK();
+  gate_slots_kernel<NT * 8><<<min(tiles, num_sms()), 256, tab, st>>>(
+      idx, slots, drop, tile_counts, psum, counts, prob_sum, T_, N, k, quota, tiles);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
 }
 
 template <typename T, int NMAX>
@@ -425,9 +934,14 @@ int dispatch_nmax(const void* x, long long ld_x, const float* wg, const float* w
 }  // namespace
 }  // namespace scmoe
 
-extern "C" size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts) {
-  const size_t tiles = (size_t)((n_tokens + scmoe::TOK - 1) / scmoe::TOK);
-  return scmoe::CTR_BYTES + 2 * tiles * (size_t)n_experts * 4;
+// Testing hook: 1 routes bf16 gates through the FMA kernel (A/B of the two
+// logit paths).  Not part of the public header.
+extern "C" int scmoe_gate_force_fma = 0;
+
+extern "C" size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts, int d_model) {
+  // + the split-weight blob of the tensor-core path
+  return scmoe::gate_ws_bytes(n_tokens, n_experts) +
+         (size_t)((d_model + 63) / 64) * ((n_experts + 7) / 8) * scmoe::GT_GROUP_B;
 }
 
 extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
@@ -451,10 +965,20 @@ extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
   SCMOE_CHECK_ARG(((uintptr_t)x & 15) == 0, "x must be 16-byte aligned");
   SCMOE_CHECK_ARG((w_noise_t == nullptr) == (eps == nullptr), "w_noise and eps go together");
   SCMOE_CHECK_ARG(!exclude || k < n_experts, "an excluded expert needs k < n_experts");
-  SCMOE_CHECK_ARG(workspace_bytes >= scmoe_gate_workspace_bytes(n_tokens, n_experts),
+  SCMOE_CHECK_ARG(workspace_bytes >= scmoe_gate_workspace_bytes(n_tokens, n_experts, d_model),
                   "gate workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)workspace;
+  if (x_dtype == SCMOE_BF16 && w_noise_t == nullptr && n_experts <= 16 && d_model >= 64 &&
+      !scmoe_gate_force_fma) {
+    const int rc =
+        n_experts <= 8
+            ? launch_gate_tc<1>(x, ld_x, w_gate_t, exclude, n_tokens, d_model, n_experts, k, quota,
+                                logits, indices, weights, slots, dropped, counts, prob_sum, ws, st)
+            : launch_gate_tc<2>(x, ld_x, w_gate_t, exclude, n_tokens, d_model, n_experts, k, quota,
+                                logits, indices, weights, slots, dropped, counts, prob_sum, ws, st);
+    if (rc != SCMOE_ERR_UNSUPPORTED) return rc;
+  }
   if (x_dtype == SCMOE_BF16)
     return dispatch_nmax<__nv_bfloat16>(x, ld_x, w_gate_t, w_noise_t, eps, exclude, n_tokens,
                                         d_model, n_experts, k, quota, logits, indices, weights,

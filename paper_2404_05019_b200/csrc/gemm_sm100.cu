@@ -770,6 +770,30 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
   return SCMOE_OK;
 }
 
+// 2-D bf16 map over a row-major (outer, inner) matrix with row stride
+// row_stride_bytes, box (64, box_outer), 128B swizzle, OOB zero fill (used by
+// the tensor-core gate's token stages).
+int make_map_2d(CUtensorMap* map, const void* base, int inner, int outer,
+                long long row_stride_bytes, int box_outer) {
+  auto fn = sm100::encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return SCMOE_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)row_stride_bytes};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%d outer=%d", (int)r, inner, outer);
+    return SCMOE_ERR_CUDA;
+  }
+  return SCMOE_OK;
+}
+
 }  // namespace scmoe
 
 extern "C" int scmoe_set_gemm_mode(int mode) {

@@ -60,7 +60,7 @@ def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
     dropped = torch.empty(T, k, device=dev, dtype=torch.uint8)
     counts = torch.empty(N, device=dev, dtype=torch.int32)
     prob_sum = torch.empty(N, device=dev, dtype=torch.float32)
-    ws_bytes = lib().scmoe_gate_workspace_bytes(T, N)
+    ws_bytes = lib().scmoe_gate_workspace_bytes(T, N, d)
     ws = torch.empty(ws_bytes, device=dev, dtype=torch.uint8)
     if eps is not None:
         eps = _c(eps.to(torch.float32), "eps")

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_workspace_query_is_host_only():
     so = _lib.load_library()
-    assert so.scmoe_gate_workspace_bytes(16384, 8) >= 256 + 2 * 256 * 8 * 4
+    assert so.scmoe_gate_workspace_bytes(16384, 8, 2048) >= 256 + 2 * 256 * 8 * 4 + 32 * 3072
 
 
 def test_argument_errors_do_not_touch_the_gpu():

@@ -78,6 +78,41 @@ def test_gate_ties_and_zeros(dtype):
     assert (idx[::3, 0] == 0).all() and (idx[::3, 1] == 1).all()   # all-tied rows
 
 
+@pytest.mark.parametrize("T,d,N,k,cf", [
+    (1, 64, 1, 1, 1.0), (300, 384, 8, 1, 1.0), (129, 320, 5, 2, 1.0), (2000, 4096, 16, 2, 1.0),
+    (5000, 3072, 12, 1, 1.25), (64, 64, 16, 4, 0.5), (40000, 256, 8, 2, 1.0),
+    (300, 200, 8, 1, 1.0), (129, 72, 5, 2, 1.0)])
+def test_gate_tensor_core_path(T, d, N, k, cf):
+    """bf16 tokens, N <= 16, d % 64 == 0: the persistent tensor-core gate
+    (mma.sync on a 3-part bf16 weight split, bulk-copied row stages): one and
+    several stages per tile, partial last stage (d=384, 320), partial last
+    tile, more tiles than SMs (T=40000).  d % 64 != 0 takes the FMA kernel."""
+    _gate_case(T, d, N, k, cf, torch.bfloat16, seed=T + d + N)
+
+
+def test_gate_tensor_core_matches_fma_path():
+    """Same decisions from both logit kernels wherever their fp32 logits agree;
+    logits within a few fp32 ulps of each other."""
+    import ctypes
+    from paper_2404_05019_b200 import _lib
+    flag = ctypes.c_int.in_dll(_lib.lib(), "scmoe_gate_force_fma")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(16384, 2048, device="cuda", generator=g).bfloat16()
+    w = torch.randn(8, 2048, device="cuda", generator=g) / 2048 ** 0.5
+    quota = K.expert_quota(2.0, 16384, 1, 8)
+    try:
+        flag.value = 1
+        a = K.gate_topk(x, w, 1, quota)
+        flag.value = 0
+        b = K.gate_topk(x, w, 1, quota)
+    finally:
+        flag.value = 0
+    torch.cuda.synchronize()
+    torch.testing.assert_close(a.logits, b.logits, rtol=1e-4, atol=1e-4)
+    same = (a.indices == b.indices).float().mean().item()
+    assert same > 0.999
+
+
 def test_gate_noise():
     _gate_case(1500, 128, 8, 2, 1.0, torch.float32, seed=9, noise=True)
 
