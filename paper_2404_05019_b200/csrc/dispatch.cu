@@ -16,7 +16,7 @@ namespace {
 
 constexpr int WARPS = 8;
 
-template <typename T>
+template <typename T, int KMAX>
 __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
     const T* __restrict__ x, long long ld_x, int n_tok, int d, int k,
     const int32_t* __restrict__ indices, const int32_t* __restrict__ slots, int cap,
@@ -25,35 +25,42 @@ __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
   const int lane = threadIdx.x & 31;
   const long long t = (long long)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (t >= n_tok) return;
-  long long dst[SCMOE_MAX_K];
-  float scl[SCMOE_MAX_K];
-  int nd = 0;
+  // per-selection destinations in registers (KMAX-unrolled; a dropped
+  // selection keeps dst = -1)
+  long long dst[KMAX];
+  float scl[KMAX];
+  bool any = false;
 #pragma unroll
-  for (int j = 0; j < SCMOE_MAX_K; ++j) {
+  for (int j = 0; j < KMAX; ++j) {
+    dst[j] = -1;
+    scl[j] = 1.f;
     if (j < k) {
       const int s = slots[t * k + j];
       if (s < cap) {
-        dst[nd] = ((long long)indices[t * k + j] * cap + s) * d;
-        scl[nd] = row_scale ? row_scale[t * k + j] : 1.f;
-        ++nd;
+        dst[j] = ((long long)indices[t * k + j] * cap + s) * d;
+        if (row_scale) scl[j] = row_scale[t * k + j];
+        any = true;
       }
     }
   }
-  if (nd == 0) return;
+  if (!any) return;
   const T* src = x + t * ld_x;
-  // 4 x 16B loads in flight per lane before the stores
-  for (int c = lane * VEC; c < d; c += 32 * VEC * 4) {
-    uint4 v[4];
+  // U x 16B loads in flight per lane before the stores
+  constexpr int U = 8;
+  for (int c = lane * VEC; c < d; c += 32 * VEC * U) {
+    uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int cc = c + u * 32 * VEC;
       if (cc < d) v[u] = ld_nc_v4(src + cc);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int cc = c + u * 32 * VEC;
       if (cc < d) {
-        for (int q = 0; q < nd; ++q) {
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+          if (dst[q] < 0) continue;
           if (row_scale) {
             // combine backward: d expert_out[e, slot] = w * d_out[t]
             Vec16<T> iv, ov;
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
   }
 }
 
-template <typename T, int MODE, bool HAS_SE, bool HAS_RES>
+template <typename T, int MODE, bool HAS_SE, bool HAS_RES, int KMAX>
 __global__ void __launch_bounds__(WARPS * 32) combine_kernel(
     const T* __restrict__ se, const T* __restrict__ y, const T* __restrict__ xcur,
     const float* __restrict__ wcg, const T* __restrict__ res,
@@ -112,27 +119,47 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(
     }
   }
 
-  long long src[SCMOE_MAX_K];
-  float wt[SCMOE_MAX_K];
-  int ns = 0;
+  // kept selections in registers (KMAX-unrolled; dropped -> src = -1)
+  long long src[KMAX];
+  float wt[KMAX];
 #pragma unroll
-  for (int j = 0; j < SCMOE_MAX_K; ++j) {
+  for (int j = 0; j < KMAX; ++j) {
+    src[j] = -1;
+    wt[j] = 0.f;
     if (j < k) {
       const int s = slots[t * k + j];
       if (s < cap) {
-        src[ns] = ((long long)indices[t * k + j] * cap + s) * d;
-        wt[ns] = weights[t * k + j];
-        ++ns;
+        src[j] = ((long long)indices[t * k + j] * cap + s) * d;
+        wt[j] = weights[t * k + j];
       }
     }
   }
-  for (int c = lane * VEC; c < d; c += 32 * VEC) {
+  // two column chunks per lane at a time: every row's loads of both chunks
+  // are issued before any math
+  constexpr int U = 2;
+  for (int c0 = lane * VEC; c0 < d; c0 += 32 * VEC * U) {
+    uint4 yv[U][KMAX], sev[U], rsv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 32 * VEC;
+      const bool in = c < d;
+#pragma unroll
+      for (int q = 0; q < KMAX; ++q)
+        yv[u][q] = (in && src[q] >= 0) ? ld_nc_v4(y + src[q] + c) : make_uint4(0, 0, 0, 0);
+      if (HAS_SE) sev[u] = in ? ld_nc_v4(se + t * d + c) : make_uint4(0, 0, 0, 0);
+      if (HAS_RES) rsv[u] = in ? ld_nc_v4(res + t * d + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int c = c0 + u * 32 * VEC;
+    if (c >= d) break;
     float r[VEC];
 #pragma unroll
     for (int i = 0; i < VEC; ++i) r[i] = 0.f;
-    for (int q = 0; q < ns; ++q) {
+#pragma unroll
+    for (int q = 0; q < KMAX; ++q) {
       Vec16<T> v;
-      v.raw = ld_nc_v4(y + src[q] + c);
+      v.raw = yv[u][q];
       float f[VEC];
       v.to_float(f);
 #pragma unroll
@@ -141,7 +168,7 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(
     float o[VEC];
     if (HAS_SE) {
       Vec16<T> v;
-      v.raw = ld_nc_v4(se + t * d + c);
+      v.raw = sev[u];
       float f[VEC];
       v.to_float(f);
 #pragma unroll
@@ -152,7 +179,7 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(
     }
     if (HAS_RES) {
       Vec16<T> v;
-      v.raw = ld_nc_v4(res + t * d + c);
+      v.raw = rsv[u];
       float f[VEC];
       v.to_float(f);
 #pragma unroll
@@ -161,22 +188,35 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(
     Vec16<T> ov;
     ov.from_float(o);
     st_v4(out + t * d + c, ov.raw);
+    }
   }
+}
+
+template <typename T, int MODE, int KMAX>
+void launch_combine_k(const T* se, const T* y, const T* xc, const float* wcg, const T* res,
+                      const int32_t* idx, const int32_t* sl, const float* w, int cap, int n, int d,
+                      int k, T* out, cudaStream_t st) {
+  const int grid = (n + WARPS - 1) / WARPS;
+  if (se && res)
+    combine_kernel<T, MODE, true, true, KMAX><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
+  else if (se)
+    combine_kernel<T, MODE, true, false, KMAX><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
+  else if (res)
+    combine_kernel<T, MODE, false, true, KMAX><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
+  else
+    combine_kernel<T, MODE, false, false, KMAX><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
 }
 
 template <typename T, int MODE>
 void launch_combine_mode(const T* se, const T* y, const T* xc, const float* wcg, const T* res,
                          const int32_t* idx, const int32_t* sl, const float* w, int cap, int n,
                          int d, int k, T* out, cudaStream_t st) {
-  const int grid = (n + WARPS - 1) / WARPS;
-  if (se && res)
-    combine_kernel<T, MODE, true, true><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
-  else if (se)
-    combine_kernel<T, MODE, true, false><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
-  else if (res)
-    combine_kernel<T, MODE, false, true><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
+  if (k == 1)
+    launch_combine_k<T, MODE, 1>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out, st);
+  else if (k == 2)
+    launch_combine_k<T, MODE, 2>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out, st);
   else
-    combine_kernel<T, MODE, false, false><<<grid, WARPS * 32, 0, st>>>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out);
+    launch_combine_k<T, MODE, SCMOE_MAX_K>(se, y, xc, wcg, res, idx, sl, w, cap, n, d, k, out, st);
 }
 
 template <typename T>
@@ -211,14 +251,20 @@ extern "C" int scmoe_dispatch_scaled(const void* x, int dtype, long long ld_x, i
   if (n_tokens <= 0) return SCMOE_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (n_tokens + WARPS - 1) / WARPS;
-  if (dtype == SCMOE_BF16)
-    dispatch_kernel<__nv_bfloat16><<<grid, WARPS * 32, 0, st>>>(
-        (const __nv_bfloat16*)x, ld_x, n_tokens, d_model, k, indices, slots, capacity, row_scale,
-        (__nv_bfloat16*)dispatch_buf);
-  else
-    dispatch_kernel<float><<<grid, WARPS * 32, 0, st>>>((const float*)x, ld_x, n_tokens, d_model, k,
-                                                        indices, slots, capacity, row_scale,
-                                                        (float*)dispatch_buf);
+#define SCMOE_DISPATCH(T, KM)                                                                  \
+  dispatch_kernel<T, KM><<<grid, WARPS * 32, 0, st>>>((const T*)x, ld_x, n_tokens, d_model, k,    \
+                                                      indices, slots, capacity, row_scale,      \
+                                                      (T*)dispatch_buf)
+  if (dtype == SCMOE_BF16) {
+    if (k == 1) SCMOE_DISPATCH(__nv_bfloat16, 1);
+    else if (k == 2) SCMOE_DISPATCH(__nv_bfloat16, 2);
+    else SCMOE_DISPATCH(__nv_bfloat16, SCMOE_MAX_K);
+  } else {
+    if (k == 1) SCMOE_DISPATCH(float, 1);
+    else if (k == 2) SCMOE_DISPATCH(float, 2);
+    else SCMOE_DISPATCH(float, SCMOE_MAX_K);
+  }
+#undef SCMOE_DISPATCH
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }
