@@ -213,6 +213,56 @@ int scmoe_combine(const void* se_out, const void* expert_out, const void* x_cur,
                   int capacity, int n_tokens, int d_model, int k, int dtype,
                   void* out, void* stream);
 
+/*
+ * K9 / K10 — expert parallelism over NVLink / NVSwitch peer memory (SURVEY
+ * §8(e); replaces the two all-to-alls around the routed experts).  Global
+ * expert e = r * experts_per_rank + el lives on rank r.  Every rank owns, in
+ * memory every peer can address (symmetric memory), a receive buffer
+ * recv (world, E_l, C, d), an output buffer y (same layout), recv_counts
+ * (world * E_l) int32 and flags (2 * world) uint32; epoch_ctr (2) uint32 is
+ * local, zero-initialised.  The peer tables are DEVICE arrays of `world`
+ * pointers (entry r = rank r's buffer).
+ *
+ * scmoe_ep_dispatch_p2p: every kept selection (t, j) of this rank's tokens is
+ *   stored straight into recv_r[(rank*E_l + el)*C + slot] on its owner r (only
+ *   kept rows move); recv_counts_r[rank*E_l + el] = min(counts[e], C); then the
+ *   epoch flag flags_r[0][rank] is released on every peer.  counts = pre-drop
+ *   per global expert (the gate's counts).  max_ctas > 0 bounds the grid so
+ *   the copy can run beside compute on a side stream.
+ * scmoe_ep_wait(which): spin until flags[which][s] >= this rank's epoch for
+ *   every s (which 0: all dispatches into my recv landed; 1: every owner's y
+ *   is ready).  Traps after ~20 s instead of hanging.
+ * scmoe_ep_signal(which): release flags_r[which][rank] = epoch on every peer
+ *   (which 1 after the grouped FFN wrote y).
+ * scmoe_ep_combine_p2p: scmoe_combine with each expert row read from
+ *   y_r[(rank*E_l + el)*C + slot] on its owner r (return trip fused into the
+ *   combine's loads).
+ * scmoe_ep_return_p2p: return trip as a push (side stream, overlaps the window
+ *   ops after the expert): rows < recv_counts[g] of y group g = (src, el) are
+ *   stored into back_src[(rank*E_l + el)*C + row], then flags_src[1][rank] is
+ *   released; the source waits (which 1) and runs scmoe_combine on back.
+ *   epoch_ctr needs 3 words for this entry.
+ */
+int scmoe_ep_dispatch_p2p(const void* x, int dtype, long long ld_x, int n_tokens, int d_model,
+                          int k, const int32_t* indices, const int32_t* slots,
+                          const int32_t* counts, int capacity, int world, int rank,
+                          int experts_per_rank, void* const* peer_recv,
+                          int32_t* const* peer_recv_counts, uint32_t* const* peer_flags,
+                          uint32_t* epoch_ctr, int max_ctas, void* stream);
+int scmoe_ep_wait(const uint32_t* flags, int which, int world, const uint32_t* epoch_ctr,
+                  void* stream);
+int scmoe_ep_signal(uint32_t* const* peer_flags, int which, int world, int rank,
+                    const uint32_t* epoch_ctr, void* stream);
+int scmoe_ep_combine_p2p(const void* se_out, const void* const* peer_y, const void* x_cur,
+                         const float* w_cg, int mode, const void* residual,
+                         const int32_t* indices, const int32_t* slots, const float* weights,
+                         int capacity, int n_tokens, int d_model, int k, int dtype, int world,
+                         int rank, int experts_per_rank, void* out, void* stream);
+int scmoe_ep_return_p2p(const void* y, int dtype, const int32_t* recv_counts, int capacity,
+                        int d_model, int world, int rank, int experts_per_rank,
+                        void* const* peer_back, uint32_t* const* peer_flags, uint32_t* epoch_ctr,
+                        int max_ctas, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

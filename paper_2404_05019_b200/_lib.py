@@ -51,6 +51,13 @@ SIGNATURES = [
                               _i, _i, _vp]),
     ("scmoe_combine", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                            _vp, _vp]),
+    ("scmoe_ep_dispatch_p2p", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _vp, _i, _i, _i, _i,
+                                   _vp, _vp, _vp, _vp, _i, _vp]),
+    ("scmoe_ep_wait", _i, [_vp, _i, _i, _vp, _vp]),
+    ("scmoe_ep_signal", _i, [_vp, _i, _i, _i, _vp, _vp]),
+    ("scmoe_ep_combine_p2p", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
+                                  _i, _i, _i, _vp, _vp]),
+    ("scmoe_ep_return_p2p", _i, [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
 ]
 
 _lib = None

@@ -1,0 +1,184 @@
+"""Expert parallelism over NVLink / NVSwitch peer memory (the fused path).
+
+The NCCL path in ep.py moves the whole capacity-padded (G, E_l, C, d)
+dispatch buffer with an equal-split all-to-all, then moves the expert outputs
+back the same way.  Here the kernels do the transfers themselves
+(csrc/dispatch.cu, K9/K10):
+
+    gate (compute) --> scmoe_ep_dispatch_p2p (side stream, bounded grid):
+                       kept rows stored into recv on their owner rank,
+                       counts published, epoch flag released on every peer
+    owner: scmoe_ep_wait(0) -> grouped FFN recv -> y -> scmoe_ep_signal(1)
+    source: scmoe_ep_wait(1) -> scmoe_ep_combine_p2p: expert rows read from
+            y on their owner, fused with SE, combination gate and residual
+
+Only kept rows cross NVLink (no padding, no staging copy), the dispatch copy
+runs beside the window ops on a side stream, and the return trip is folded
+into the combine kernel's loads.  Ordering is carried by per-rank epoch
+counters in device memory, so a captured CUDA graph replays correctly.
+
+`PeerExchange.from_group` builds the symmetric buffers with
+torch.distributed._symmetric_memory (allocation + rendezvous only — every
+byte is moved by our kernels).  `PeerExchange.virtual` lays out G ranks'
+buffers on ONE GPU with the same pointer tables, so the exchange logic is
+tested bit-for-bit on a single B200.
+
+Buffer reuse across calls is safe by construction: a source's next dispatch
+is issued after its combine, which waited for every owner's y-ready flag of
+the previous call (so the owners are done reading recv); an owner's next FFN
+waits for every source's next dispatch, issued after that source's combine
+finished reading y.
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional
+
+import torch
+
+from . import _lib
+from ._lib import check, dtype_code, lib, ptr, stream_ptr
+
+
+class PeerExchange:
+    """Receive / output buffers, counts, flags and peer tables of one rank."""
+
+    def __init__(self, world: int, rank: int, e_local: int, capacity: int, d_model: int,
+                 dtype: torch.dtype, device, storage: Optional[torch.Tensor] = None):
+        self.world, self.rank, self.e_local = world, rank, e_local
+        self.capacity, self.d_model, self.dtype = capacity, d_model, dtype
+        dev = torch.device(device)
+        G = world * e_local
+        self._sizes, self._offs, off = self.layout(world, e_local, capacity, d_model, dtype)
+        self.nbytes = off
+        if storage is None:
+            storage = torch.zeros(off, dtype=torch.uint8, device=dev)
+        if storage.numel() < off:
+            raise ValueError("peer storage too small")
+        self.storage = storage
+        b = storage
+        def part(i):
+            return b[self._offs[i]:self._offs[i] + self._sizes[i]]
+        self.recv = part(0).view(dtype).view(G, capacity, d_model)
+        self.y = part(1).view(dtype).view(G, capacity, d_model)
+        self.back = part(2).view(dtype).view(G, capacity, d_model)
+        self.recv_counts = part(3).view(torch.int32)
+        self.flags = part(4).view(torch.int32)
+        self.epoch = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.tables = None
+
+    @staticmethod
+    def layout(world, e_local, capacity, d_model, dtype):
+        """(sizes, offsets, total bytes) of [recv | y | back | recv_counts |
+        flags], each 256-byte aligned."""
+        G = world * e_local
+        esz = torch.tensor([], dtype=dtype).element_size()
+        rows = G * capacity * d_model
+        sizes = [rows * esz, rows * esz, rows * esz, G * 4, 2 * world * 4]
+        offs, off = [], 0
+        for n in sizes:
+            offs.append(off)
+            off += (n + 255) // 256 * 256
+        return sizes, offs, off
+
+    # -- peer tables -------------------------------------------------------------
+    def set_peer_bases(self, bases: List[int]) -> "PeerExchange":
+        """bases[r] = address of rank r's storage as mapped in THIS process."""
+        if len(bases) != self.world:
+            raise ValueError("one base per rank")
+        dev = self.storage.device
+        tab = torch.tensor([[b + o for b in bases] for o in self._offs],
+                           dtype=torch.int64, device=dev)
+        self.tables = tab     # rows: recv, y, back, recv_counts, flags
+        return self
+
+    def _tab(self, i: int) -> int:
+        return self.tables[i].data_ptr()
+
+    @classmethod
+    def virtual(cls, world: int, e_local: int, capacity: int, d_model: int, dtype, device):
+        """`world` ranks on one GPU: separate storages, peer tables pointing at
+        each other's storage — the same addressing the NVLink path uses."""
+        xs = [cls(world, r, e_local, capacity, d_model, dtype, device) for r in range(world)]
+        bases = [x.storage.data_ptr() for x in xs]
+        for x in xs:
+            x.set_peer_bases(bases)
+        return xs
+
+    @classmethod
+    def from_group(cls, group, e_local: int, capacity: int, d_model: int, dtype, device):
+        """Symmetric storage over a process group (torch symmetric memory:
+        allocation and handle exchange only)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        nbytes = cls.layout(world, e_local, capacity, d_model, dtype)[2]
+        name = group.group_name if hasattr(group, "group_name") else group
+        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        buf.zero_()
+        hdl = symm_mem.rendezvous(buf, name)
+        own = buf.data_ptr() - hdl.buffer_ptrs[rank]
+        bases = [p + own for p in hdl.buffer_ptrs]
+        x = cls(world, rank, e_local, capacity, d_model, dtype, device, storage=buf)
+        x._handle = hdl
+        hdl.barrier()
+        return x.set_peer_bases(bases)
+
+    # -- the exchange ------------------------------------------------------------
+    def dispatch(self, x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor,
+                 counts: torch.Tensor, max_ctas: int = 0, stream=None) -> None:
+        T, d = x.shape
+        k = indices.shape[1]
+        check(lib().scmoe_ep_dispatch_p2p(
+            ptr(x), dtype_code(x.dtype), x.stride(0), T, d, k, ptr(indices), ptr(slots),
+            ptr(counts), self.capacity, self.world, self.rank, self.e_local, self._tab(0),
+            self._tab(3), self._tab(4), ptr(self.epoch), max_ctas, stream_ptr(stream)))
+
+    def wait(self, which: int, stream=None) -> None:
+        check(lib().scmoe_ep_wait(ptr(self.flags), which, self.world, ptr(self.epoch),
+                                  stream_ptr(stream)))
+
+    def signal(self, which: int, stream=None) -> None:
+        check(lib().scmoe_ep_signal(self._tab(4), which, self.world, self.rank, ptr(self.epoch),
+                                    stream_ptr(stream)))
+
+    def expert_ffn(self, experts, signal: bool = True, stream=None) -> torch.Tensor:
+        """Owner side: wait for every source's rows, grouped FFN recv -> y
+        (groups (src, el) -> local expert el); with `signal`, release y-ready
+        for the pull-form combine."""
+        self.wait(0, stream)
+        experts(self.recv, self.recv_counts, self.capacity, out=self.y, stream=stream)
+        if signal:
+            self.signal(1, stream)
+        return self.y
+
+    def push_back(self, max_ctas: int = 0, stream=None) -> None:
+        """Owner side, push form of the return trip: valid rows of y into every
+        source's `back` buffer, then release flag 1 on the sources."""
+        check(lib().scmoe_ep_return_p2p(
+            ptr(self.y), dtype_code(self.dtype), ptr(self.recv_counts), self.capacity,
+            self.d_model, self.world, self.rank, self.e_local, self._tab(2), self._tab(4),
+            ptr(self.epoch), max_ctas, stream_ptr(stream)))
+
+    def combine_local(self, indices, slots, weights, **kw) -> torch.Tensor:
+        """Source side after push_back: wait for every owner's rows, then the
+        ordinary combine over `back` ((E, C, d), global expert order)."""
+        from . import kernels as K
+        stream = kw.pop("stream", None)
+        self.wait(1, stream)
+        return K.combine(self.back.view(-1, self.capacity, self.d_model), indices, slots, weights,
+                         self.capacity, stream=stream, **kw)
+
+    def combine(self, indices, slots, weights, se_out=None, mode: str = "direct_add",
+                x_cur=None, w_cg=None, residual=None, out=None, stream=None) -> torch.Tensor:
+        """Source side: wait for every owner's y, then the fused gather-sum."""
+        self.wait(1, stream)
+        T, k = indices.shape
+        if out is None:
+            out = torch.empty(T, self.d_model, dtype=self.dtype, device=indices.device)
+        check(lib().scmoe_ep_combine_p2p(
+            ptr(se_out), self._tab(1), ptr(x_cur), ptr(w_cg), _lib.COMBINE_MODES[mode],
+            ptr(residual), ptr(indices), ptr(slots), ptr(weights), self.capacity, T,
+            self.d_model, k, dtype_code(self.dtype), self.world, self.rank, self.e_local,
+            ptr(out), stream_ptr(stream)))
+        return out
