@@ -10,7 +10,9 @@ Workload (N=1 line, BASELINE.json configs[2]): GPT3-MoE-XL-shaped block pair
 N(0,1) tokens and random-init weights (no checkpoints offline).  The same-box
 top-2 MoE block pair (same shapes, same kernels) is timed in the same run for
 the speed-up.  Under torchrun (N>1) experts are sharded 8/N per rank (expert
-parallelism, NCCL all-to-all on a side stream), T per GPU fixed (weak scaling).
+parallelism; by default the exchange is our peer-memory dispatch / return kernels
+on a side stream, `--ep-backend nccl` uses NCCL all-to-all), T per GPU fixed
+(weak scaling).
 
 A "step" is one block-pair forward over the GPU's T tokens.  `value` is
 device-timed with inputs resident in HBM; `e2e` runs the same public
@@ -64,6 +66,29 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# stdout carries the single JSON line only: native libraries (NCCL's version
+# banner, symmetric-memory setup) write to fd 1 directly, so fd 1 is pointed at
+# stderr for the whole run and the JSON line goes to the saved original stdout
+_JSON_FD = None
+
+
+def _claim_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 # ---------------------------------------------------------------------------
 # distributed plumbing
 
@@ -75,6 +100,14 @@ def dist_setup(force_dist: bool = False):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1 or force_dist:
+        if ws == 1:      # one-rank group without torchrun
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            for k_, v_ in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"),
+                           ("MASTER_PORT", str(port))):
+                os.environ.setdefault(k_, v_)
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -207,7 +240,7 @@ def run_reference(args):
                          "blas": blas},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -215,12 +248,12 @@ def run_reference(args):
 # our arm
 
 
-def build_blocks(w, ws, rank, dtype, group):
+def build_blocks(w, ws, rank, dtype, group, ep_backend="nccl"):
     import torch
     import paper_2404_05019_b200 as P
     n_exp = w["n_experts"] or max(ws, 1)
     common = dict(n_heads=w["heads"], seq_len=w["seq"], causal=w["causal"], dtype=dtype,
-                  capacity_factor=w["cf"], ep_group=group)
+                  capacity_factor=w["cf"], ep_group=group, ep_backend=ep_backend)
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     sc = P.ScMoEBlockPair(w["d"], w["h"], n_exp, variant="scmoe", shortcut_pos=w["pos"],
                           combine_mode=w["combine"], generator=gen, **common)
@@ -395,7 +428,7 @@ def run_ours(args):
         group = dist.group.WORLD
     T = w["seq"] * w["seqs"]
     d, h = w["d"], w["h"]
-    sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group)
+    sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend)
     gen = torch.Generator(device="cuda").manual_seed(99 + rank)
     x = torch.randn(T, d, device="cuda", generator=gen).to(dtype)
 
@@ -418,7 +451,8 @@ def run_ours(args):
         # the same steps captured once into CUDA graphs and replayed (one
         # launch per step; single GPU — NCCL runs stay eager)
         from paper_2404_05019_b200.runtime import CapturedStep, HostStreamRunner
-        use_graphs = group is None and not args.no_graphs
+        # the p2p exchange is graph-safe (device-side epochs); NCCL runs eager
+        use_graphs = (group is None or args.ep_backend == "p2p") and not args.no_graphs
 
         def fwd(blk):
             return lambda xx: blk(xx)[0]
@@ -520,6 +554,7 @@ def run_ours(args):
                    "experts_per_gpu": n_exp // ws, "heads": w["heads"], "seq_len": w["seq"],
                    "tokens_per_gpu": T, "capacity_factor": w["cf"], "shortcut_pos": w["pos"],
                    "combine": w["combine"], "parallelism": f"ep{ws}" if ws > 1 else "single",
+                   "ep_backend": args.ep_backend if group is not None else None,
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
         "speedup_vs_top2": med["t2"] / med["sc"],
         "ab": {"rounds": args.ab_rounds, "steps_per_round": max(3, args.steps // 2),
@@ -562,7 +597,7 @@ def run_ours(args):
                                 "sample": f"{args.cpu_tokens} tokens x {args.cpu_reps} reps, dense "
                                           f"fp64 oracle of the same block pair", "blas": blas}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     import torch.distributed as dist
     if dist.is_initialized():
         dist.destroy_process_group()
@@ -583,11 +618,14 @@ def main():
                     help="expert-parallel code path even on one rank (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ab-rounds", type=int, default=5)
+    ap.add_argument("--ep-backend", choices=("p2p", "nccl"), default="p2p",
+                    help="expert-parallel exchange: our peer-memory kernels or NCCL all-to-all")
     ap.add_argument("--no-hbm-ops", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=128)
     args = ap.parse_args()
+    _claim_stdout()
     if args.warmup < 3 and args.impl == "ours":
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3

@@ -108,11 +108,18 @@ class ScMoEBlockPair(nn.Module):
                  noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
                  seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
                  device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True,
-                 chunks: int = 1):
+                 chunks: int = 1, ep_backend: str = "nccl", p2p_ctas: int = 32):
         super().__init__()
         if chunks < 1:
             raise ConfigError("chunks must be >= 1")
+        if ep_backend not in ("nccl", "p2p"):
+            raise ConfigError(f"unknown ep_backend {ep_backend!r}")
         self.chunks = chunks
+        # "nccl": all-to-all of the capacity buffers (ep.py); "p2p": our kernels
+        # move only kept rows over peer memory (ep_p2p.py); p2p_ctas bounds the
+        # side-stream copy kernels' grids so they run beside the window ops
+        self.ep_backend, self.p2p_ctas = ep_backend, p2p_ctas
+        self._xchg = None
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
         if variant == "scmoe" and shortcut_pos not in POSITIONS:
@@ -186,6 +193,18 @@ class ScMoEBlockPair(nn.Module):
     def _feed(self, h):
         return layer_norm(h) if self.pre_layernorm else h
 
+    def peer_exchange(self, capacity: int):
+        """Symmetric buffers for the p2p backend (re-created if the capacity,
+        i.e. the per-rank token count, changes)."""
+        from .ep_p2p import PeerExchange
+        x = self._xchg
+        if x is None or x.capacity != capacity:
+            moe = self.moe
+            self._xchg = PeerExchange.from_group(self.ep_group, moe.experts.n_experts, capacity,
+                                                 moe.d_model, moe.dtype,
+                                                 moe.gate.w_gate_t.device)
+        return self._xchg
+
     def comm_stream(self) -> torch.cuda.Stream:
         if self._comm_stream is None:
             self._comm_stream = torch.cuda.Stream(priority=-1)
@@ -249,6 +268,9 @@ class ScMoEBlockPair(nn.Module):
         off = self.offload if not train else None
         if off is not None and (use_ep or chunks > 1):
             raise NotImplementedError("expert offload is a single-GPU, unchunked inference mode")
+        p2p = use_ep and self.ep_backend == "p2p" and not train
+        if p2p and chunks > 1:
+            raise NotImplementedError("chunked pipelining runs on the nccl backend")
 
         def gate():
             if train:
@@ -340,6 +362,18 @@ class ScMoEBlockPair(nn.Module):
                     env["recv_counts"] = ep_mod.exchange_counts(env["kept"], self.ep_group)
                     env["buf"] = TR.ExchangeFn.apply(buf, self.ep_group)
                 return
+            if p2p:
+                # kept rows go straight to their owners over peer memory, on the
+                # side stream beside the window ops (bounded grid)
+                xg = self.peer_exchange(dec.capacity)
+                cs.wait_stream(st)
+                with rec.op("dispatch", "comm", cs):
+                    xg.dispatch(src(), dec.indices, dec.slots, dec.counts, max_ctas=self.p2p_ctas,
+                                stream=cs)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                env["disp_ev"] = ev
+                return
             buf = K.dispatch(src(), dec.indices, dec.slots, moe.n_experts, dec.capacity)
             env["buf"] = buf
             if use_ep:
@@ -359,6 +393,17 @@ class ScMoEBlockPair(nn.Module):
                 rows = env["recv_counts"] if use_ep else env["kept"]
                 y = TR.FFNFn.apply(env["buf"], e.w1t, e.b1, e.w2t, e.b2, None, rows, dec.capacity)
                 env["y"] = TR.ExchangeFn.apply(y, self.ep_group) if use_ep else y
+                return
+            if p2p:
+                xg = self._xchg
+                st.wait_event(env["disp_ev"])
+                xg.expert_ffn(moe.experts, signal=False, stream=st)
+                cs.wait_stream(st)
+                with rec.op("combine", "comm", cs):
+                    xg.push_back(max_ctas=self.p2p_ctas, stream=cs)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                env["y_ev"] = ev
                 return
             if use_ep:
                 p = env["pending"]
@@ -387,6 +432,14 @@ class ScMoEBlockPair(nn.Module):
                 return
             if use_ep:
                 st.wait_event(env["y_ev"])
+            if p2p:
+                xg = self._xchg
+                kw = dict(residual=env["h_mh_cur"], stream=st)
+                if self.variant != "standard":
+                    kw.update(se_out=env["se"], mode=moe.combine_mode, x_cur=env["x_cur"],
+                              w_cg=moe.w_cg)
+                env["out"] = xg.combine_local(dec.indices, dec.slots, dec.weights, **kw)
+                return
             cidx = env["plan"].slot_idx if off is not None else dec.indices
             if self.variant == "standard":
                 env["out"] = K.combine(env["y"], cidx, dec.slots, dec.weights, dec.capacity,

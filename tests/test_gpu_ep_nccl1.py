@@ -77,3 +77,31 @@ def test_ep_calibrate_and_train_step():
     l0 = float(blk.train_step(x, lr=1e-3))
     l1 = float(blk.train_step(x, lr=1e-3))
     assert l1 < l0
+
+
+@pytest.mark.parametrize("variant,slot", [("scmoe", 0), ("scmoe", 2), ("standard", None)])
+def test_ep_p2p_backend_equals_local(variant, slot):
+    """ep_backend="p2p": dispatch and return trip are our peer-memory kernels
+    on the side stream (symmetric memory over the one-rank group); repeated
+    forwards reuse the buffers (epoch flags)."""
+    import torch.distributed as dist
+    from paper_2404_05019_b200.timeline import Recorder
+    T, d, h, N = 1024, 256, 512, 8
+    kw = dict(variant=variant, k_routed=1 if variant == "scmoe" else 2,
+              shortcut_pos="pos2" if variant == "scmoe" else None, n_heads=4, seq_len=256,
+              capacity_factor=1.25, dtype=torch.bfloat16)
+    loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2), **kw)
+    epb = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2),
+                           ep_group=dist.group.WORLD, ep_backend="p2p", **kw)
+    if slot is not None:
+        epb.slot = loc.slot = slot
+    for it in range(3):
+        x = torch.randn(T, d, device="cuda").bfloat16()
+        with torch.no_grad():
+            a, _, _ = loc(x)
+            rec = Recorder()
+            b, _, _ = epb(x, recorder=rec)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), it
+        comm = [s for s in rec.spans() if s.stream == "comm"]
+        assert len(comm) == 2
