@@ -17,9 +17,10 @@ runs beside the window ops on a side stream, and the return trip is folded
 into the combine kernel's loads.  Ordering is carried by per-rank epoch
 counters in device memory, so a captured CUDA graph replays correctly.
 
-`PeerExchange.from_group` builds the symmetric buffers with
-torch.distributed._symmetric_memory (allocation + rendezvous only — every
-byte is moved by our kernels).  `PeerExchange.virtual` lays out G ranks'
+`PeerExchange.from_group` maps every rank's buffers into every peer with
+CUDA IPC handles exchanged over the process group (or torch symmetric
+memory) — allocation and handle exchange only; every byte of the exchange is
+moved by our kernels.  `PeerExchange.virtual` lays out G ranks'
 buffers on ONE GPU with the same pointer tables, so the exchange logic is
 tested bit-for-bit on a single B200.
 
@@ -106,22 +107,49 @@ class PeerExchange:
         return xs
 
     @classmethod
-    def from_group(cls, group, e_local: int, capacity: int, d_model: int, dtype, device):
-        """Symmetric storage over a process group (torch symmetric memory:
-        allocation and handle exchange only)."""
+    def from_group(cls, group, e_local: int, capacity: int, d_model: int, dtype, device,
+                   method: str = "ipc"):
+        """Peer-mapped storage over a process group.  Allocation and handle
+        exchange only — every byte of the exchange is moved by our kernels.
+
+        method "ipc": each rank allocates its storage, the CUDA IPC handles
+        (torch's storage sharing: cudaIpcGetMemHandle / cudaIpcOpenMemHandle
+        with lazy peer access) travel through the group as objects, and every
+        rank maps every peer's storage.  Works across the GPUs of a node
+        (NVLink peer access) and across processes sharing one GPU.
+        method "symm": torch symmetric memory (one GPU per rank only)."""
         import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm_mem
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        nbytes = cls.layout(world, e_local, capacity, d_model, dtype)[2]
-        name = group.group_name if hasattr(group, "group_name") else group
-        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-        buf.zero_()
-        hdl = symm_mem.rendezvous(buf, name)
-        own = buf.data_ptr() - hdl.buffer_ptrs[rank]
-        bases = [p + own for p in hdl.buffer_ptrs]
-        x = cls(world, rank, e_local, capacity, d_model, dtype, device, storage=buf)
-        x._handle = hdl
-        hdl.barrier()
+        if method == "symm":
+            import torch.distributed._symmetric_memory as symm_mem
+            nbytes = cls.layout(world, e_local, capacity, d_model, dtype)[2]
+            name = group.group_name if hasattr(group, "group_name") else group
+            buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, name)
+            own = buf.data_ptr() - hdl.buffer_ptrs[rank]
+            bases = [p + own for p in hdl.buffer_ptrs]
+            x = cls(world, rank, e_local, capacity, d_model, dtype, device, storage=buf)
+            x._handle = hdl
+            hdl.barrier()
+            return x.set_peer_bases(bases)
+        if method != "ipc":
+            raise ValueError(f"unknown method {method!r}")
+        x = cls(world, rank, e_local, capacity, d_model, dtype, device)
+        torch.cuda.synchronize()             # storage zeroed before peers map it
+        meta = x.storage.untyped_storage()._share_cuda_()
+        metas = [None] * world
+        dist.all_gather_object(metas, meta, group=group)
+        x._peer_storages = []
+        bases = []
+        for r, m in enumerate(metas):
+            if r == rank:
+                bases.append(x.storage.data_ptr())
+            else:
+                st = torch.UntypedStorage._new_shared_cuda(*m)
+                x._peer_storages.append(st)
+                bases.append(st.data_ptr())
+        dist.barrier(group=group)            # every rank mapped every peer
         return x.set_peer_bases(bases)
 
     # -- the exchange ------------------------------------------------------------

@@ -1,0 +1,86 @@
+"""The peer-memory expert-parallel path across PROCESSES: two ranks (two
+processes) share the one B200 of the test box, their symmetric buffers are
+mapped into each other through CUDA IPC (torch symmetric memory over a gloo
+group — allocation and handle exchange only), and every byte of the exchange
+is moved by our kernels with system-scope fences and epoch flags, exactly as
+across NVLink.  Each rank's block-pair output must equal a single-process
+block holding all experts, on that rank's tokens, bit for bit (per-rank
+routing and quota, gating.py:134-135)."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, variant, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        import paper_2404_05019_b200 as P
+        T, d, h, N = 512, 256, 512, 4 * world
+        kw = dict(variant=variant, k_routed=1 if variant == "scmoe" else 2,
+                  shortcut_pos="pos2" if variant == "scmoe" else None, n_heads=4, seq_len=256,
+                  capacity_factor=1.25, dtype=torch.bfloat16)
+        loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(5),
+                               **kw)
+        epb = P.ScMoEBlockPair(d, h, N, ep_group=dist.group.WORLD, ep_backend="p2p", **kw)
+        e_l = N // world
+        with torch.no_grad():
+            src = dict(loc.named_parameters())
+            for name, p in epb.named_parameters():
+                full = src[name]
+                if name.startswith("moe.experts."):
+                    p.copy_(full[rank * e_l:(rank + 1) * e_l])
+                else:
+                    p.copy_(full)
+        for it in range(3):
+            g = torch.Generator(device="cuda").manual_seed(1000 * it + rank)
+            x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+            with torch.no_grad():
+                a, _, _ = loc(x)
+                b, _, _ = epb(x)
+            torch.cuda.synchronize()
+            if not torch.equal(a, b):
+                raise AssertionError(f"rank {rank} call {it}: max diff "
+                                     f"{(a.float() - b.float()).abs().max().item()}")
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("variant", ["scmoe", "standard"])
+def test_p2p_ep_two_processes(variant):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world, port = 2, _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, variant, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, msg = q.get(timeout=240)
+        res[r] = msg
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v == "ok" for v in res.values()), res
