@@ -56,7 +56,9 @@ struct Cfg {
   static constexpr int A_BYTES = CTA_M * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256 + (MAX_GROUPS + 1) * 4;
+  // + per-epilogue-warp bias slice (8 warps x 128 fp32), staged once per tile
+  static constexpr size_t MISC = 256 + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + MISC + 8 * 128 * 4;
 };
 
 // instruction descriptor: D fp32, A/B bf16, M = TILE_M, N = 256, operand majors
@@ -285,7 +287,7 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc,
 // or zeros for padding rows
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
                                                bool row_ok, bool pad_row, long long row_off,
-                                               int n, const float* brow) {
+                                               int n, const float* sb) {
   if (n >= p.N || !(row_ok || pad_row)) return;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -299,9 +301,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
       float v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
-      if (brow) {
-        const float4 b0 = *reinterpret_cast<const float4*>(brow + nn);
-        const float4 b1 = *reinterpret_cast<const float4*>(brow + nn + 4);
+      if (sb) {   // this chunk's bias, staged in shared memory (warp broadcast)
+        const float4 b0 = *reinterpret_cast<const float4*>(sb + u * 8);
+        const float4 b1 = *reinterpret_cast<const float4*>(sb + u * 8 + 4);
         v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
         v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
       }
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty_bar = bars + 2 * C::STAGES + ACC_STAGES;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 2 * ACC_STAGES);
   int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
+  float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -518,8 +521,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
       bool row_ok, pad_row = false;
       long long row_off;
@@ -535,6 +536,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         brow = p.bias ? p.bias + (long long)(tc.g % p.n_wgroups) * p.N : nullptr;
       }
       const bool empty = WGRAD && tc.kb_lo >= tc.kb_hi;   // no MMA ran: write zeros
+      // stage this warp's 128 bias columns before waiting for the accumulator
+      // (the loads overlap the MMAs; the chunk loop reads smem broadcasts)
+      float* sbw = s_bias + ew * 128;
+      if (!WGRAD && brow) {
+        const int nb = tc.n0 + half * 128 + 4 * lane;
+        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (nb + 3 < p.N) b = *reinterpret_cast<const float4*>(brow + nb);
+        else
+          for (int i = 0; i < 4 && nb + i < p.N; ++i) (&b.x)[i] = brow[nb + i];
+        __syncwarp();        // previous tile's reads of sbw are done
+        *reinterpret_cast<float4*>(sbw + 4 * lane) = b;
+        __syncwarp();
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
       // TMEM -> registers in 4 chunks of 32 columns, chunk c+1's tcgen05.ld in
       // flight while chunk c is processed
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
         const int n = tc.n0 + half * 128 + c * 32;
         if (WGRAD) epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
-        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow);
+        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr);
         if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == 2) {
           // the whole accumulator is in registers: hand TMEM back to the MMA warp
