@@ -55,7 +55,7 @@ WORKLOADS = {
     # BASELINE.json configs[3] (every-block placement, pos1), 16 experts
     "every_block": dict(name="every-block scmoe pos1 (configs[3])", d=4096, h=16384, n_experts=16,
                         heads=32, seq=2048, seqs=4, cf=2.0, pos="pos1", combine="direct_add",
-                        causal=True),
+                        causal=True, every_block=True),
 }
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -199,13 +199,24 @@ def cpu_reference_time(w, tokens: int, reps: int, warmup: int = 1):
     from oracle import scmoe_oracle as O
     rng = O.Rng(0)
     n_exp = w["n_experts"] or 8
-    pp = O.init_pair(w["d"], w["h"], n_exp, rng.spawn(0), variant="scmoe",
-                     combine_mode=w["combine"])
     x = rng.spawn(1).normal((tokens, w["d"]))
+    if w.get("every_block"):
+        # one every-block Transformer block (arch.py:632-663), ScMoE pos1
+        blocks = O.init_model(1, w["d"], w["h"], n_exp, rng.spawn(0), moe_frequency="every-block",
+                              variant="scmoe", combine_mode=w["combine"])
+
+        def run():
+            O.model_forward(blocks, x, "scmoe", "pos1", w["cf"], 1, moe_frequency="every-block")
+    else:
+        pp = O.init_pair(w["d"], w["h"], n_exp, rng.spawn(0), variant="scmoe",
+                         combine_mode=w["combine"])
+
+        def run():
+            O.block_pair_forward(pp, x, "scmoe", w["pos"], w["cf"], 1)
     times = []
     for i in range(warmup + reps):
         t0 = time.perf_counter()
-        O.block_pair_forward(pp, x, "scmoe", w["pos"], w["cf"], 1)
+        run()
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -254,12 +265,16 @@ def build_blocks(w, ws, rank, dtype, group, ep_backend="nccl"):
     n_exp = w["n_experts"] or max(ws, 1)
     common = dict(n_heads=w["heads"], seq_len=w["seq"], causal=w["causal"], dtype=dtype,
                   capacity_factor=w["cf"], ep_group=group, ep_backend=ep_backend)
+    # every-block placement (arch.py:632-663): one Transformer block whose
+    # feed is the MoE layer; otherwise the Block-MLP + Block-MoE pair
+    cls = P.ScMoEBlock if w.get("every_block") else P.ScMoEBlockPair
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    sc = P.ScMoEBlockPair(w["d"], w["h"], n_exp, variant="scmoe", shortcut_pos=w["pos"],
-                          combine_mode=w["combine"], generator=gen, **common)
-    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    t2 = P.ScMoEBlockPair(w["d"], w["h"], n_exp, variant="standard", k_routed=2, generator=gen,
-                          **common)
+    sc = cls(w["d"], w["h"], n_exp, variant="scmoe", shortcut_pos=w["pos"],
+             combine_mode=w["combine"], generator=gen, **common)
+    t2 = None
+    if n_exp >= 2:      # one expert in total (configs[1] shape at N=1) has no top-2
+        gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+        t2 = cls(w["d"], w["h"], n_exp, variant="standard", k_routed=2, generator=gen, **common)
     return sc, t2, n_exp
 
 
@@ -437,7 +452,8 @@ def run_ours(args):
         choice = sc.calibrate(x)
         for _ in range(args.warmup):
             sc(x)
-            t2(x)
+            if t2 is not None:
+                t2(x)
         torch.cuda.synchronize()
 
         # ---- ScMoE block pair, device-timed; clocks sampled over every
@@ -447,7 +463,7 @@ def run_ours(args):
         # the roofline kernel's launch time)
         ms_sc_eager, recs = timed(lambda r: sc(x, recorder=r), args.steps, ws,
                                   recorder_factory=lambda: Recorder())
-        ms_t2_eager, _ = timed(lambda r: t2(x), args.steps, ws)
+        ms_t2_eager = timed(lambda r: t2(x), args.steps, ws)[0] if t2 is not None else None
         # the same steps captured once into CUDA graphs and replayed (one
         # launch per step; single GPU — NCCL runs stay eager)
         from paper_2404_05019_b200.runtime import CapturedStep, HostStreamRunner
@@ -459,25 +475,28 @@ def run_ours(args):
 
         src = x.clone()
         if use_graphs:
-            g_sc, g_t2 = CapturedStep(fwd(sc), [x]), CapturedStep(fwd(t2), [x])
+            g_sc = CapturedStep(fwd(sc), [x])
             g_lsc = CapturedStep(lambda xx: sc.moe(xx, src)[0], [x])
-            g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
-            run = {"sc": lambda r: g_sc.replay(), "t2": lambda r: g_t2.replay(),
-                   "lsc": lambda r: g_lsc.replay(), "lt2": lambda r: g_lt2.replay()}
+            run = {"sc": lambda r: g_sc.replay(), "lsc": lambda r: g_lsc.replay()}
+            if t2 is not None:
+                g_t2 = CapturedStep(fwd(t2), [x])
+                g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
+                run.update(t2=lambda r: g_t2.replay(), lt2=lambda r: g_lt2.replay())
         else:
-            run = {"sc": lambda r: sc(x), "t2": lambda r: t2(x),
-                   "lsc": lambda r: sc.moe(x, src), "lt2": lambda r: t2.moe(x)}
+            run = {"sc": lambda r: sc(x), "lsc": lambda r: sc.moe(x, src)}
+            if t2 is not None:
+                run.update(t2=lambda r: t2(x), lt2=lambda r: t2.moe(x))
         # the headline: exactly K steps of the ScMoE block pair
         ms_sc, _ = timed(run["sc"], args.steps, ws)
         # ScMoE vs top-2 (block pair and layer only): interleaved rounds so
         # clock / power-cap drift hits both arms alike; medians over rounds
         rounds = {k: [] for k in run}
         for _ in range(args.ab_rounds):
-            for key in ("sc", "t2", "lsc", "lt2"):
+            for key in [k_ for k_ in ("sc", "t2", "lsc", "lt2") if k_ in run]:
                 rounds[key].append(timed(run[key], max(3, args.steps // 2), ws)[0])
         med = {k: statistics.median(v) for k, v in rounds.items()}
-        ms_t2 = med["t2"]
-        ms_layer_sc, ms_layer_t2 = med["lsc"], med["lt2"]
+        ms_t2 = med.get("t2")
+        ms_layer_sc, ms_layer_t2 = med["lsc"], med.get("lt2")
 
         # ---- end to end through the public API, host buffers -----------------
         # every step copies its input from pinned host memory and its output
@@ -544,7 +563,7 @@ def run_ours(args):
             traffic = None
 
     value = ws * T / (ms_sc * 1e-3)
-    t2_value = ws * T / (ms_t2 * 1e-3)
+    t2_value = ws * T / (ms_t2 * 1e-3) if ms_t2 else None
     line = {
         "metric": "ScMoE block tokens/s", "value": value, "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_sc,
@@ -556,7 +575,7 @@ def run_ours(args):
                    "combine": w["combine"], "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "ep_backend": args.ep_backend if group is not None else None,
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
-        "speedup_vs_top2": med["t2"] / med["sc"],
+        "speedup_vs_top2": med["t2"] / med["sc"] if "t2" in med else None,
         "ab": {"rounds": args.ab_rounds, "steps_per_round": max(3, args.steps // 2),
                "median_ms": med, "note": "ScMoE / top-2 block pair and layer-only, interleaved "
                                          "rounds, CUDA-graph replays"},
@@ -565,9 +584,9 @@ def run_ours(args):
                   "top2_ms_per_step": ms_t2_eager,
                   "note": "same steps without graph capture; op_ms / roofline / comm come "
                           "from these per-op CUDA events"},
-        "top2": {"value": t2_value, "unit": "tokens/s", "ms_per_step": ms_t2},
+        "top2": {"value": t2_value, "unit": "tokens/s", "ms_per_step": ms_t2} if ms_t2 else None,
         "layer_only": {"scmoe_ms": ms_layer_sc, "top2_ms": ms_layer_t2,
-                       "speedup": ms_layer_t2 / ms_layer_sc},
+                       "speedup": ms_layer_t2 / ms_layer_sc if ms_layer_t2 else None},
         "comm": {"overlap_fraction": overlap, "exposed_ms": exposed, "comm_ms": comm_ms,
                  "expert_slot": choice.slot, "schedule_costs_ms": json.loads(sc.last_costs.to_json())},
         "op_ms": op_ms,
@@ -590,7 +609,11 @@ def run_ours(args):
                        "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
                        "ms_per_step": e2e_ms, "api": "runtime.HostStreamRunner(ScMoEBlockPair)",
                        "copies": "pinned host, H2D/D2H overlapped with neighbouring steps"}
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    n_e = w["n_experts"] or 8
+    dense_gb = (n_e + 2) * 2 * w["d"] * w["h"] * 8 / 1e9
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and dense_gb > 8:
+        line["cpu_baseline"] = {"value": None, "skipped": f"dense fp64 weights {dense_gb:.0f} GB"}
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         times, cores, blas = cpu_reference_time(w, args.cpu_tokens, args.cpu_reps)
         v = args.cpu_tokens / (sum(times) / len(times))
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
