@@ -125,6 +125,91 @@ __global__ void __launch_bounds__(WARPS * 32) dispatch_kernel(
                          LocalRows<T>{buf, cap, d});
 }
 
+// ---- K2 via the TMA bulk-copy engine ------------------------------------------
+// The permutation is pure data movement of whole rows (d*s bytes, contiguous
+// at both ends), so the copy engine does it: one elected thread per CTA pulls
+// token rows into a shared-memory ring with cp.async.bulk (global -> shared,
+// mbarrier completion) and pushes each row to every kept (expert, slot) row
+// with cp.async.bulk (shared -> global, bulk groups).  No register staging;
+// CTA c streams a contiguous range of tokens.
+
+__device__ __forceinline__ uint32_t bk_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bk_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nBK_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra BK_WAIT_%=;\n}\n" ::"r"(bk_smem(bar)), "r"(parity) : "memory");
+}
+
+constexpr int BK_SLOTS = 8;      // rows in flight per CTA
+constexpr int BK_LAG = 4;        // store groups allowed in flight before a slot is reused
+
+template <int KMAX>
+__global__ void __launch_bounds__(32) dispatch_bulk_kernel(
+    const uint8_t* __restrict__ x, long long ld_bytes, int n_tok, int row_bytes, int k,
+    const int32_t* __restrict__ indices, const int32_t* __restrict__ slots, int cap,
+    uint8_t* __restrict__ buf) {
+  extern __shared__ __align__(128) uint8_t bk_ring[];
+  __shared__ __align__(8) uint64_t bars[BK_SLOTS];
+  if (threadIdx.x != 0) return;
+  const int per = (n_tok + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(n_tok, t0 + per);
+  if (t0 >= t1) return;
+  for (int i = 0; i < BK_SLOTS; ++i)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_smem(&bars[i])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto kept = [&](long long t) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < k) any |= slots[t * k + j] < cap;
+    return any;
+  };
+  auto load = [&](int t, int slot) {
+    if (!kept(t)) return;
+    uint64_t* bar = &bars[slot];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(bk_smem(bar)), "r"(row_bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(bk_smem(bk_ring + (size_t)slot * row_bytes)), "l"(x + (long long)t * ld_bytes),
+          "r"(row_bytes), "r"(bk_smem(bar))
+        : "memory");
+  };
+  const int n = t1 - t0;
+  uint32_t phase_bits = 0;                 // parity per slot
+  for (int i = 0; i < min(n, BK_SLOTS); ++i) load(t0 + i, i);
+  for (int i = 0; i < n; ++i) {
+    const int t = t0 + i, slot = i % BK_SLOTS;
+    if (kept(t)) {
+      bk_wait(&bars[slot], (phase_bits >> slot) & 1u);
+      phase_bits ^= 1u << slot;
+      const uint8_t* row = bk_ring + (size_t)slot * row_bytes;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        if (j < k) {
+          const int s = slots[(long long)t * k + j];
+          if (s < cap) {
+            uint8_t* dst = buf + ((long long)indices[(long long)t * k + j] * cap + s) * row_bytes;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(dst), "r"(bk_smem(row)), "r"(row_bytes) : "memory");
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // reuse the slot of token i - BK_LAG once its stores have read shared memory
+    const int r = i - BK_LAG;
+    if (r >= 0 && r + BK_SLOTS < n) {
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(BK_LAG) : "memory");
+      load(t0 + r + BK_SLOTS, r % BK_SLOTS);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---- peer-memory signalling -------------------------------------------------
 // flags (per rank, symmetric): [0][src] = dispatch epoch received from src,
 // [1][owner] = y-ready / rows-returned epoch received from owner.  epoch_ctr
@@ -439,11 +524,45 @@ extern "C" int scmoe_dispatch_scaled(const void* x, int dtype, long long ld_x, i
   return SCMOE_OK;
 }
 
+// Testing hooks: 1 routes scmoe_dispatch through the register-staged kernel;
+// CTAs per SM of the bulk-copy kernel.
+extern "C" int scmoe_dispatch_force_ldst = 0;
+extern "C" int scmoe_dispatch_bulk_ctas_per_sm = 16;   // measured: 1x 45, 4x 31, 16x 28.7 us (= ldst)
+
 extern "C" int scmoe_dispatch(const void* x, int dtype, long long ld_x, int n_tokens,
                               int d_model, int k, const int32_t* indices, const int32_t* slots,
                               int capacity, void* dispatch_buf, void* stream) {
-  return scmoe_dispatch_scaled(x, dtype, ld_x, n_tokens, d_model, k, indices, slots, capacity,
-                               nullptr, dispatch_buf, stream);
+  using namespace scmoe;
+  const int esz = dtype == SCMOE_BF16 ? 2 : 4;
+  const long long row_bytes = (long long)d_model * esz;
+  if (scmoe_dispatch_force_ldst || n_tokens <= 0 || (dtype != SCMOE_BF16 && dtype != SCMOE_F32) ||
+      k < 1 || k > SCMOE_MAX_K || capacity < 1 || row_bytes % 16 || (ld_x * esz) % 16 ||
+      row_bytes * BK_SLOTS > 96 * 1024 || !aligned16(x) || !aligned16(dispatch_buf))
+    return scmoe_dispatch_scaled(x, dtype, ld_x, n_tokens, d_model, k, indices, slots, capacity,
+                                 nullptr, dispatch_buf, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = (size_t)row_bytes * BK_SLOTS;
+  static size_t smem_set[3] = {0, 0, 0};
+  const int kk = k == 1 ? 0 : (k == 2 ? 1 : 2);
+  if (smem > 48 * 1024 && smem > smem_set[kk]) {
+    if (k == 1) SCMOE_CUDA_TRY(cudaFuncSetAttribute(dispatch_bulk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    else if (k == 2) SCMOE_CUDA_TRY(cudaFuncSetAttribute(dispatch_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    else SCMOE_CUDA_TRY(cudaFuncSetAttribute(dispatch_bulk_kernel<SCMOE_MAX_K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    smem_set[kk] = 96 * 1024;
+  }
+  // enough CTAs for the copy engines of every SM, few enough that each CTA
+  // streams a long contiguous token range
+  const int grid = min(n_tokens, num_sms() * max(1, scmoe_dispatch_bulk_ctas_per_sm));
+#define SCMOE_BULK(KM)                                                                          \
+  dispatch_bulk_kernel<KM><<<grid, 32, smem, st>>>((const uint8_t*)x, ld_x * esz, n_tokens,      \
+                                                   (int)row_bytes, k, indices, slots, capacity, \
+                                                   (uint8_t*)dispatch_buf)
+  if (k == 1) SCMOE_BULK(1);
+  else if (k == 2) SCMOE_BULK(2);
+  else SCMOE_BULK(SCMOE_MAX_K);
+#undef SCMOE_BULK
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
 }
 
 extern "C" int scmoe_combine(const void* se_out, const void* expert_out, const void* x_cur,

@@ -64,8 +64,12 @@ for k in (1, 2):
     dec = K.gate_topk(x, w, k, quota)
     kept = int((dec.slots < quota).sum().item())
     buf = K.dispatch(x, dec.indices, dec.slots, N, quota)
-    us = time_us(lambda: K.dispatch(x, dec.indices, dec.slots, N, quota, out=buf))
-    res[f"dispatch_k{k}"] = dict(us=us, gbps=2 * kept * d * 2 / us / 1e3)
+    dflag = ctypes.c_int.in_dll(_lib.lib(), "scmoe_dispatch_force_ldst")
+    for name, f in (("bulk", 0), ("ldst", 1)):
+        dflag.value = f
+        us = time_us(lambda: K.dispatch(x, dec.indices, dec.slots, N, quota, out=buf))
+        res[f"dispatch_k{k}_{name}"] = dict(us=us, gbps=2 * kept * d * 2 / us / 1e3)
+    dflag.value = 0
     se = torch.randn(T, d, device="cuda", generator=g).bfloat16()
     resid = torch.randn(T, d, device="cuda", generator=g).bfloat16()
     out = torch.empty_like(se)
