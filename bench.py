@@ -192,27 +192,64 @@ class Clocks:
 # CPU reference leg (oracle = float64 restatement of the reference algorithm)
 
 
+def _reference_package():
+    """The unmodified reference (scmoelab), installed offline into
+    baseline/_ref (git-ignored; travels to the GPU box with the snapshot).
+    None when it is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "scmoelab")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from scmoelab import arch, numkit
+    except Exception:  # pragma: no cover
+        return None
+    return arch, numkit
+
+
 def cpu_reference_time(w, tokens: int, reps: int, warmup: int = 1):
-    """Seconds per block-pair forward of the reference algorithm on `tokens`
-    tokens of the workload's shape, using every host thread numpy/BLAS gets."""
-    import numpy as np
-    from oracle import scmoe_oracle as O
-    rng = O.Rng(0)
+    """Seconds per block-pair (or every-block block) forward of the reference
+    on `tokens` tokens of the workload's shape, on every host thread
+    numpy/BLAS gets.  Runs the real reference (scmoelab arch.forward, value
+    mode) when baseline/_ref holds it ("reference"), else the float64 port of
+    its algorithm in oracle/ ("port").  Both evaluate every expert densely
+    (arch.py:418-433)."""
     n_exp = w["n_experts"] or 8
-    x = rng.spawn(1).normal((tokens, w["d"]))
-    if w.get("every_block"):
-        # one every-block Transformer block (arch.py:632-663), ScMoE pos1
-        blocks = O.init_model(1, w["d"], w["h"], n_exp, rng.spawn(0), moe_frequency="every-block",
-                              variant="scmoe", combine_mode=w["combine"])
+    pkg = _reference_package()
+    if pkg is not None:
+        arch, numkit = pkg
+        every = bool(w.get("every_block"))
+        cfg = arch.ModelConfig(n_blocks=1 if every else 2, d_model=w["d"], d_hidden=w["h"],
+                               n_experts=n_exp, k_routed=1,
+                               moe_frequency="every-block" if every else "every-second-block",
+                               variant="scmoe", shortcut_pos=w["pos"], combine_mode=w["combine"],
+                               capacity_factor=w["cf"])
+        params = arch.init_params(cfg, numkit.Rng(0))
+        x = numkit.Rng(1).normal((tokens, w["d"]))
 
         def run():
-            O.model_forward(blocks, x, "scmoe", "pos1", w["cf"], 1, moe_frequency="every-block")
+            arch.forward(cfg, params, x)
+        kind = "reference"
     else:
-        pp = O.init_pair(w["d"], w["h"], n_exp, rng.spawn(0), variant="scmoe",
-                         combine_mode=w["combine"])
+        from oracle import scmoe_oracle as O
+        rng = O.Rng(0)
+        x = rng.spawn(1).normal((tokens, w["d"]))
+        if w.get("every_block"):
+            blocks = O.init_model(1, w["d"], w["h"], n_exp, rng.spawn(0),
+                                  moe_frequency="every-block", variant="scmoe",
+                                  combine_mode=w["combine"])
 
-        def run():
-            O.block_pair_forward(pp, x, "scmoe", w["pos"], w["cf"], 1)
+            def run():
+                O.model_forward(blocks, x, "scmoe", "pos1", w["cf"], 1,
+                                moe_frequency="every-block")
+        else:
+            pp = O.init_pair(w["d"], w["h"], n_exp, rng.spawn(0), variant="scmoe",
+                             combine_mode=w["combine"])
+
+            def run():
+                O.block_pair_forward(pp, x, "scmoe", w["pos"], w["cf"], 1)
+        kind = "port"
     times = []
     for i in range(warmup + reps):
         t0 = time.perf_counter()
@@ -226,7 +263,7 @@ def cpu_reference_time(w, tokens: int, reps: int, warmup: int = 1):
     except Exception:  # pragma: no cover
         blas = []
     cores = len(os.sched_getaffinity(0))
-    return times, cores, blas
+    return times, cores, blas, kind
 
 
 def run_reference(args):
@@ -235,7 +272,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     w = WORKLOADS[args.workload]
-    times, cores, blas = cpu_reference_time(w, args.ref_tokens, args.steps, args.warmup)
+    times, cores, blas, kind = cpu_reference_time(w, args.ref_tokens, args.steps, args.warmup)
     mean = sum(times) / len(times)
     value = args.ref_tokens / mean
     line = {
@@ -245,9 +282,11 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": w["name"], "d_model": w["d"],
                                         "d_hidden": w["h"], "n_experts": w["n_experts"] or 8,
                                         "tokens_per_step": args.ref_tokens},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.ref_tokens} tokens per step of the {w['name']} block "
-                                   f"pair, dense fp64 (every expert on every token, as arch.py:418-433)",
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.ref_tokens} tokens per step of the {w['name']}, "
+                                   + ("scmoelab arch.forward (baseline/_ref)" if kind == "reference"
+                                      else "float64 port in oracle/")
+                                   + ", dense fp64 (every expert on every token, arch.py:418-433)",
                          "blas": blas},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -614,11 +653,14 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and dense_gb > 8:
         line["cpu_baseline"] = {"value": None, "skipped": f"dense fp64 weights {dense_gb:.0f} GB"}
     elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        times, cores, blas = cpu_reference_time(w, args.cpu_tokens, args.cpu_reps)
+        times, cores, blas, kind = cpu_reference_time(w, args.cpu_tokens, args.cpu_reps)
         v = args.cpu_tokens / (sum(times) / len(times))
-        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                                "sample": f"{args.cpu_tokens} tokens x {args.cpu_reps} reps, dense "
-                                          f"fp64 oracle of the same block pair", "blas": blas}
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": kind,
+                                "sample": f"{args.cpu_tokens} tokens x {args.cpu_reps} reps of the "
+                                          f"same block, dense fp64, "
+                                          + ("scmoelab arch.forward (baseline/_ref)"
+                                             if kind == "reference" else "oracle/ port"),
+                                "blas": blas}
     if rank == 0:
         emit(line)
     import torch.distributed as dist
