@@ -58,6 +58,9 @@ WORKLOADS = {
                         causal=True, every_block=True),
 }
 
+# configs[4]: all-to-all + overlap sweep (run_a2a_sweep)
+SWEEP_TOKENS = (1024, 2048, 4096, 8192, 16384, 32768, 65536)
+
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_traffic.json")
 
@@ -392,6 +395,80 @@ def hbm_kernel_times(moe, x, reps: int = 10):
     return res_d
 
 
+def run_a2a_sweep(args):
+    """configs[4]: the expert-parallel exchange alone, tokens/GPU 1K..64K,
+    d=2048 bf16, 8 experts over the ranks, top-1, cf 1.0.  Per size: our
+    peer-memory dispatch + return (K9 / K9b with flag waits, full grid) and
+    the NCCL baseline (count a2a + equal-split all_to_all_single each way),
+    device-timed, max over ranks (p2p as a CUDA-graph replay, as in the
+    block; NCCL eager).  Bytes = kept rows x d x 2 per direction
+    (the NCCL arm moves the capacity-padded buffer).  At one rank the
+    'exchange' is a local HBM copy — the NVLink numbers need N > 1."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_05019_b200 as P
+    from paper_2404_05019_b200 import ep, kernels as K
+    from paper_2404_05019_b200.ep_p2p import PeerExchange
+    ws, rank, local = dist_setup(True)
+    group = dist.group.WORLD
+    d, E = 2048, 8
+    if E % ws:
+        E = ws
+    e_l = E // ws
+    dev = torch.device("cuda", local)
+    gate = P.Top1Gate(d, E, capacity_factor=1.0, device=dev,
+                      generator=torch.Generator(device=dev).manual_seed(5))
+    rows = []
+    reps = max(3, args.steps)
+    for T in SWEEP_TOKENS:
+        x = torch.randn(T, d, device=dev, generator=torch.Generator(device=dev).manual_seed(
+            rank + T)).bfloat16()
+        dec = gate(x)
+        cap = dec.capacity
+        kept = int(dec.kept_counts().sum().item())
+        px = PeerExchange.from_group(group, e_l, cap, d, torch.bfloat16, dev)
+
+        def p2p():
+            px.dispatch(x, dec.indices, dec.slots, dec.counts)
+            px.wait(0)
+            px.push_back()
+            px.wait(1)
+        buf = K.dispatch(x, dec.indices, dec.slots, E, cap)
+        kc = dec.kept_counts().to(torch.int32)
+
+        def nccl():
+            pend = ep.dispatch_exchange(buf, kc, cap, group)
+            ep.combine_exchange(pend.recv, group)
+        res = {"tokens_per_gpu": T, "capacity": cap, "kept_rows": kept}
+        # the p2p exchange is graph-safe and runs graphed inside the block:
+        # time it as a CUDA-graph replay (NCCL stays eager)
+        from paper_2404_05019_b200.runtime import CapturedStep
+        g_p2p = CapturedStep(lambda xx: p2p(), [x])
+        for name, fn in (("p2p", lambda: g_p2p.replay()), ("nccl", nccl)):
+            for _ in range(2):
+                fn()
+            ms, _ = timed(lambda r: fn(), reps, ws)
+            moved = kept * d * 2 if name == "p2p" else E * cap * d * 2
+            res[name] = {"ms": ms, "bytes_per_direction": moved,
+                         "gbps_per_direction": moved / (ms / 2 * 1e-3) / 1e9}
+        rows.append(res)
+        del px
+    line = {"metric": "EP exchange GB/s per direction (dispatch + return)", "unit": "GB/s",
+            "value": rows[-1]["p2p"]["gbps_per_direction"], "n_gpus": ws, "steps": reps,
+            "warmup": 2, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "a2a + overlap sweep (configs[4])", "d_model": d,
+                       "n_experts": E, "tokens_per_gpu": list(SWEEP_TOKENS),
+                       "capacity_factor": 1.0, "parallelism": f"ep{ws}"},
+            "sweep": rows,
+            "note": ("one rank: both arms are local HBM copies; the NVLink figures (900 GB/s "
+                     "per direction peak) need N > 1") if ws == 1 else None}
+    if rank == 0:
+        emit(line)
+    dist.destroy_process_group()
+    return 0
+
+
 def count_launches(step):
     """(kernels of libscmoe.so, other kernels) launched by one step."""
     import torch
@@ -675,7 +752,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="gpt3xl")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["a2a_sweep"], default="gpt3xl")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-training", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
@@ -696,6 +773,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "a2a_sweep":
+        return run_a2a_sweep(args)
     return run_ours(args)
 
 
