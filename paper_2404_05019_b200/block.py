@@ -50,6 +50,42 @@ def layer_norm(x: torch.Tensor) -> torch.Tensor:
 
 
 PACKED_ATTENTION = True     # training attention through flash-attn's packed-QKV kernels
+ATTN_TRAIN = "cudnn_packed"  # "cudnn_packed" | "flash_packed" | "autograd"
+
+
+class _CudnnPackedAttention(torch.autograd.Function):
+    """Training attention core on cuDNN SDPA with the layouts under our
+    control: q/k/v are views of the packed (T, 3d) projection, the output is
+    returned as (T, d), and the backward writes dq/dk/dv straight into the
+    packed (B, S, 3, H, hd) gradient with one copy per tensor (autograd's
+    unbind/stack + permute copies were ~12% of the step).  The SDPA forward
+    records its own small autograd graph (saved output / log-sum-exp), which
+    the backward replays — no recomputation."""
+
+    @staticmethod
+    def forward(ctx, qkv, b, s, h, causal, scale):
+        t, d3 = qkv.shape
+        d = d3 // 3
+        hd = d // h
+        with torch.enable_grad():
+            q5 = qkv.detach().view(b, s, 3, h, hd)
+            q, k, v = (q5[:, :, i].transpose(1, 2).requires_grad_() for i in range(3))
+            o = F.scaled_dot_product_attention(q, k, v, is_causal=causal, scale=scale)
+        ctx.inner = (q, k, v, o)
+        ctx.shape = (b, s, h, hd)
+        return o.detach().transpose(1, 2).reshape(t, d)
+
+    @staticmethod
+    def backward(ctx, g):
+        q, k, v, o = ctx.inner
+        b, s, h, hd = ctx.shape
+        go = g.reshape(b, s, h, hd).transpose(1, 2)
+        dq, dk, dv = torch.autograd.grad(o, (q, k, v), go)
+        dqkv = torch.empty(b, s, 3, h, hd, device=g.device, dtype=g.dtype)
+        for i, gi in enumerate((dq, dk, dv)):
+            dqkv[:, :, i].copy_(gi.transpose(1, 2))
+        ctx.inner = None
+        return dqkv.view(b * s, 3 * h * hd), None, None, None, None, None
 
 
 def _use_packed_attention(qkv: torch.Tensor, hd: int) -> bool:
@@ -102,7 +138,9 @@ class Attention(nn.Module):
         else:
             qkv = K.grouped_gemm(x, self.w_qkv_t, None)                    # (T, 3d)
         scale = 1.0 / math.sqrt(d) if h == 1 else 1.0 / math.sqrt(hd)
-        if train and _use_packed_attention(qkv, hd):
+        if train and ATTN_TRAIN == "cudnn_packed" and qkv.dtype == torch.bfloat16:
+            o = _CudnnPackedAttention.apply(qkv, b, s, h, self.causal, scale)
+        elif train and ATTN_TRAIN == "flash_packed" and _use_packed_attention(qkv, hd):
             # training: flash-attn's packed-QKV kernels read (B, S, 3, H, hd) and
             # write dqkv in the same packed layout — no stack / permute copies
             # around the attention backward (they were ~12% of the step)
