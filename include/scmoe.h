@@ -179,6 +179,13 @@ int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap
 int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_t* ids,
                       const int32_t* n_rows, int max_rows, void* dst, void* stream);
 
+/* Attention layout glue (training): n_src (<= 3) bf16 tensors (B, H, S, hd),
+ * element strides[3*i .. 3*i+2] = (b, h, s) of source i, hd contiguous, packed
+ * into dst (B, S, n_src, H, hd) contiguous — dq/dk/dv into the packed QKV
+ * gradient, the SDPA output into (T, d) rows.  srcs / strides are host arrays. */
+int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_src, int B, int H,
+                     int S, int hd, int dtype, void* dst, void* stream);
+
 /* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);

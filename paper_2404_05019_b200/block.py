@@ -73,7 +73,9 @@ class _CudnnPackedAttention(torch.autograd.Function):
             o = F.scaled_dot_product_attention(q, k, v, is_causal=causal, scale=scale)
         ctx.inner = (q, k, v, o)
         ctx.shape = (b, s, h, hd)
-        return o.detach().transpose(1, 2).reshape(t, d)
+        if o.stride(1) == hd and o.stride(2) == h * hd:      # already (B, S, H, hd) in memory
+            return o.detach().transpose(1, 2).reshape(t, d)
+        return K.pack_heads([o.detach()]).view(t, d)
 
     @staticmethod
     def backward(ctx, g):
@@ -81,9 +83,7 @@ class _CudnnPackedAttention(torch.autograd.Function):
         b, s, h, hd = ctx.shape
         go = g.reshape(b, s, h, hd).transpose(1, 2)
         dq, dk, dv = torch.autograd.grad(o, (q, k, v), go)
-        dqkv = torch.empty(b, s, 3, h, hd, device=g.device, dtype=g.dtype)
-        for i, gi in enumerate((dq, dk, dv)):
-            dqkv[:, :, i].copy_(gi.transpose(1, 2))
+        dqkv = K.pack_heads([dq, dk, dv])          # one vectorised pass into (B, S, 3, H, hd)
         ctx.inner = None
         return dqkv.view(b * s, 3 * h * hd), None, None, None, None, None
 

@@ -306,3 +306,60 @@ extern "C" int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Attention layout glue for training (block.py _CudnnPackedAttention): up to
+// three (B, H, S, hd) tensors with arbitrary strides (hd contiguous) packed
+// into one (B, S, n, H, hd) tensor — dq/dk/dv into the packed QKV gradient,
+// or the SDPA output into (T, d) rows.  One thread per 16-byte vector,
+// consecutive threads write consecutive destination bytes.
+namespace scmoe {
+namespace pack_detail {
+struct PackSrc {
+  const uint4* p[3];
+  long long sb[3], sh[3], ss[3];   // element strides of (B, H, S)
+};
+
+__global__ void pack_heads_kernel(PackSrc src, int n, int B, int H, int S, int hd,
+                                  uint4* __restrict__ dst) {
+  const int v_per_head = hd / 8;                        // bf16: 8 per 16 bytes
+  const long long total = (long long)B * S * n * H * v_per_head;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long r = i;
+    const int e = (int)(r % v_per_head); r /= v_per_head;
+    const int h = (int)(r % H); r /= H;
+    const int c = (int)(r % n); r /= n;
+    const int s = (int)(r % S); r /= S;
+    const int b = (int)r;
+    const long long off = b * src.sb[c] + h * src.sh[c] + s * src.ss[c];   // elements
+    dst[i] = __ldg(src.p[c] + off / 8 + e);
+  }
+}
+}  // namespace pack_detail
+}  // namespace scmoe
+
+extern "C" int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_src,
+                                int B, int H, int S, int hd, int dtype, void* dst, void* stream) {
+  using namespace scmoe;
+  using namespace scmoe::pack_detail;
+  SCMOE_CHECK_ARG(dtype == SCMOE_BF16, "pack_heads supports bf16");
+  SCMOE_CHECK_ARG(n_src >= 1 && n_src <= 3 && srcs && strides && dst, "bad arguments");
+  SCMOE_CHECK_ARG(hd % 8 == 0 && B > 0 && H > 0 && S > 0, "hd must be a multiple of 8");
+  PackSrc ps{};
+  for (int i = 0; i < n_src; ++i) {
+    ps.p[i] = (const uint4*)srcs[i];
+    ps.sb[i] = strides[3 * i];
+    ps.sh[i] = strides[3 * i + 1];
+    ps.ss[i] = strides[3 * i + 2];
+    SCMOE_CHECK_ARG(((uintptr_t)srcs[i] & 15) == 0 && ps.sb[i] % 8 == 0 && ps.sh[i] % 8 == 0 &&
+                        ps.ss[i] % 8 == 0,
+                    "source %d must be 16-byte aligned with strides multiple of 8", i);
+  }
+  SCMOE_CHECK_ARG(((uintptr_t)dst & 15) == 0, "dst must be 16-byte aligned");
+  const long long total = (long long)B * S * n_src * H * (hd / 8);
+  const int grid = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
+  pack_heads_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ps, n_src, B, H, S, hd, (uint4*)dst);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}

@@ -302,3 +302,23 @@ def dispatch_scaled(x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor,
                                       ptr(_c(indices, "indices")), ptr(_c(slots, "slots")),
                                       capacity, ptr(row_scale), ptr(out), stream_ptr(stream)))
     return out
+
+
+def pack_heads(srcs, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """(B, H, S, hd) bf16 tensors (any strides, hd contiguous) -> one
+    (B, S, n, H, hd) contiguous tensor (scmoe_pack_heads)."""
+    import ctypes
+    b, h, s, hd = srcs[0].shape
+    for t in srcs:
+        ensure_device(t)
+        if t.shape != srcs[0].shape or t.stride(3) != 1 or t.dtype != torch.bfloat16:
+            raise ValueError("pack_heads: bf16 (B, H, S, hd) sources with contiguous hd")
+    n = len(srcs)
+    if out is None:
+        out = torch.empty(b, s, n, h, hd, device=srcs[0].device, dtype=srcs[0].dtype)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in srcs])
+    strides = (ctypes.c_longlong * (3 * n))(*[v for t in srcs for v in t.stride()[:3]])
+    check(lib().scmoe_pack_heads(ctypes.cast(ptrs, ctypes.c_void_p),
+                                 ctypes.cast(strides, ctypes.c_void_p), n, b, h, s, hd,
+                                 _lib.SCMOE_BF16, ptr(out), stream_ptr(stream)))
+    return out

@@ -255,3 +255,17 @@ def test_dispatch_and_combine(dtype, k):
     out = K.combine(y, dec.indices, dec.slots, dec.weights, quota)
     tol = 1e-5 if dtype == torch.float32 else 2e-2
     torch.testing.assert_close(out.double(), routed, rtol=tol, atol=tol * routed.abs().max().item())
+
+
+def test_pack_heads_matches_torch():
+    """scmoe_pack_heads: strided (B, H, S, hd) sources -> (B, S, n, H, hd)."""
+    B, H, S, hd = 3, 5, 70, 32
+    base = torch.randn(B, S, 3, H, hd, device="cuda").bfloat16()
+    srcs = [base[:, :, i].transpose(1, 2) for i in range(3)]          # BSHD strides
+    srcs[1] = srcs[1].contiguous()                                     # BHSD contiguous
+    out = K.pack_heads(srcs)
+    ref = torch.stack([t.transpose(1, 2) for t in srcs], dim=2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    one = K.pack_heads([srcs[1]])
+    assert torch.equal(one[:, :, 0], srcs[1].transpose(1, 2))
