@@ -102,7 +102,16 @@ def dist_setup(force_dist: bool = False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = os.environ.get("SCMOE_BENCH_SHARED_GPU") == "1"
     if ws > 1 or force_dist:
+        if shared:
+            # test hook: every rank on GPU 0 with a gloo group — exercises the
+            # N > 1 code paths (EP sharding, peer mapping over CUDA IPC, flags,
+            # graph capture, max-over-ranks timing) on a one-GPU box; timings
+            # are meaningless (the ranks share one GPU)
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return ws, rank, 0
         if ws == 1:      # one-rank group without torchrun
             import socket
             with socket.socket() as sk:
@@ -592,12 +601,22 @@ def run_ours(args):
         src = x.clone()
         if use_graphs:
             g_sc = CapturedStep(fwd(sc), [x])
-            g_lsc = CapturedStep(lambda xx: sc.moe(xx, src)[0], [x])
-            run = {"sc": lambda r: g_sc.replay(), "lsc": lambda r: g_lsc.replay()}
+            run = {"sc": lambda r: g_sc.replay()}
             if t2 is not None:
                 g_t2 = CapturedStep(fwd(t2), [x])
-                g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
-                run.update(t2=lambda r: g_t2.replay(), lt2=lambda r: g_lt2.replay())
+                run.update(t2=lambda r: g_t2.replay())
+            if group is None:
+                g_lsc = CapturedStep(lambda xx: sc.moe(xx, src)[0], [x])
+                run.update(lsc=lambda r: g_lsc.replay())
+                if t2 is not None:
+                    g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
+                    run.update(lt2=lambda r: g_lt2.replay())
+            else:
+                # the bare layer's EP path is the NCCL exchange (the p2p
+                # exchange lives in the block's scheduled forward): eager
+                run.update(lsc=lambda r: sc.moe(x, src))
+                if t2 is not None:
+                    run.update(lt2=lambda r: t2.moe(x))
         else:
             run = {"sc": lambda r: sc(x), "lsc": lambda r: sc.moe(x, src)}
             if t2 is not None:
