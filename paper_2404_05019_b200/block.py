@@ -212,6 +212,8 @@ class ScMoEBlockPair(nn.Module):
                                   combine_mode=combine_mode, capacity_factor=capacity_factor,
                                   noise_enabled=noise_enabled, ep_group=ep_group, **kw)
         self.ep_group = ep_group
+        if hasattr(self.moe, "ep_backend"):
+            self.moe.ep_backend = ep_backend
         self.offload = None
         self.offload_mode = "none"
         self.slot: Optional[int] = None
@@ -253,15 +255,9 @@ class ScMoEBlockPair(nn.Module):
         return layer_norm(h) if self.pre_layernorm else h
 
     def peer_exchange(self, capacity: int):
-        """Symmetric buffers for the p2p backend (re-created if the capacity,
-        i.e. the per-rank token count, changes)."""
-        from .ep_p2p import PeerExchange
-        x = self._xchg
-        if x is None or x.capacity != capacity:
-            moe = self.moe
-            self._xchg = PeerExchange.from_group(self.ep_group, moe.experts.n_experts, capacity,
-                                                 moe.d_model, moe.dtype,
-                                                 moe.gate.w_gate_t.device)
+        """Peer-mapped buffers of the p2p backend — the MoE layer's own (one
+        set per layer, re-created when the per-rank capacity changes)."""
+        self._xchg = self.moe.peer_exchange(capacity)
         return self._xchg
 
     def comm_stream(self) -> torch.cuda.Stream:

@@ -346,6 +346,10 @@ class _RoutedMoE(nn.Module):
                 raise ConfigError(f"n_experts={n_experts} not divisible by EP size {ws}")
         self.ep_size = ws
         self.experts = RoutedExperts(n_experts // ws, d_model, d_hidden, dtype, device, generator)
+        # expert-parallel exchange: "nccl" (all-to-all of the capacity
+        # buffers, ep.py) or "p2p" (our peer-memory kernels, ep_p2p.py)
+        self.ep_backend = "nccl"
+        self._xchg = None
 
     @property
     def noise_enabled(self):
@@ -372,6 +376,8 @@ class _RoutedMoE(nn.Module):
     def routed_experts(self, x_src: torch.Tensor, dec: GateDecision, stream=None) -> torch.Tensor:
         """dispatch + expert FFN (+ EP exchange); returns the (N, C, d) expert
         output buffer that combine gathers from."""
+        if self.ep_group is not None and self.ep_backend == "p2p":
+            return self._p2p_routed(x_src, dec, stream)
         buf = K.dispatch(x_src, dec.indices, dec.slots, self.n_experts, dec.capacity, stream=stream)
         if self.ep_group is None:
             # rows(g) = min(pre-drop count, capacity) is computed in the kernel
@@ -379,6 +385,26 @@ class _RoutedMoE(nn.Module):
             return self.experts(buf, rows, dec.capacity, stream=stream)
         from . import ep
         return ep.expert_parallel_ffn(self.experts, buf, dec, self.ep_group)
+
+    def peer_exchange(self, capacity: int):
+        """Peer-mapped buffers of the p2p backend (re-created when the
+        capacity, i.e. the per-rank token count, changes)."""
+        from .ep_p2p import PeerExchange
+        if self._xchg is None or self._xchg.capacity != capacity:
+            self._xchg = PeerExchange.from_group(self.ep_group, self.experts.n_experts, capacity,
+                                                 self.d_model, self.dtype,
+                                                 self.gate.w_gate_t.device)
+        return self._xchg
+
+    def _p2p_routed(self, x_src, dec, stream=None) -> torch.Tensor:
+        """Synchronous p2p EP on one stream: rows to their owners, owner FFN,
+        rows back; returns the (E, C, d) buffer combine gathers from."""
+        xg = self.peer_exchange(dec.capacity)
+        xg.dispatch(x_src, dec.indices, dec.slots, dec.counts, stream=stream)
+        xg.expert_ffn(self.experts, signal=False, stream=stream)
+        xg.push_back(stream=stream)
+        xg.wait(1, stream)
+        return xg.back.view(-1, dec.capacity, self.d_model)
 
     # -- training (autograd through the K7 kernels) ---------------------------
     def training_path(self) -> bool:

@@ -59,6 +59,21 @@ def _worker(rank, world, port, variant, q):
             if not torch.equal(a, b):
                 raise AssertionError(f"rank {rank} call {it}: max diff "
                                      f"{(a.float() - b.float()).abs().max().item()}")
+        # the standalone layer module (moe_shared / moe_standard drop-in) on the
+        # p2p backend, same weights as the local block's layer
+        epl = epb.moe
+        with torch.no_grad():
+            x = torch.randn(T, d, device="cuda", generator=torch.Generator(device="cuda")
+                            .manual_seed(7 + rank)).bfloat16()
+            if variant == "scmoe":
+                a = loc.moe(x, x.flip(0))[0]
+                b = epl(x, x.flip(0))[0]
+            else:
+                a = loc.moe(x)[0]
+                b = epl(x)[0]
+        torch.cuda.synchronize()
+        if not torch.equal(a, b):
+            raise AssertionError(f"rank {rank}: layer-level p2p differs")
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
