@@ -91,6 +91,23 @@ int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                     uint8_t* dropped, int32_t* counts, float* prob_sum,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* The tensor-core gate (bf16 tokens, no noise, N <= 16, d >= 64) multiplies a
+ * 3-part bf16 split of the fp32 gate weights.  scmoe_gate_topk splits them on
+ * every call; an inference caller with fixed weights splits once
+ * (scmoe_gate_split_weights into scmoe_gate_split_bytes of 16-byte aligned
+ * device memory) and calls scmoe_gate_topk_presplit — same outputs, one
+ * kernel launch less.  split_bytes is 0 when the tensor-core path does not
+ * apply. */
+size_t scmoe_gate_split_bytes(int n_experts, int d_model);
+int scmoe_gate_split_weights(const float* w_gate_t, int n_experts, int d_model, void* blob,
+                             void* stream);
+int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld_x, const float* w_gate_t,
+                             const void* w_split, const int32_t* exclude, int n_tokens,
+                             int d_model, int n_experts, int k, int quota, float* logits,
+                             int32_t* indices, float* weights, int32_t* slots, uint8_t* dropped,
+                             int32_t* counts, float* prob_sum, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /*
  * K2 — dispatch ("encode"): copy each kept selection's row
  * of x_src into the capacity-slotted buffer

@@ -33,6 +33,10 @@ SIGNATURES = [
     ("scmoe_gate_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_gate_topk", _i, [_vp, _i, _ll, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                              _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    ("scmoe_gate_split_bytes", _sz, [_i, _i]),
+    ("scmoe_gate_split_weights", _i, [_vp, _i, _i, _vp, _vp]),
+    ("scmoe_gate_topk_presplit", _i, [_vp, _i, _ll, _vp, _vp, _vp, _i, _i, _i, _i, _i,
+                                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     ("scmoe_dispatch", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),
     ("scmoe_grouped_gemm", _i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i,
                                 _vp]),

@@ -87,13 +87,14 @@ struct RouteState {            // survives between publish and finish (shared me
 
 // LOCAL = true (tensor-core gate): no look-back at all — the in-tile rank of
 // every selection goes to `slots` and the tile's per-expert count to
-// status[tile][e]; gate_slots_kernel adds the prefix over earlier tiles.
+// status[tile][e]; the kernel's tail adds the prefix over earlier tiles.
 template <int NMAX, int TOK_, int THREADS_, int BASE = 0, int BAR = 1, bool LOCAL = false>
 __device__ __forceinline__ void route_publish(
     const float (*s_logit)[NMAX + 1], RouteState<NMAX, TOK_>& rs, int tile,
     const int32_t* __restrict__ exclude, int n_tok, int N, int k, float* __restrict__ logits,
     int32_t* __restrict__ indices, float* __restrict__ weights, int32_t* __restrict__ counts,
-    uint32_t* __restrict__ status, float* __restrict__ psum, int32_t* __restrict__ slots = nullptr) {
+    uint32_t* __restrict__ status, float* __restrict__ psum, int32_t* __restrict__ slots = nullptr,
+    uint32_t* lcache = nullptr) {
   constexpr int RW = TOK_ / 32;
   __shared__ int s_wcnt[RW][NMAX];
   __shared__ float s_wprob[RW][NMAX];
@@ -225,6 +226,7 @@ __device__ __forceinline__ void route_publish(
         const int lr = s_wcnt[warp][sel[j]] + rank[j];
         if (LOCAL) {
           slots[(long long)t * k + j] = lr;
+          if (lcache && j < 2) lcache[tid * 2 + j] = ((uint32_t)sel[j] << 16) | (uint32_t)lr;
         } else {
           rs.sel[tid][j] = (int8_t)sel[j];
           rs.lr[tid][j] = lr;
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
 // over x.
 //
 // Persistent and warp-specialised, one CTA per SM, tiles of TOK tokens
-// assigned round-robin (no cross-tile dependency: gate_slots_kernel adds the
+// assigned round-robin (no cross-tile dependency while streaming; the tail adds the
 // capacity-slot prefix over tiles afterwards).
 //   producer warp  — per stage, KC/64 TMA boxes of TOK rows x 64 columns
 //                    (cp.async.bulk.tensor.2d, 128B swizzle, OOB rows/columns
@@ -520,6 +522,11 @@ __device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -589,6 +596,7 @@ __global__ void gate_split_weights_kernel(const float* __restrict__ wg_t, int d,
   }
 }
 
+
 template <int NT>
 __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
     const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ blob,
@@ -624,19 +632,112 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
   if (warp > GT_PRODUCER) {
     // ---------------- routing warps ----------------
     // per tile: top-k, weights, in-tile ranks and per-expert tile counts (no
-    // cross-tile dependency; gate_slots_kernel adds the tile prefix)
+    // cross-tile dependency); after the CTA's last tile, a grid-wide wait for
+    // every tile's counts (safe: the grid is persistent and resident, and no
+    // CTA waits on the one waiting), then the tile prefixes turn this CTA's
+    // in-tile ranks into capacity slots — no second launch.
     __shared__ RouteState<NMAX, TOK> rs;
     constexpr int RT = GT_ROUTERS * 32;
+    constexpr int LCACHE_TILES = 4;        // (expert, in-tile rank) of this CTA's first tiles
+    __shared__ uint32_t s_lcache[LCACHE_TILES][TOK * 2];
+    const int rtid = tid - GT_ROUTE_BASE;
     for (uint32_t n = 0;; ++n) {
       const int b = n & 1;
       mbar_wait(&lfull_bar[b], (n >> 1) & 1);
       const int tile = s_logit_tile[b];
       if (tile < 0) break;
-      route_publish<NMAX, TOK, RT, GT_ROUTE_BASE, 2, true>(s_logit[b], rs, tile, exclude, n_tok, N,
-                                                           k, logits, indices, weights, counts,
-                                                           status, psum, slots);
+      route_publish<NMAX, TOK, RT, GT_ROUTE_BASE, 2, true>(
+          s_logit[b], rs, tile, exclude, n_tok, N, k, logits, indices, weights, counts, status,
+          psum, slots, (n < LCACHE_TILES && k <= 2) ? s_lcache[n] : nullptr);
       __syncwarp();
       if (lane == 0) mbar_arrive(&lempty_bar[b]);   // publish read s_logit[b] before its barrier
+      // every router thread's writes -> CTA barrier -> one release add (cumulative):
+      // no per-thread fence (a __threadfence is a MEMBAR.SC.GPU per thread)
+      consumer_sync<RT, 2>();
+      if (rtid == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctrs + 2) : "memory");
+    }
+    if (rtid == 0) {
+      const long long t0 = clock64();
+      while (ld_acquire_gpu(ctrs + 2) < (uint32_t)num_tiles) {
+        __nanosleep(200);
+        if (clock64() - t0 > (40LL << 30)) __trap();   // ~20 s: never hang the GPU
+      }
+    }
+    consumer_sync<RT, 2>();
+    // the stage ring is idle now: load the whole (tiles, N) count table (and
+    // on CTA 0 the probability partials) into it with every router thread
+    // (many loads in flight), transposed to [N][tiles + 1]
+    const int ld = num_tiles + 1;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(gsm);
+    float* ptab = reinterpret_cast<float*>(gsm) + (size_t)N * ld;
+    const int ent = num_tiles * N;
+    const bool first = blockIdx.x == 0;
+#pragma unroll 8
+    for (int m = rtid; m < ent; m += RT) {
+      tab[(m % N) * ld + m / N] = __ldcg(status + m);
+      if (first) ptab[(m % N) * ld + m / N] = __ldcg(psum + m);
+    }
+    consumer_sync<RT, 2>();
+    // this CTA's tiles only need their own prefixes: a parallel reduction over
+    // the shared-memory table per tile (thread (e, p) sums tiles p, p+P, ...)
+    constexpr int P = RT / NMAX;
+    __shared__ uint32_t s_red[P][NMAX];
+    __shared__ uint32_t s_base[NMAX];
+    const int e = rtid % NMAX, p = rtid / NMAX;
+    for (int tile = blockIdx.x, n = 0; tile < num_tiles; tile += gridDim.x, ++n) {
+      uint32_t acc = 0;
+      if (e < N)
+        for (int t = p; t < tile; t += P) acc += tab[e * ld + t];
+      s_red[p][e] = acc;
+      consumer_sync<RT, 2>();
+      if (rtid < NMAX) {
+        uint32_t base = 0;
+#pragma unroll
+        for (int q = 0; q < P; ++q) base += s_red[q][rtid];
+        s_base[rtid] = base;
+      }
+      consumer_sync<RT, 2>();
+      const bool cached = n < LCACHE_TILES && k <= 2;
+      for (int i = rtid; i < TOK * k; i += RT) {
+        const long long t = (long long)tile * TOK + i / k;
+        if (t >= n_tok) break;
+        const long long o = t * k + i % k;
+        int slot;
+        if (cached) {
+          const uint32_t v = s_lcache[n][(i / k) * 2 + i % k];
+          slot = (int)s_base[v >> 16] + (int)(v & 0xffffu);
+        } else {
+          slot = (int)s_base[indices[o]] + slots[o];
+        }
+        slots[o] = slot;
+        dropped[o] = slot >= quota ? 1 : 0;
+      }
+      consumer_sync<RT, 2>();
+    }
+    if (first) {
+      // totals and the softmax mean: fixed summation order (deterministic)
+      __shared__ float s_ps[P][NMAX];
+      uint32_t c = 0;
+      float ps = 0.f;
+      if (e < N)
+        for (int t = p; t < num_tiles; t += P) {
+          c += tab[e * ld + t];
+          ps += ptab[e * ld + t];
+        }
+      s_red[p][e] = c;
+      s_ps[p][e] = ps;
+      consumer_sync<RT, 2>();
+      if (rtid < N) {
+        uint32_t cs = 0;
+        float fs = 0.f;
+        for (int q = 0; q < P; ++q) {
+          cs += s_red[q][rtid];
+          fs += s_ps[q][rtid];
+        }
+        counts[rtid] = (int)cs;
+        prob_sum[rtid] = fs;
+      }
     }
     return;
   }
@@ -753,114 +854,50 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
   }
 }
 
-// Second pass of the tensor-core gate.  Tile b's capacity-slot base for
-// expert e is the sum of the tile counts of tiles < b.  Every CTA loads the
-// whole (tiles, N) count table into shared memory with coalesced loads and
-// scans it (one warp per expert column, a warp-wide exclusive scan over
-// per-lane runs), then rewrites the in-tile ranks of its tiles (round robin)
-// into capacity slots and drop flags.  CTA 0 writes counts[] and prob_sum[]
-// (fixed summation order: deterministic).
-template <int NMAX>
-__global__ void __launch_bounds__(256) gate_slots_kernel(
-    const int32_t* __restrict__ indices, int32_t* __restrict__ slots, uint8_t* __restrict__ dropped,
-    const uint32_t* __restrict__ tile_counts, const float* __restrict__ psum,
-    int32_t* __restrict__ counts, float* __restrict__ prob_sum, int n_tok, int N, int k, int quota,
-    int num_tiles) {
-  extern __shared__ uint32_t s_tab[];          // [N][num_tiles + 1] -> exclusive prefix
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ent = num_tiles * N, ld = num_tiles + 1;   // padded rows: conflict-free
-  for (int m = tid; m < ent; m += 256) s_tab[(m % N) * ld + m / N] = tile_counts[m];
-  __syncthreads();
-  // one warp per expert row: 32 consecutive tiles per round, warp inclusive
-  // scan, running carry
-  for (int e = warp; e < N; e += 8) {
-    uint32_t carry = 0;
-    uint32_t* row = s_tab + e * ld;
-    for (int j0 = 0; j0 < num_tiles; j0 += 32) {
-      const int j = j0 + lane;
-      const uint32_t v = j < num_tiles ? row[j] : 0u;
-      uint32_t incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      if (j < num_tiles) row[j] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (blockIdx.x == 0 && lane == 0) counts[e] = (int)carry;
-  }
-  __syncthreads();
-  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-    for (int i = tid; i < TOK * k; i += 256) {
-      const long long t = (long long)tile * TOK + i / k;
-      if (t >= n_tok) break;
-      const long long o = t * k + i % k;
-      const int slot = (int)s_tab[indices[o] * ld + tile] + slots[o];
-      slots[o] = slot;
-      dropped[o] = slot >= quota ? 1 : 0;
-    }
-  }
-  if (blockIdx.x == 0) {
-    constexpr int P = 256 / NMAX;
-    __shared__ float s_ps[P][NMAX];
-    const int e = tid % NMAX, p = tid / NMAX;
-    float ps = 0.f;
-    if (e < N)
-      for (int j = p; j < num_tiles; j += P) ps += psum[(size_t)j * N + e];
-    s_ps[p][e] = ps;
-    __syncthreads();
-    if (tid < N) {
-      float fs = 0.f;
-      for (int q = 0; q < P; ++q) fs += s_ps[q][tid];
-      prob_sum[tid] = fs;
-    }
-  }
-}
 
-constexpr int GT_SLOTS_SMEM_MAX = 200 * 1024;   // count table in shared memory
 
 template <int NT>
-int launch_gate_tc(const void* x, long long ld_x, const float* wg, const int32_t* excl, int T_,
-                   int d, int N, int k, int quota, float* logits, int32_t* idx, float* w,
-                   int32_t* slots, uint8_t* drop, int32_t* counts, float* prob_sum, uint8_t* ws,
-                   cudaStream_t st) {
+int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* presplit,
+                   const int32_t* excl, int T_, int d, int N, int k, int quota, float* logits,
+                   int32_t* idx, float* w, int32_t* slots, uint8_t* drop, int32_t* counts,
+                   float* prob_sum, uint8_t* ws, cudaStream_t st) {
   using C = GateTC<NT>;
   const int tiles = (T_ + TOK - 1) / TOK;
   const int ngrp = (d + 63) / 64;
+  uint32_t* ctrs = reinterpret_cast<uint32_t*>(ws);
   uint32_t* tile_counts = reinterpret_cast<uint32_t*>(ws + CTR_BYTES);
   float* psum = reinterpret_cast<float*>(ws + CTR_BYTES + (size_t)tiles * N * 4);
-  uint8_t* blob = ws + gate_ws_bytes(T_, N);
-  const size_t tab = (size_t)(tiles + 1) * N * 4;
-  if (tab > (size_t)GT_SLOTS_SMEM_MAX) {
-    set_error("tensor-core gate: %d tokens x %d experts exceed the slot pass's table", T_, N);
+  // the in-kernel slot pass scans the (tiles, N) count and probability tables
+  // inside the stage ring
+  if ((size_t)2 * (tiles + 1) * N * 4 > (size_t)C::STAGES * C::STAGEB) {
+    set_error("tensor-core gate: %d tokens x %d experts exceed the in-kernel slot table", T_, N);
     return SCMOE_ERR_UNSUPPORTED;
   }
-  {
+  const uint8_t* blob = (const uint8_t*)presplit;
+  if (!blob) {      // split the weights now (inference callers pass a cached blob)
+    uint8_t* b = ws + gate_ws_bytes(T_, N);
     const int total = ngrp * NT * 128;
-    gate_split_weights_kernel<NT><<<(total + 255) / 256, 256, 0, st>>>(wg, d, N, ngrp,
-                                                                       (uint2*)blob);
+    gate_split_weights_kernel<NT><<<(total + 255) / 256, 256, 0, st>>>(wg, d, N, ngrp, (uint2*)b);
     SCMOE_LAUNCH_CHECK();
+    blob = b;
   }
+  // publish counter of the in-kernel slot pass (a memset node in a graph)
+  SCMOE_CUDA_TRY(cudaMemsetAsync(ctrs, 0, 16, st));
   static bool attr_set = false;   // once per instantiation, never inside a graph capture
   if (!attr_set) {
     SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_tc_kernel<NT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_slots_kernel<NT * 8>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        GT_SLOTS_SMEM_MAX));
     attr_set = true;
   }
   CUtensorMap xmap;
   const int rc = make_map_2d(&xmap, x, d, T_, ld_x * 2, TOK);
   if (rc != SCMOE_OK) return rc;
+  // persistent and fully resident (one CTA per SM): the in-kernel wait for
+  // every tile's counts cannot deadlock
   const int grid = min(tiles, num_sms());
   gate_topk_tc_kernel<NT><<<grid, GT_THREADS, C::SMEM, st>>>(
-      xmap, blob, excl, T_, d, N, k, quota, logits, idx, w, slots, drop, counts, prob_sum, nullptr,
+      xmap, blob, excl, T_, d, N, k, quota, logits, idx, w, slots, drop, counts, prob_sum, ctrs,
       tile_counts, psum, tiles);
-  SCMOE_LAUNCH_CHECK();
-  gate_slots_kernel<NT * 8><<<min(tiles, num_sms()), 256, tab, st>>>(
-      idx, slots, drop, tile_counts, psum, counts, prob_sum, T_, N, k, quota, tiles);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }
@@ -944,14 +981,14 @@ extern "C" size_t scmoe_gate_workspace_bytes(int n_tokens, int n_experts, int d_
          (size_t)((d_model + 63) / 64) * ((n_experts + 7) / 8) * scmoe::GT_GROUP_B;
 }
 
-extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
-                               const float* w_gate_t, const float* w_noise_t, const float* eps,
-                               const int32_t* exclude,
-                               int n_tokens, int d_model, int n_experts, int k, int quota,
-                               float* logits, int32_t* indices, float* weights, int32_t* slots,
-                               uint8_t* dropped, int32_t* counts, float* prob_sum,
-                               void* workspace, size_t workspace_bytes, void* stream) {
-  using namespace scmoe;
+namespace scmoe {
+namespace {
+int gate_topk_impl(const void* x, int x_dtype, long long ld_x, const float* w_gate_t,
+                   const void* w_split, const float* w_noise_t, const float* eps,
+                   const int32_t* exclude, int n_tokens, int d_model, int n_experts, int k,
+                   int quota, float* logits, int32_t* indices, float* weights, int32_t* slots,
+                   uint8_t* dropped, int32_t* counts, float* prob_sum, void* workspace,
+                   size_t workspace_bytes, void* stream) {
   SCMOE_CHECK_ARG(n_tokens >= 1, "n_tokens must be >= 1 (got %d)", n_tokens);
   SCMOE_CHECK_ARG(n_experts >= 1 && n_experts <= SCMOE_MAX_EXPERTS, "n_experts=%d out of [1,%d]",
                   n_experts, SCMOE_MAX_EXPERTS);
@@ -969,15 +1006,20 @@ extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
                   "gate workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)workspace;
-  if (x_dtype == SCMOE_BF16 && w_noise_t == nullptr && n_experts <= 16 && d_model >= 64 &&
-      !scmoe_gate_force_fma) {
+  const bool tc = x_dtype == SCMOE_BF16 && w_noise_t == nullptr && n_experts <= 16 &&
+                  d_model >= 64 && !scmoe_gate_force_fma;
+  SCMOE_CHECK_ARG(!w_split || tc, "a pre-split weight blob needs the tensor-core gate "
+                                  "(bf16 tokens, no noise, N <= 16, d >= 64)");
+  if (tc) {
     const int rc =
         n_experts <= 8
-            ? launch_gate_tc<1>(x, ld_x, w_gate_t, exclude, n_tokens, d_model, n_experts, k, quota,
-                                logits, indices, weights, slots, dropped, counts, prob_sum, ws, st)
-            : launch_gate_tc<2>(x, ld_x, w_gate_t, exclude, n_tokens, d_model, n_experts, k, quota,
-                                logits, indices, weights, slots, dropped, counts, prob_sum, ws, st);
-    if (rc != SCMOE_ERR_UNSUPPORTED) return rc;
+            ? launch_gate_tc<1>(x, ld_x, w_gate_t, w_split, exclude, n_tokens, d_model, n_experts,
+                                k, quota, logits, indices, weights, slots, dropped, counts,
+                                prob_sum, ws, st)
+            : launch_gate_tc<2>(x, ld_x, w_gate_t, w_split, exclude, n_tokens, d_model, n_experts,
+                                k, quota, logits, indices, weights, slots, dropped, counts,
+                                prob_sum, ws, st);
+    if (rc != SCMOE_ERR_UNSUPPORTED) return rc;   // very large T: the FMA kernel below
   }
   if (x_dtype == SCMOE_BF16)
     return dispatch_nmax<__nv_bfloat16>(x, ld_x, w_gate_t, w_noise_t, eps, exclude, n_tokens,
@@ -986,4 +1028,61 @@ extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
   return dispatch_nmax<float>(x, ld_x, w_gate_t, w_noise_t, eps, exclude, n_tokens, d_model,
                               n_experts, k, quota, logits, indices, weights, slots, dropped,
                               counts, prob_sum, ws, st);
+}
+}  // namespace
+}  // namespace scmoe
+
+extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
+                               const float* w_gate_t, const float* w_noise_t, const float* eps,
+                               const int32_t* exclude,
+                               int n_tokens, int d_model, int n_experts, int k, int quota,
+                               float* logits, int32_t* indices, float* weights, int32_t* slots,
+                               uint8_t* dropped, int32_t* counts, float* prob_sum,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  return scmoe::gate_topk_impl(x, x_dtype, ld_x, w_gate_t, nullptr, w_noise_t, eps, exclude,
+                               n_tokens, d_model, n_experts, k, quota, logits, indices, weights,
+                               slots, dropped, counts, prob_sum, workspace, workspace_bytes,
+                               stream);
+}
+
+extern "C" size_t scmoe_gate_split_bytes(int n_experts, int d_model) {
+  if (n_experts < 1 || n_experts > 16 || d_model < 64) return 0;
+  return (size_t)((d_model + 63) / 64) * ((n_experts + 7) / 8) * scmoe::GT_GROUP_B;
+}
+
+extern "C" int scmoe_gate_split_weights(const float* w_gate_t, int n_experts, int d_model,
+                                        void* blob, void* stream) {
+  using namespace scmoe;
+  SCMOE_CHECK_ARG(scmoe_gate_split_bytes(n_experts, d_model) > 0,
+                  "the tensor-core gate needs N <= 16 and d >= 64");
+  SCMOE_CHECK_ARG(d_model % 8 == 0 && w_gate_t && blob && ((uintptr_t)blob & 15) == 0,
+                  "bad arguments");
+  const int ngrp = (d_model + 63) / 64;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_experts <= 8) {
+    const int total = ngrp * 128;
+    gate_split_weights_kernel<1><<<(total + 255) / 256, 256, 0, st>>>(w_gate_t, d_model,
+                                                                      n_experts, ngrp,
+                                                                      (uint2*)blob);
+  } else {
+    const int total = ngrp * 2 * 128;
+    gate_split_weights_kernel<2><<<(total + 255) / 256, 256, 0, st>>>(w_gate_t, d_model,
+                                                                      n_experts, ngrp,
+                                                                      (uint2*)blob);
+  }
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld_x,
+                                        const float* w_gate_t, const void* w_split,
+                                        const int32_t* exclude, int n_tokens, int d_model,
+                                        int n_experts, int k, int quota, float* logits,
+                                        int32_t* indices, float* weights, int32_t* slots,
+                                        uint8_t* dropped, int32_t* counts, float* prob_sum,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  return scmoe::gate_topk_impl(x, x_dtype, ld_x, w_gate_t, w_split, nullptr, nullptr, exclude,
+                               n_tokens, d_model, n_experts, k, quota, logits, indices, weights,
+                               slots, dropped, counts, prob_sum, workspace, workspace_bytes,
+                               stream);
 }

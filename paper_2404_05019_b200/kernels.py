@@ -41,10 +41,25 @@ class GateOut:
     quota: int
 
 
+def gate_split_weights(w_gate_t: torch.Tensor, stream=None) -> Optional[torch.Tensor]:
+    """3-part bf16 split of the fp32 gate weights for the tensor-core gate, or
+    None when that path does not apply (N > 16 or d < 64)."""
+    N, d = w_gate_t.shape
+    nbytes = lib().scmoe_gate_split_bytes(N, d)
+    if nbytes == 0:
+        return None
+    blob = torch.empty(nbytes, device=w_gate_t.device, dtype=torch.uint8)
+    check(lib().scmoe_gate_split_weights(ptr(_c(w_gate_t, "w_gate_t")), N, d, ptr(blob),
+                                         stream_ptr(stream)))
+    return blob
+
+
 def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
               w_noise_t: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
-              exclude: Optional[torch.Tensor] = None, stream=None) -> GateOut:
-    """K1/K1b: logits, top-k, masked-softmax weights and capacity slots."""
+              exclude: Optional[torch.Tensor] = None, w_split: Optional[torch.Tensor] = None,
+              stream=None) -> GateOut:
+    """K1/K1b: logits, top-k, masked-softmax weights and capacity slots.
+    `w_split` (from gate_split_weights) skips the per-call weight split."""
     ensure_device(x)
     if x.dim() != 2 or x.stride(1) != 1:
         raise ValueError("x must be a row-major (T, d) matrix")
@@ -66,11 +81,18 @@ def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
         eps = _c(eps.to(torch.float32), "eps")
     if exclude is not None:
         exclude = _c(exclude.to(torch.int32).reshape(-1), "exclude")
-    check(lib().scmoe_gate_topk(
-        ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")),
-        ptr(w_noise_t), ptr(eps), ptr(exclude), T, d, N, k, quota,
-        ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
-        ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
+    if w_split is not None and w_noise_t is None:
+        check(lib().scmoe_gate_topk_presplit(
+            ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")), ptr(w_split),
+            ptr(exclude), T, d, N, k, quota,
+            ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
+            ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
+    else:
+        check(lib().scmoe_gate_topk(
+            ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")),
+            ptr(w_noise_t), ptr(eps), ptr(exclude), T, d, N, k, quota,
+            ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
+            ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
     return GateOut(logits, indices, weights, slots, dropped, counts, prob_sum, quota)
 
 

@@ -172,6 +172,22 @@ class Top1Gate(nn.Module):
     def quota(self, n_tokens: int) -> int:
         return K.expert_quota(self.capacity.capacity_factor, n_tokens, self.k, self.n_experts)
 
+    def presplit(self, x_src: torch.Tensor) -> Optional[torch.Tensor]:
+        """Inference only: the tensor-core gate's split weights, cached per
+        weight version (in-place updates bump `_version`).  A CUDA graph
+        captured with a valid cache replays with that split, so weights must
+        not change between replays of such a graph (training steps — grad
+        mode — always split inside the call)."""
+        w = self.w_gate_t
+        if (torch.is_grad_enabled() or self.noise_enabled or x_src.dtype != torch.bfloat16
+                or w.requires_grad):
+            return None
+        key = (w.data_ptr(), w._version)
+        if getattr(self, "_split_key", None) != key:
+            self._split = K.gate_split_weights(w)
+            self._split_key = key
+        return self._split
+
     def forward(self, x_src: torch.Tensor, eps: Optional[torch.Tensor] = None,
                 generator: Optional[torch.Generator] = None, replay: Optional[MoEReplay] = None,
                 stream=None) -> GateDecision:
@@ -187,7 +203,8 @@ class Top1Gate(nn.Module):
         quota = self.quota(t)
         g = K.gate_topk(x_src, self.w_gate_t, self.k, quota,
                         w_noise_t=self.w_noise_t if self.noise_enabled else None,
-                        eps=eps if self.noise_enabled else None, stream=stream)
+                        eps=eps if self.noise_enabled else None,
+                        w_split=self.presplit(x_src), stream=stream)
         dec = GateDecision(g.logits, g.indices, g.weights, g.dropped.bool(), g.slots, g.counts,
                            g.prob_sum, quota, quota, eps if self.noise_enabled else None)
         if replay is not None and replay.indices is not None:

@@ -269,3 +269,30 @@ def test_pack_heads_matches_torch():
     assert torch.equal(out, ref)
     one = K.pack_heads([srcs[1]])
     assert torch.equal(one[:, :, 0], srcs[1].transpose(1, 2))
+
+
+def test_gate_presplit_equals_per_call_split():
+    """scmoe_gate_topk_presplit with a cached weight split gives the same
+    decision as the per-call split; Top1Gate re-splits after an in-place
+    weight update (weight version changes)."""
+    import paper_2404_05019_b200 as P
+    T, d, N = 3000, 512, 8
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    w = torch.randn(N, d, device="cuda") / d ** 0.5
+    quota = K.expert_quota(1.0, T, 1, N)
+    a = K.gate_topk(x, w, 1, quota)
+    b = K.gate_topk(x, w, 1, quota, w_split=K.gate_split_weights(w))
+    torch.cuda.synchronize()
+    for f in ("logits", "indices", "slots", "dropped", "counts", "weights"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
+    gate = P.Top1Gate(d, N, capacity_factor=1.0)
+    with torch.no_grad():
+        d1 = gate(x)
+        s1 = gate._split
+        gate.w_gate_t.mul_(-1.0)                 # in-place update: new version
+        d2 = gate(x)
+    assert gate._split is not s1
+    ref = K.gate_topk(x, gate.w_gate_t, 1, quota)
+    torch.cuda.synchronize()
+    assert torch.equal(d2.indices, ref.indices) and torch.equal(d2.slots, ref.slots)
+    assert not torch.equal(d1.indices, d2.indices)
