@@ -222,6 +222,22 @@ int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const float* b1,
                      int d_model, int d_hidden, void* stream);
 
 /*
+ * K4+K5 fused (inference, direct-add combine): the shared expert on x_cur
+ * whose GEMM2 epilogue also gathers the routed rows and the residual:
+ *   out[t] = bf16(SE(x_cur)[t]) + sum_j w[t,j] * expert_out[idx[t,j], slot[t,j]]
+ *            (+ residual[t]),   selections with slot >= capacity skipped,
+ * bit-identical to scmoe_expert_ffn followed by scmoe_combine (same fp32
+ * operation order) without the SE output round trip or the combine launch.
+ * bf16, one group of n_tokens rows, k <= 2.  hidden: (n_tokens, d_hidden).
+ */
+int scmoe_shared_ffn_combine(const void* x, int dtype, const void* w1t, const float* b1,
+                             const void* w2t, const float* b2, const void* residual,
+                             const void* expert_out, const int32_t* indices,
+                             const int32_t* slots, const float* weights, int capacity, int k,
+                             void* hidden, void* out, int n_tokens, int d_model, int d_hidden,
+                             void* stream);
+
+/*
  * K5 — combine ("decode") + combination gate + optional residual:
  *   routed[t] = sum_j (slots[t,j] < capacity) * weights[t,j] * expert_out[indices[t,j], slots[t,j], :]
  *   direct_add: f = se + routed; cg1: f = sigmoid(x_cur.w_cg[0]) * se + routed;

@@ -61,6 +61,8 @@ SIGNATURES = [
     ("scmoe_ep_signal", _i, [_vp, _i, _i, _i, _vp, _vp]),
     ("scmoe_ep_combine_p2p", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                                   _i, _i, _i, _vp, _vp]),
+    ("scmoe_shared_ffn_combine", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                      _i, _i, _vp, _vp, _i, _i, _i, _vp]),
     ("scmoe_pack_heads", _i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     ("scmoe_ep_return_p2p", _i, [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
 ]

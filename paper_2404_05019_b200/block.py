@@ -472,10 +472,22 @@ class ScMoEBlockPair(nn.Module):
                 env["y"] = moe.experts(env["buf"], rows, dec.capacity)
 
         def shared():
+            dec = env.get("dec")
+            if ("y" in env and not train and not use_ep and chunks == 1 and off is None
+                    and self.variant in ("scmoe", "shared")
+                    and moe.shared.can_fuse_combine(env["x_cur"], dec, moe.combine_mode)):
+                # the routed rows are ready: the combine (+ the block residual)
+                # runs in the shared expert's GEMM2 epilogue; decode is a no-op
+                env["out"] = moe.shared.forward_combine(env["x_cur"], env["y"], dec,
+                                                        residual=env["h_mh_cur"])
+                env["fused"] = True
+                return
             env["se"] = moe.shared(env["x_cur"])
 
         def decode():
             dec = env["dec"]
+            if env.get("fused"):
+                return
             if chunks > 1:
                 return decode_chunked()
             if train:

@@ -30,7 +30,8 @@ int num_sms() {
 int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias,
                       const void* residual, const void* aux_in, void* aux_out, void* out,
                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st);
+                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st,
+                      const CombineSpec* cs = nullptr);
 int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const float* residual,
                      float* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st);
@@ -213,6 +214,25 @@ extern "C" int scmoe_expert_ffn(const void* x, int dtype, const void* w1t, const
   return scmoe_grouped_gemm(hidden, dtype, w2t, b2, residual, out, num_groups, n_wgroups,
                             group_cap, group_rows, rows_clip, d_model, d_hidden, SCMOE_EPI_BIAS,
                             stream);
+}
+
+extern "C" int scmoe_shared_ffn_combine(const void* x, int dtype, const void* w1t,
+                                        const float* b1, const void* w2t, const float* b2,
+                                        const void* residual, const void* expert_out,
+                                        const int32_t* indices, const int32_t* slots,
+                                        const float* weights, int capacity, int k, void* hidden,
+                                        void* out, int n_tokens, int d_model, int d_hidden,
+                                        void* stream) {
+  using namespace scmoe;
+  SCMOE_CHECK_ARG(dtype == SCMOE_BF16, "the fused combine runs on bf16");
+  SCMOE_CHECK_ARG(k >= 1 && k <= 2 && capacity >= 1, "fused combine: k <= 2");
+  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, 1, 1, n_tokens, nullptr,
+                              n_tokens, d_hidden, d_model, SCMOE_EPI_BIAS_GELU, stream);
+  if (rc) return rc;
+  const CombineSpec cs{expert_out, indices, slots, weights, capacity, k};
+  return grouped_gemm_bf16(hidden, w2t, 0, b2, residual, nullptr, nullptr, out, 1, 1, n_tokens,
+                           nullptr, n_tokens, d_model, d_hidden, SCMOE_EPI_BIAS, 0,
+                           (cudaStream_t)stream, &cs);
 }
 
 extern "C" size_t scmoe_grouped_wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out,

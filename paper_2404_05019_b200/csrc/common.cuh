@@ -42,6 +42,16 @@ void set_error(const char* fmt, ...);
 
 int num_sms();
 
+// Fused ScMoE combine in the shared expert's GEMM2 epilogue (direct add):
+// y is the routed experts' (E, capacity, d) output.
+struct CombineSpec {
+  const void* y;
+  const int32_t* indices;
+  const int32_t* slots;
+  const float* weights;
+  int capacity, k;
+};
+
 // ---- element access ---------------------------------------------------------
 
 __device__ __forceinline__ float to_f32(float v) { return v; }

@@ -82,6 +82,13 @@ struct Params {
   __nv_bfloat16* aux_out;                  // forward: store the pre-activation
   __nv_bfloat16* out;
   float* out_f32;                          // wgrad partials [splits][W][m_out][N]
+  // fused ScMoE combine (direct add) in the shared expert's GEMM2 epilogue:
+  // out[t] = bf16(acc + b2) + sum_j w_j * cy[c_idx[t,j], c_slot[t,j]] (+ residual)
+  const __nv_bfloat16* cy;
+  const int32_t* c_idx;
+  const int32_t* c_slot;
+  const float* c_w;
+  int c_cap, c_k;                          // c_k = 0: off
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -287,7 +294,9 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc,
 // or zeros for padding rows
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
                                                bool row_ok, bool pad_row, long long row_off,
-                                               int n, const float* sb) {
+                                               int n, const float* sb,
+                                               const __nv_bfloat16* cy0 = nullptr, float cw0 = 0.f,
+                                               const __nv_bfloat16* cy1 = nullptr, float cw1 = 0.f) {
   if (n >= p.N || !(row_ok || pad_row)) return;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -322,6 +331,36 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
         zv.to_float(z);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(z[i]);
+      }
+      if (p.c_k) {
+        // the ScMoE combine, same fp32 sequence as combine_kernel: shared
+        // expert row rounded to bf16, routed rows fmaf-accumulated in
+        // selection order, then se + routed, then + residual
+        Vec16<__nv_bfloat16> sev;
+        sev.from_float(v);
+        float se[8], rt[8];
+        sev.to_float(se);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rt[i] = 0.f;
+        if (cy0) {
+          Vec16<__nv_bfloat16> yv;
+          yv.raw = ld_nc_v4(cy0 + nn);
+          float f[8];
+          yv.to_float(f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rt[i] = fmaf(cw0, f[i], rt[i]);
+        }
+        if (cy1) {
+          Vec16<__nv_bfloat16> yv;
+          yv.raw = ld_nc_v4(cy1 + nn);
+          float f[8];
+          yv.to_float(f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rt[i] = fmaf(cw1, f[i], rt[i]);
+        }
+        const float one = 1.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = one * se[i] + one * rt[i];
       }
       if (p.residual) {
         Vec16<__nv_bfloat16> rv;
@@ -549,6 +588,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         *reinterpret_cast<float4*>(sbw + 4 * lane) = b;
         __syncwarp();
       }
+      // fused combine: this row's (token's) routed rows, before the wait
+      const __nv_bfloat16* cy0 = nullptr;
+      const __nv_bfloat16* cy1 = nullptr;
+      float cw0 = 0.f, cw1 = 0.f;
+      if (!WGRAD && p.c_k && row_ok) {
+        const long long o = (long long)row * p.c_k;
+        const int s0 = p.c_slot[o];
+        if (s0 < p.c_cap) {
+          cy0 = p.cy + ((long long)p.c_idx[o] * p.c_cap + s0) * p.N;
+          cw0 = p.c_w[o];
+        }
+        if (p.c_k > 1) {
+          const int s1 = p.c_slot[o + 1];
+          if (s1 < p.c_cap) {
+            cy1 = p.cy + ((long long)p.c_idx[o + 1] * p.c_cap + s1) * p.N;
+            cw1 = p.c_w[o + 1];
+          }
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       // TMEM -> registers in 4 chunks of 32 columns, chunk c+1's tcgen05.ld in
@@ -564,7 +622,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
         const int n = tc.n0 + half * 128 + c * 32;
         if (WGRAD) epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
-        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr);
+        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
+                            cy0, cw0, cy1, cw1);
         if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == 2) {
           // the whole accumulator is in registers: hand TMEM back to the MMA warp
@@ -684,7 +743,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias,
                       const void* residual, const void* aux_in, void* aux_out, void* out,
                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st) {
+                      int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st,
+                      const CombineSpec* cs) {
   using namespace sm100;
   SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
   SCMOE_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "bf16 GEMM needs k_in and n_out multiples of 8");
@@ -707,6 +767,18 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   p.aux_in = (const __nv_bfloat16*)aux_in;
   p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
+  if (cs) {
+    SCMOE_CHECK_ARG(num_groups == 1 && epi == EPI_BIAS && cs->k >= 1 && cs->k <= 2 && cs->y &&
+                        cs->indices && cs->slots && cs->weights && cs->capacity >= 1 &&
+                        aligned16(cs->y),
+                    "fused combine: one group, bias epilogue, k <= 2");
+    p.cy = (const __nv_bfloat16*)cs->y;
+    p.c_idx = cs->indices;
+    p.c_slot = cs->slots;
+    p.c_w = cs->weights;
+    p.c_cap = cs->capacity;
+    p.c_k = cs->k;
+  }
   const int sms = num_sms();
   const long long n_tiles_n = (N + BN - 1) / BN;
   const long long tiles_2sm = (long long)num_groups * ((cap + 255) / 256) * n_tiles_n;

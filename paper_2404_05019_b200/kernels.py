@@ -344,3 +344,26 @@ def pack_heads(srcs, out: Optional[torch.Tensor] = None, stream=None) -> torch.T
                                  ctypes.cast(strides, ctypes.c_void_p), n, b, h, s, hd,
                                  _lib.SCMOE_BF16, ptr(out), stream_ptr(stream)))
     return out
+
+
+def shared_ffn_combine(x: torch.Tensor, w1t: torch.Tensor, b1: torch.Tensor, w2t: torch.Tensor,
+                       b2: torch.Tensor, expert_out: torch.Tensor, indices: torch.Tensor,
+                       slots: torch.Tensor, weights: torch.Tensor, capacity: int,
+                       residual: Optional[torch.Tensor] = None,
+                       out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Shared expert on x with the direct-add ScMoE combine fused into its
+    GEMM2 epilogue (scmoe_shared_ffn_combine): = combine(SE(x), routed) + res."""
+    ensure_device(x)
+    T, d = x.shape
+    h = w1t.shape[-2]
+    hidden = torch.empty(T, h, device=x.device, dtype=x.dtype)
+    if out is None:
+        out = torch.empty(T, d, device=x.device, dtype=x.dtype)
+    if residual is not None:
+        _c(residual, "residual")
+    check(lib().scmoe_shared_ffn_combine(
+        ptr(_c(x, "x")), dtype_code(x.dtype), ptr(_c(w1t, "w1t")), ptr(b1), ptr(_c(w2t, "w2t")),
+        ptr(b2), ptr(residual), ptr(_c(expert_out, "expert_out")), ptr(_c(indices, "indices")),
+        ptr(_c(slots, "slots")), ptr(_c(weights, "weights")), capacity, indices.shape[1],
+        ptr(hidden), ptr(out), T, d, h, stream_ptr(stream)))
+    return out

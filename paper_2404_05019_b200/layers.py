@@ -291,6 +291,22 @@ class SharedExpert(nn.Module):
         return K.expert_ffn(x, self.w1t, self.b1, self.w2t, self.b2, hidden=hidden, out=out,
                             residual=residual, stream=stream)
 
+    def forward_combine(self, x: torch.Tensor, expert_out: torch.Tensor, dec,
+                        residual: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Inference: SE(x) with the direct-add combine of the routed rows
+        (+ residual) fused into the second GEMM's epilogue — bit-identical to
+        forward() followed by the combine kernel."""
+        return K.shared_ffn_combine(x, self.w1t, self.b1, self.w2t, self.b2, expert_out,
+                                    dec.indices, dec.slots, dec.weights, dec.capacity,
+                                    residual=residual, stream=stream)
+
+    def can_fuse_combine(self, x: torch.Tensor, dec, combine_mode: str) -> bool:
+        return (combine_mode == "direct_add" and x.dtype == torch.bfloat16 and dec.k <= 2
+                and not torch.is_grad_enabled() and FUSED_COMBINE)
+
+
+FUSED_COMBINE = True     # SE GEMM2 epilogue does the direct-add combine (A/B switch)
+
 
 class RoutedExperts(nn.Module):
     """N stacked experts (E, h, d) / (E, d, h), evaluated only on the rows
@@ -518,6 +534,9 @@ class ScMoELayer(_RoutedMoE):
             return out, dec, aux
         dec = self.route(src, eps=eps, replay=replay, generator=generator)
         y = self.routed_experts(src, dec)
+        if self.shared.can_fuse_combine(x_cur, dec, self.combine_mode):
+            out = self.shared.forward_combine(x_cur, y, dec, residual=residual)
+            return out, dec, dec.aux_loss()
         se = self.shared(x_cur)
         out = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, se_out=se,
                         mode=self.combine_mode, x_cur=x_cur, w_cg=self.w_cg, residual=residual)

@@ -318,3 +318,33 @@ def test_every_block_training_step():
     for blk in model.blocks:
         for p in (blk.attn_cur.w_qkv_t, blk.moe.experts.w1t, blk.moe.shared.b2, blk.moe.gate.w_gate_t):
             assert p.grad is not None and torch.isfinite(p.grad.float()).all()
+
+
+@pytest.mark.parametrize("k,cf", [(1, 2.0), (1, 0.5), (2, 1.0)])
+def test_fused_shared_combine_bit_identical(k, cf):
+    """scmoe_shared_ffn_combine (combine in the SE GEMM2 epilogue) equals the
+    shared expert followed by the combine kernel bit for bit (drops included)."""
+    import paper_2404_05019_b200 as P
+    from paper_2404_05019_b200 import kernels as K, layers as L
+    T, d, h, N = 1000, 256, 512, 8
+    layer = P.ScMoELayer(d, h, N, k_routed=k, capacity_factor=cf, dtype=torch.bfloat16,
+                         generator=torch.Generator(device="cuda").manual_seed(4))
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    src = torch.randn(T, d, device="cuda").bfloat16()
+    res = torch.randn(T, d, device="cuda").bfloat16()
+    with torch.no_grad():
+        dec = layer.route(src)
+        y = layer.routed_experts(src, dec)
+        fused = layer.shared.forward_combine(x, y, dec, residual=res)
+        se = layer.shared(x)
+        ref = K.combine(y, dec.indices, dec.slots, dec.weights, dec.capacity, se_out=se,
+                        residual=res)
+        try:
+            L.FUSED_COMBINE = False
+            unfused_layer = layer(x, src, residual=res)[0]
+        finally:
+            L.FUSED_COMBINE = True
+        fused_layer = layer(x, src, residual=res)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(fused, ref)
+    assert torch.equal(fused_layer, unfused_layer)
