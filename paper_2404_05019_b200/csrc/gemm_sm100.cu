@@ -121,6 +121,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
+// Accumulator release from the epilogue: the TMEM reads are ordered by
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync; the arrive itself needs
+// no cluster-scope release of the epilogue's global stores (that compiled to a
+// MEMBAR.ALL.GPU per warp per tile, draining every output store before the
+// MMA warp could reuse the accumulator — the small-K limiter).
+__device__ __forceinline__ void mbar_arrive_cluster_tmem(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -630,7 +640,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (TWO_SM) mbar_arrive_cluster(&tempty_bar[acc], 0);
+            if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
             else mbar_arrive(&tempty_bar[acc]);
           }
         }
