@@ -6,6 +6,9 @@ import torch
 from paper_2404_05019_b200 import kernels as K
 shapes = [("ffn1 16384x2048->8192", 16384, 2048, 8192), ("ffn2 16384x8192->2048", 16384, 8192, 2048),
           ("qkv 16384x2048->6144", 16384, 2048, 6144)]
+if len(sys.argv) > 1 and sys.argv[1] == "train":      # configs[1] (d 384, h 1536) shapes
+    shapes = [("ffn1 18432x384->1536", 18432, 384, 1536), ("ffn2 18432x1536->384", 18432, 1536, 384),
+              ("qkv 18432x384->1152", 18432, 384, 1152), ("o 18432x384->384", 18432, 384, 384)]
 res = {}
 for name, M, Kd, N in shapes:
     a = torch.randn(M, Kd, device="cuda").bfloat16()
