@@ -56,3 +56,44 @@ def test_from_reference_layout():
     np.testing.assert_allclose(m.shared.w2t.numpy(), pp.moe.shared.w2.T, rtol=1e-6)
     np.testing.assert_allclose(m.gate.w_gate_t.numpy(), pp.moe.gate.w_gate.T, rtol=1e-6)
     np.testing.assert_allclose(m.w_cg.numpy(), pp.moe.w_cg, rtol=1e-6)
+
+
+def test_peer_exchange_layout_and_tables():
+    """p2p EP host logic (no GPU): buffer layout is 256-byte aligned in the
+    order recv | y | back | recv_counts | flags, and every peer-table row is
+    the peer's base plus that buffer's offset."""
+    from paper_2404_05019_b200.ep_p2p import PeerExchange
+    world, e_l, cap, d = 4, 2, 100, 64
+    sizes, offs, total = PeerExchange.layout(world, e_l, cap, d, torch.bfloat16)
+    G = world * e_l
+    assert sizes == [G * cap * d * 2] * 3 + [G * 4, 2 * world * 4]
+    assert all(o % 256 == 0 for o in offs) and offs == sorted(offs) and total >= offs[-1] + sizes[-1]
+    x = PeerExchange(world, 1, e_l, cap, d, torch.bfloat16, "cpu")
+    assert x.recv.shape == x.y.shape == x.back.shape == (G, cap, d)
+    assert x.flags.numel() == 2 * world and x.epoch.numel() == 4
+    bases = [1 << 40, 2 << 40, 3 << 40, 4 << 40]
+    x.set_peer_bases(bases)
+    for i, o in enumerate(offs):
+        assert x.tables[i].tolist() == [b + o for b in bases]
+    with pytest.raises(ValueError):
+        x.set_peer_bases(bases[:2])
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """The driver contract: stdout carries exactly one JSON line (fd 1 is
+    redirected to stderr for the run, so native banners cannot interleave)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--workload", "swinv2s", "--steps", "1", "--warmup", "0",
+                        "--ref-tokens", "16"], capture_output=True, text=True, timeout=600,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
