@@ -348,3 +348,46 @@ def test_fused_shared_combine_bit_identical(k, cf):
     torch.cuda.synchronize()
     assert torch.equal(fused, ref)
     assert torch.equal(fused_layer, unfused_layer)
+
+
+def _reference_package():
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref = os.path.join(root, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "scmoelab")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from scmoelab import arch, gating, numkit
+    return arch, gating, numkit
+
+
+@pytest.mark.parametrize("variant,pos,mode,freq", [
+    ("scmoe", "pos2", "cg1", "every-second-block"), ("scmoe", "pos1", "direct_add", "every-block"),
+    ("standard", None, "direct_add", "every-second-block")])
+def test_compat_drives_the_real_reference_model(variant, pos, mode, freq):
+    """The unmodified reference (scmoelab, installed offline in baseline/_ref)
+    runs its own arch.forward with compat.install() routing every MoE layer
+    through our kernels; the result equals the reference's numpy forward
+    replaying the GPU's routing decisions (fp32, rtol 1e-4)."""
+    pkg = _reference_package()
+    if pkg is None:
+        pytest.skip("baseline/_ref (the installed reference) is not present")
+    arch, gating, numkit = pkg
+    from paper_2404_05019_b200 import compat
+    n_blocks = 2 if freq == "every-second-block" else 3
+    cfg = arch.ModelConfig(n_blocks=n_blocks, d_model=64, d_hidden=128, n_experts=4,
+                           k_routed=1 if variant == "scmoe" else 2, moe_frequency=freq,
+                           variant=variant, shortcut_pos=pos, combine_mode=mode,
+                           capacity_factor=1.0)
+    params = arch.init_params(cfg, numkit.Rng(3))
+    tokens = numkit.Rng(4).normal((96, 64))
+    compat.install(dtype=torch.float32)
+    try:
+        gpu_out, gpu_trace = arch.forward(cfg, params, tokens)
+    finally:
+        compat.uninstall()
+    assert arch.moe_shared.__module__.startswith("scmoelab")
+    ref_out, _ = arch.forward(cfg, params, tokens, replay=arch.replay_from_trace(gpu_trace))
+    _check(gpu_out, ref_out, 1e-4, "reference arch.forward through compat")
