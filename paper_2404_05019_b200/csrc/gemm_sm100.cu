@@ -387,6 +387,39 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
   }
 }
 
+// Fast epilogue for the common forward cases (no residual / aux / fused
+// combine): bias and GELU are compile-time, the chunk is known to be in range,
+// so the 32 values run as straight-line code — the general epilogue_chunk is
+// latency-bound on per-element checks with only 8 epilogue warps per SM.
+template <bool BIAS, bool GELU>
+__device__ __forceinline__ void epilogue_chunk_fast(const uint32_t (&r)[32], bool row_ok,
+                                                    __nv_bfloat16* __restrict__ dst,
+                                                    const float* __restrict__ sb) {
+  if (!row_ok) return;
+  uint4 o[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
+    if (BIAS) {
+      const float4 b0 = *reinterpret_cast<const float4*>(sb + u * 8);
+      const float4 b1 = *reinterpret_cast<const float4*>(sb + u * 8 + 4);
+      v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+      v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+    }
+    if (GELU) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
+    }
+    Vec16<__nv_bfloat16> w;
+    w.from_float(v);
+    o[u] = w.raw;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) st_v4(dst + u * 8, o[u]);
+}
+
 // fp32 wgrad partial: 32 columns of one output row
 __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32_t (&r)[32],
                                                    bool row_ok, bool zero, long long row_off,
@@ -565,6 +598,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ew = warp - 4;
     const int quad = warp & 3;   // TMEM lanes [32*quad, 32*quad+32)
     const int half = ew >> 2;    // accumulator columns [128*half, 128*half+128)
+    // the fast epilogue covers bias / bias+GELU stores without residual,
+    // pre-activation / GELU-backward operands, zero tails or the fused combine
+    const bool fast = !WGRAD && !p.residual && !p.aux_out && !p.aux_in && !p.c_k &&
+                      !p.zero_tail && (p.epi == EPI_BIAS || p.epi == EPI_BIAS_GELU);
+    const bool fast_gelu = p.epi == EPI_BIAS_GELU;
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
       const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
@@ -631,9 +669,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
         if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
         const int n = tc.n0 + half * 128 + c * 32;
-        if (WGRAD) epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
-        else epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
-                            cy0, cw0, cy1, cw1);
+        if (WGRAD) {
+          epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
+        } else if (fast && n + 32 <= p.N) {
+          __nv_bfloat16* dst = p.out + row_off + n;
+          const float* sb = brow ? sbw + c * 32 : nullptr;
+          if (fast_gelu) {
+            if (sb) epilogue_chunk_fast<true, true>(cur, row_ok, dst, sb);
+            else epilogue_chunk_fast<false, true>(cur, row_ok, dst, sb);
+          } else {
+            if (sb) epilogue_chunk_fast<true, false>(cur, row_ok, dst, sb);
+            else epilogue_chunk_fast<false, false>(cur, row_ok, dst, sb);
+          }
+        } else {
+          epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
+                         cy0, cw0, cy1, cw1);
+        }
         if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == 2) {
           // the whole accumulator is in registers: hand TMEM back to the MMA warp
