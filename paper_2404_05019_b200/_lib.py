@@ -14,7 +14,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscmoe.so")
+# SCMOE_LIB overrides the library path (A/B of two builds in one session)
+LIB_PATH = os.environ.get("SCMOE_LIB") or os.path.join(_HERE, "libscmoe.so")
 
 SCMOE_OK, SCMOE_ERR_ARG, SCMOE_ERR_CUDA, SCMOE_ERR_UNSUPPORTED = 0, 1, 2, 3
 SCMOE_F32, SCMOE_BF16 = 0, 1
