@@ -108,7 +108,7 @@ class PeerExchange:
 
     @classmethod
     def from_group(cls, group, e_local: int, capacity: int, d_model: int, dtype, device,
-                   method: str = "ipc"):
+                   method: str = "auto"):
         """Peer-mapped storage over a process group.  Allocation and handle
         exchange only — every byte of the exchange is moved by our kernels.
 
@@ -117,9 +117,31 @@ class PeerExchange:
         with lazy peer access) travel through the group as objects, and every
         rank maps every peer's storage.  Works across the GPUs of a node
         (NVLink peer access) and across processes sharing one GPU.
-        method "symm": torch symmetric memory (one GPU per rank only)."""
+        method "symm": torch symmetric memory (one GPU per rank only; one
+        mapping per peer without a CUDA context per peer device).
+        method "auto": "symm" when every rank can rendezvous, else "ipc"
+        (e.g. ranks sharing a GPU).  The choice is agreed over the group."""
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if method == "auto":
+            ok = 1
+            try:
+                import torch.distributed._symmetric_memory  # noqa: F401
+            except Exception:
+                ok = 0
+            flags = [None] * world
+            dist.all_gather_object(flags, ok, group=group)
+            if all(flags):
+                try:
+                    x = cls.from_group(group, e_local, capacity, d_model, dtype, device,
+                                       method="symm")
+                    ok = 1
+                except Exception:   # e.g. two ranks on one device
+                    x, ok = None, 0
+                dist.all_gather_object(flags, ok, group=group)
+                if all(flags):      # every rank mapped every peer: agreed
+                    return x
+            method = "ipc"
         if method == "symm":
             import torch.distributed._symmetric_memory as symm_mem
             nbytes = cls.layout(world, e_local, capacity, d_model, dtype)[2]
