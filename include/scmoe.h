@@ -298,6 +298,17 @@ int scmoe_ep_combine_p2p(const void* se_out, const void* const* peer_y, const vo
                          const int32_t* indices, const int32_t* slots, const float* weights,
                          int capacity, int n_tokens, int d_model, int k, int dtype, int world,
                          int rank, int experts_per_rank, void* out, void* stream);
+/* Expert-parallel return fused into the expert FFN (one kernel does the
+ * GEMM and the transfer): scmoe_expert_ffn whose GEMM2 epilogue stores the
+ * rows of group g to out_group_ptrs[g] + row * d_model (a DEVICE array of
+ * num_groups pointers — on the owner rank, group (src, el) points into the
+ * source's back buffer over peer memory), tile by tile, then fences at
+ * system scope; follow with scmoe_ep_signal(which 1). */
+int scmoe_expert_ffn_to_peers(const void* x, int dtype, const void* w1t, const float* b1,
+                              const void* w2t, const float* b2, void* hidden,
+                              void* const* out_group_ptrs, int num_groups, int n_wgroups,
+                              int group_cap, const int32_t* group_rows, int rows_clip,
+                              int d_model, int d_hidden, void* stream);
 int scmoe_ep_return_p2p(const void* y, int dtype, const int32_t* recv_counts, int capacity,
                         int d_model, int world, int rank, int experts_per_rank,
                         void* const* peer_back, uint32_t* const* peer_flags, uint32_t* epoch_ctr,

@@ -167,7 +167,8 @@ class ScMoEBlockPair(nn.Module):
                  noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
                  seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
                  device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True,
-                 chunks: int = 1, ep_backend: str = "nccl", p2p_ctas: int = 32):
+                 chunks: int = 1, ep_backend: str = "nccl", p2p_ctas: int = 32,
+                 p2p_return: str = "fused"):
         super().__init__()
         if chunks < 1:
             raise ConfigError("chunks must be >= 1")
@@ -177,7 +178,12 @@ class ScMoEBlockPair(nn.Module):
         # "nccl": all-to-all of the capacity buffers (ep.py); "p2p": our kernels
         # move only kept rows over peer memory (ep_p2p.py); p2p_ctas bounds the
         # side-stream copy kernels' grids so they run beside the window ops
-        self.ep_backend, self.p2p_ctas = ep_backend, p2p_ctas
+        if p2p_return not in ("fused", "push"):
+            raise ConfigError(f"unknown p2p_return {p2p_return!r}")
+        # p2p return trip: "fused" — the owner's GEMM2 epilogue stores rows into
+        # the sources' back buffers over peer memory, tile by tile; "push" — a
+        # separate copy kernel on the comm stream after the FFN
+        self.ep_backend, self.p2p_ctas, self.p2p_return = ep_backend, p2p_ctas, p2p_return
         self._xchg = None
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
@@ -452,6 +458,10 @@ class ScMoEBlockPair(nn.Module):
             if p2p:
                 xg = self._xchg
                 st.wait_event(env["disp_ev"])
+                if self.p2p_return == "fused":
+                    xg.expert_ffn_to_peers(moe.experts, stream=st)
+                    env["y_ev"] = None
+                    return
                 xg.expert_ffn(moe.experts, signal=False, stream=st)
                 cs.wait_stream(st)
                 with rec.op("combine", "comm", cs):
@@ -497,7 +507,7 @@ class ScMoEBlockPair(nn.Module):
                     None if std else moe.w_cg, env["h_mh_cur"], dec.indices, dec.slots, env["kept"],
                     dec.capacity, "direct_add" if std else moe.combine_mode)
                 return
-            if use_ep:
+            if use_ep and env.get("y_ev") is not None:
                 st.wait_event(env["y_ev"])
             if p2p:
                 xg = self._xchg

@@ -31,7 +31,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
                       const void* residual, const void* aux_in, void* aux_out, void* out,
                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                       int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st,
-                      const CombineSpec* cs = nullptr);
+                      const CombineSpec* cs = nullptr, void* const* out_groups = nullptr);
 int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const float* residual,
                      float* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st);
@@ -233,6 +233,25 @@ extern "C" int scmoe_shared_ffn_combine(const void* x, int dtype, const void* w1
   return grouped_gemm_bf16(hidden, w2t, 0, b2, residual, nullptr, nullptr, out, 1, 1, n_tokens,
                            nullptr, n_tokens, d_model, d_hidden, SCMOE_EPI_BIAS, 0,
                            (cudaStream_t)stream, &cs);
+}
+
+extern "C" int scmoe_expert_ffn_to_peers(const void* x, int dtype, const void* w1t,
+                                         const float* b1, const void* w2t, const float* b2,
+                                         void* hidden, void* const* out_group_ptrs,
+                                         int num_groups, int n_wgroups, int group_cap,
+                                         const int32_t* group_rows, int rows_clip, int d_model,
+                                         int d_hidden, void* stream) {
+  using namespace scmoe;
+  SCMOE_CHECK_ARG(dtype == SCMOE_BF16 && out_group_ptrs, "bf16 with an output-group table");
+  if (rows_clip <= 0) rows_clip = group_cap;
+  int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, num_groups, n_wgroups,
+                              group_cap, group_rows, rows_clip, d_hidden, d_model,
+                              SCMOE_EPI_BIAS_GELU, stream);
+  if (rc) return rc;
+  // out is only the shape reference; every row goes through out_group_ptrs
+  return grouped_gemm_bf16(hidden, w2t, 0, b2, nullptr, nullptr, nullptr, hidden, num_groups,
+                           n_wgroups, group_cap, group_rows, rows_clip, d_model, d_hidden,
+                           SCMOE_EPI_BIAS, 0, (cudaStream_t)stream, nullptr, out_group_ptrs);
 }
 
 extern "C" size_t scmoe_grouped_wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out,

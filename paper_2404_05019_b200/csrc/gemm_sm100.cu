@@ -89,6 +89,9 @@ struct Params {
   const int32_t* c_slot;
   const float* c_w;
   int c_cap, c_k;                          // c_k = 0: off
+  // per-group output base (expert-parallel return fused into GEMM2): group g's
+  // rows go to out_groups[g] + row * N (peer memory), nullptr: out + g*cap*N
+  __nv_bfloat16* const* out_groups;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -304,7 +307,7 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc,
 // or zeros for padding rows
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
                                                bool row_ok, bool pad_row, long long row_off,
-                                               int n, const float* sb,
+                                               __nv_bfloat16* orow, int n, const float* sb,
                                                const __nv_bfloat16* cy0 = nullptr, float cw0 = 0.f,
                                                const __nv_bfloat16* cy1 = nullptr, float cw1 = 0.f) {
   if (n >= p.N || !(row_ok || pad_row)) return;
@@ -313,7 +316,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
     const int nn = n + u * 8;
     if (nn < p.N) {
       if (!row_ok) {
-        st_v4(p.out + row_off + nn, make_uint4(0, 0, 0, 0));
+        st_v4(orow + nn, make_uint4(0, 0, 0, 0));
         if (p.aux_out) st_v4(p.aux_out + row_off + nn, make_uint4(0, 0, 0, 0));
         continue;
       }
@@ -382,7 +385,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
       }
       Vec16<__nv_bfloat16> o;
       o.from_float(v);
-      st_v4(p.out + row_off + nn, o.raw);
+      st_v4(orow + nn, o.raw);
     }
   }
 }
@@ -611,6 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
       bool row_ok, pad_row = false;
       long long row_off;
+      __nv_bfloat16* orow = nullptr;
       const float* brow = nullptr;
       if (WGRAD) {
         row_ok = row < p.m_out;
@@ -620,6 +624,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         row_ok = row < rows;
         pad_row = p.zero_tail && row < p.cap;
         row_off = ((long long)tc.g * p.cap + row) * p.N;
+        orow = p.out_groups ? p.out_groups[tc.g] + (long long)row * p.N : p.out + row_off;
         brow = p.bias ? p.bias + (long long)(tc.g % p.n_wgroups) * p.N : nullptr;
       }
       const bool empty = WGRAD && tc.kb_lo >= tc.kb_hi;   // no MMA ran: write zeros
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && n + 32 <= p.N) {
-          __nv_bfloat16* dst = p.out + row_off + n;
+          __nv_bfloat16* dst = orow + n;
           const float* sb = brow ? sbw + c * 32 : nullptr;
           if (fast_gelu) {
             if (sb) epilogue_chunk_fast<true, true>(cur, row_ok, dst, sb);
@@ -682,7 +687,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             else epilogue_chunk_fast<false, false>(cur, row_ok, dst, sb);
           }
         } else {
-          epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
+          epilogue_chunk(p, cur, row_ok, pad_row, row_off, orow, n, brow ? sbw + c * 32 : nullptr,
                          cy0, cw0, cy1, cw1);
         }
         if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -699,6 +704,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
+  // rows stored into peer memory (fused expert-parallel return): each writing
+  // thread fences at system scope before the kernel completes; the following
+  // signal kernel then releases the ready flags
+  if (!WGRAD && warp >= 4 && p.out_groups) __threadfence_system();
   tc_fence_before();
   __syncthreads();
   if (TWO_SM) cluster_sync();  // the leader's MMAs write the peer's TMEM
@@ -805,7 +814,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
                       const void* residual, const void* aux_in, void* aux_out, void* out,
                       int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                       int rows_clip, int N, int K, int epi, int zero_tail, cudaStream_t st,
-                      const CombineSpec* cs) {
+                      const CombineSpec* cs, void* const* out_groups) {
   using namespace sm100;
   SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
   SCMOE_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "bf16 GEMM needs k_in and n_out multiples of 8");
@@ -828,6 +837,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   p.aux_in = (const __nv_bfloat16*)aux_in;
   p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
+  p.out_groups = (__nv_bfloat16* const*)out_groups;
   if (cs) {
     SCMOE_CHECK_ARG(num_groups == 1 && epi == EPI_BIAS && cs->k >= 1 && cs->k <= 2 && cs->y &&
                         cs->indices && cs->slots && cs->weights && cs->capacity >= 1 &&

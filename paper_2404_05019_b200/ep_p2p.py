@@ -91,6 +91,14 @@ class PeerExchange:
         tab = torch.tensor([[b + o for b in bases] for o in self._offs],
                            dtype=torch.int64, device=dev)
         self.tables = tab     # rows: recv, y, back, recv_counts, flags
+        # fused return: group (src, el) of this owner -> the source's back rows
+        # (rank * E_l + el) * C (global expert order on the source)
+        esz = torch.tensor([], dtype=self.dtype).element_size()
+        row = self.capacity * self.d_model * esz
+        self.group_out = torch.tensor(
+            [bases[g // self.e_local] + self._offs[2] +
+             (self.rank * self.e_local + g % self.e_local) * row
+             for g in range(self.world * self.e_local)], dtype=torch.int64, device=dev)
         return self
 
     def _tab(self, i: int) -> int:
@@ -201,6 +209,28 @@ class PeerExchange:
         if signal:
             self.signal(1, stream)
         return self.y
+
+    def expert_ffn_to_peers(self, experts, stream=None) -> None:
+        """Owner side, fused form of the return trip: wait for every source's
+        rows, then one grouped FFN whose GEMM2 epilogue stores each finished
+        row tile straight into the source's `back` buffer over peer memory
+        (no local y, no separate return kernel); then release flag 1."""
+        self.wait(0, stream)
+        check(lib().scmoe_expert_ffn_to_peers(
+            ptr(self.recv), dtype_code(self.dtype), ptr(experts.w1t), ptr(experts.b1),
+            ptr(experts.w2t), ptr(experts.b2), ptr(self._hidden(experts)),
+            self.group_out.data_ptr(), self.world * self.e_local, experts.n_experts,
+            self.capacity, ptr(self.recv_counts), self.capacity, self.d_model, experts.d_hidden,
+            stream_ptr(stream)))
+        self.signal(1, stream)
+
+    def _hidden(self, experts) -> torch.Tensor:
+        h = getattr(self, "_hidden_buf", None)
+        shape = (self.world * self.e_local, self.capacity, experts.d_hidden)
+        if h is None or tuple(h.shape) != shape:
+            h = torch.empty(shape, dtype=self.dtype, device=self.recv.device)
+            self._hidden_buf = h
+        return h
 
     def push_back(self, max_ctas: int = 0, stream=None) -> None:
         """Owner side, push form of the return trip: valid rows of y into every

@@ -434,8 +434,7 @@ class _RoutedMoE(nn.Module):
         rows back; returns the (E, C, d) buffer combine gathers from."""
         xg = self.peer_exchange(dec.capacity)
         xg.dispatch(x_src, dec.indices, dec.slots, dec.counts, stream=stream)
-        xg.expert_ffn(self.experts, signal=False, stream=stream)
-        xg.push_back(stream=stream)
+        xg.expert_ffn_to_peers(self.experts, stream=stream)     # return fused into GEMM2
         xg.wait(1, stream)
         return xg.back.view(-1, dec.capacity, self.d_model)
 

@@ -79,8 +79,9 @@ def test_ep_calibrate_and_train_step():
     assert l1 < l0
 
 
-@pytest.mark.parametrize("variant,slot", [("scmoe", 0), ("scmoe", 2), ("standard", None)])
-def test_ep_p2p_backend_equals_local(variant, slot):
+@pytest.mark.parametrize("variant,slot,ret", [("scmoe", 0, "fused"), ("scmoe", 2, "push"),
+                                              ("standard", None, "fused"), ("scmoe", 1, "push")])
+def test_ep_p2p_backend_equals_local(variant, slot, ret):
     """ep_backend="p2p": dispatch and return trip are our peer-memory kernels
     on the side stream (symmetric memory over the one-rank group); repeated
     forwards reuse the buffers (epoch flags)."""
@@ -92,7 +93,7 @@ def test_ep_p2p_backend_equals_local(variant, slot):
               capacity_factor=1.25, dtype=torch.bfloat16)
     loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2), **kw)
     epb = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(2),
-                           ep_group=dist.group.WORLD, ep_backend="p2p", **kw)
+                           ep_group=dist.group.WORLD, ep_backend="p2p", p2p_return=ret, **kw)
     if slot is not None:
         epb.slot = loc.slot = slot
     for it in range(3):
@@ -104,4 +105,4 @@ def test_ep_p2p_backend_equals_local(variant, slot):
         torch.cuda.synchronize()
         assert torch.equal(a, b), it
         comm = [s for s in rec.spans() if s.stream == "comm"]
-        assert len(comm) == 2
+        assert len(comm) == (1 if ret == "fused" else 2)   # fused: return inside GEMM2

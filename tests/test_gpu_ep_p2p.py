@@ -8,7 +8,9 @@ are per rank (gating.py:134-135), the grouped FFN rows are identical.
 
 Covered: world 2 / 4, 1 and 2 experts per rank, top-1 ScMoE (SE + CG
 combine) and top-2, pull-form combine (rows read from the owner's y) and
-push-form return (owner stores rows into the source's back buffer), several
+push-form return (owner stores rows into the source's back buffer), the
+fused return (the owner's GEMM2 epilogue stores rows into the sources' back
+buffers), several
 calls in a row (epoch flags advance, buffers reused), a CUDA-graph capture of
 the whole sequence replayed with new inputs, and a one-rank symmetric-memory
 rendezvous over NCCL."""
@@ -54,6 +56,9 @@ def _run_ep(layer, xs, srcs, world, e_l, form, mode):
         vx[r].dispatch(srcs[r], decs[r].indices, decs[r].slots, decs[r].counts,
                        max_ctas=(32 if r % 2 else 0))
     for r in range(world):
+        if form == "fused":
+            vx[r].expert_ffn_to_peers(vex[r])
+            continue
         vx[r].expert_ffn(vex[r], signal=(form == "pull"))
         if form == "push":
             vx[r].push_back(max_ctas=16)
@@ -79,7 +84,7 @@ def _layer(kind, d, h, n, mode):
 
 @pytest.mark.parametrize("world,e_l", [(2, 1), (2, 2), (4, 1), (4, 2)])
 @pytest.mark.parametrize("kind,mode", [("scmoe", "direct_add"), ("scmoe", "cg2"), ("top2", None)])
-@pytest.mark.parametrize("form", ["pull", "push"])
+@pytest.mark.parametrize("form", ["pull", "push", "fused"])
 def test_p2p_ep_equals_local(world, e_l, kind, mode, form):
     T, d, h = 300, 128, 256
     layer = _layer(kind, d, h, world * e_l, mode)
