@@ -353,7 +353,7 @@ def timed(fn, steps, ws, recorder_factory=None):
 def hbm_kernel_times(moe, x, reps: int = 10):
     """Per-launch device time of the HBM-bound hot-path ops (K1 gate, K2
     dispatch, K5 combine) at the bench shape: each op captured in a CUDA graph,
-    L2 flushed (512 MB write) before every replay, CUDA events around the
+    L2 flushed (512 MB read) before every replay, CUDA events around the
     replay alone, median over `reps`.  Algorithmic bytes:
     gate T*d*s + T*N*4, dispatch 2*kept*d*s, combine (k+3)*T*d*s."""
     import torch
@@ -362,6 +362,7 @@ def hbm_kernel_times(moe, x, reps: int = 10):
     N = moe.n_experts
     dec = moe.route(x)
     kept = int(dec.kept_counts().sum().item())
+    rows_read = int(((dec.slots < dec.capacity).any(dim=1)).sum().item())
     buf = K.dispatch(x, dec.indices, dec.slots, N, dec.capacity)
     se = torch.randn_like(x)
     res = torch.randn_like(x)
@@ -369,11 +370,13 @@ def hbm_kernel_times(moe, x, reps: int = 10):
     ops = {
         "gate": (lambda: moe.route(x), T * d * 2 + T * N * 4),
         "dispatch": (lambda: K.dispatch(x, dec.indices, dec.slots, N, dec.capacity, out=buf),
-                     2 * kept * d * 2),
+                     (rows_read + kept) * d * 2),
         "combine": (lambda: K.combine(buf, dec.indices, dec.slots, dec.weights, dec.capacity,
                                       se_out=se, residual=res, out=out), (dec.k + 3) * T * d * 2),
     }
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=x.device)
+    # read-only L2 flush: a write flush would leave ~126 MB of dirty lines whose
+    # write-back then competes with the measured kernel
+    flush = torch.ones(128 * 1024 * 1024, dtype=torch.float32, device=x.device)
     st = torch.cuda.current_stream()
     res_d = {}
     for name, (fn, nbytes) in ops.items():
@@ -390,7 +393,7 @@ def hbm_kernel_times(moe, x, reps: int = 10):
         torch.cuda.synchronize()
         ts = []
         for i in range(reps + 2):
-            flush.zero_()
+            flush.sum()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             g.replay()
