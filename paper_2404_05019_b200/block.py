@@ -419,9 +419,18 @@ class ScMoEBlockPair(nn.Module):
                 buf = TR.DispatchFn.apply(src(), dec.indices, dec.slots, env["kept"], moe.n_experts,
                                           dec.capacity)
                 env["buf"] = buf
-                if use_ep:   # exchanges inline on the compute stream while training
-                    env["recv_counts"] = ep_mod.exchange_counts(env["kept"], self.ep_group)
-                    env["buf"] = TR.ExchangeFn.apply(buf, self.ep_group)
+                if use_ep:
+                    # the exchange runs on the comm stream beside the window ops;
+                    # autograd runs its backward (the reverse exchange) on that
+                    # stream too and synchronises the gradients across streams
+                    cs.wait_stream(st)
+                    buf.record_stream(cs)
+                    with rec.op("dispatch", "comm", cs), torch.cuda.stream(cs):
+                        env["recv_counts"] = ep_mod.exchange_counts(env["kept"], self.ep_group)
+                        env["buf"] = TR.ExchangeFn.apply(buf, self.ep_group)
+                        ev = torch.cuda.Event()
+                        ev.record(cs)
+                    env["disp_ev"] = ev
                 return
             if p2p:
                 # kept rows go straight to their owners over peer memory, on the
@@ -451,9 +460,22 @@ class ScMoEBlockPair(nn.Module):
                 return expert_offload()
             if train:
                 e = moe.experts
+                if use_ep:
+                    st.wait_event(env["disp_ev"])
+                    env["buf"].record_stream(st)
+                    env["recv_counts"].record_stream(st)
                 rows = env["recv_counts"] if use_ep else env["kept"]
                 y = TR.FFNFn.apply(env["buf"], e.w1t, e.b1, e.w2t, e.b2, None, rows, dec.capacity)
-                env["y"] = TR.ExchangeFn.apply(y, self.ep_group) if use_ep else y
+                if not use_ep:
+                    env["y"] = y
+                    return
+                cs.wait_stream(st)
+                y.record_stream(cs)
+                with rec.op("combine", "comm", cs), torch.cuda.stream(cs):
+                    env["y"] = TR.ExchangeFn.apply(y, self.ep_group)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                env["y_ev"] = ev
                 return
             if p2p:
                 xg = self._xchg
@@ -502,6 +524,9 @@ class ScMoEBlockPair(nn.Module):
                 return decode_chunked()
             if train:
                 std = self.variant == "standard"
+                if use_ep:
+                    st.wait_event(env["y_ev"])
+                    env["y"].record_stream(st)
                 env["out"] = TR.CombineFn.apply(
                     env["y"], None if std else env["se"], env["w"], None if std else env["x_cur"],
                     None if std else moe.w_cg, env["h_mh_cur"], dec.indices, dec.slots, env["kept"],

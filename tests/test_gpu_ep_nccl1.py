@@ -106,3 +106,28 @@ def test_ep_p2p_backend_equals_local(variant, slot, ret):
         assert torch.equal(a, b), it
         comm = [s for s in rec.spans() if s.stream == "comm"]
         assert len(comm) == (1 if ret == "fused" else 2)   # fused: return inside GEMM2
+
+
+@pytest.mark.parametrize("variant", ["scmoe", "standard"])
+def test_ep_training_step_equals_local(variant):
+    """Training under expert parallelism: the exchanges (and their backward,
+    the reverse exchanges) run on the comm stream; on one rank the gradients
+    and the updated weights equal the local block's bit for bit."""
+    import torch.distributed as dist
+    T, d, h, N = 512, 128, 256, 4
+    kw = dict(variant=variant, k_routed=1 if variant == "scmoe" else 2,
+              shortcut_pos="pos2" if variant == "scmoe" else None, n_heads=4, seq_len=128,
+              capacity_factor=1.25, dtype=torch.bfloat16)
+    loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(6), **kw)
+    epb = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(6),
+                           ep_group=dist.group.WORLD, **kw)
+    loc.requires_grad_(True)
+    epb.requires_grad_(True)
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    for it in range(2):
+        la = loc.train_step(x, lr=1e-3)
+        lb = epb.train_step(x, lr=1e-3)
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb), it
+    for (na, pa), (nb, pb) in zip(loc.named_parameters(), epb.named_parameters()):
+        assert torch.equal(pa, pb), na
