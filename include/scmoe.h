@@ -207,6 +207,10 @@ int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_sr
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);
 
+/* Tuning / test hook: tcgen05 tile width, 0 = auto (128 when n_out is an odd
+ * multiple of 128 and the narrow tile needs fewer column-waves), 128 or 256. */
+int scmoe_set_gemm_tile_n(int bn);
+
 /*
  * Full expert_forward (arch.py:349-351) over groups: GEMM1 (bias+GELU) into
  * `hidden` (num_groups, group_cap, d_hidden), then GEMM2 (bias, + residual

@@ -38,36 +38,42 @@
 namespace scmoe {
 namespace sm100 {
 
-constexpr int BN = 256, BK = 64;
+constexpr int BK = 64;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + EPI_WARPS * 32;
-constexpr int ACC_STAGES = 2;
-constexpr int TMEM_COLS = ACC_STAGES * BN;
+constexpr int TMEM_COLS = 512;                   // 512 / BN accumulator stages
 constexpr int MAX_GROUPS = 1024;
 constexpr int MN_BOX = 64;                       // MN-major TMA box: 64 (mn) x 64 (k)
 constexpr int MN_BOX_BYTES = MN_BOX * BK * 2;    // 8 KB
 
-template <bool TWO_SM>
+// BN_ = 256 (default) or 128: the narrow tile for n_out = 384-style widths
+// (configs[1]) that would leave half a 256-column tile idle; it also doubles
+// the accumulator stages (4 x 128 TMEM columns) for small-K tiles.
+template <bool TWO_SM, int BN_ = 256>
 struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int ACC_STAGES = TMEM_COLS / BN;
   static constexpr int CTA_M = 128;                       // rows of A per CTA
   static constexpr int TILE_M = TWO_SM ? 256 : 128;       // rows per (cluster) tile
   static constexpr int B_ROWS = TWO_SM ? BN / 2 : BN;     // rows of B per CTA
-  static constexpr int STAGES = TWO_SM ? 6 : 4;
   static constexpr int A_BYTES = CTA_M * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024 / STAGE_BYTES) < 8 ? (192 * 1024 / STAGE_BYTES) : 8;
   // + per-epilogue-warp bias slice (8 warps x 128 fp32), staged once per tile
   static constexpr size_t MISC = 256 + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 16;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + MISC + 8 * 128 * 4;
+  // + per-epilogue-warp 2 KB store-transpose staging
+  static constexpr size_t SMEM =
+      1024 + (size_t)STAGES * STAGE_BYTES + MISC + 8 * 128 * 4 + EPI_WARPS * 2048;
 };
 
 // instruction descriptor: D fp32, A/B bf16, M = TILE_M, N = 256, operand majors
-template <bool TWO_SM, bool A_MN, bool B_MN>
+template <bool TWO_SM, bool A_MN, bool B_MN, int BN>
 struct Idesc {
   static constexpr uint32_t value = (1u << 4) | (1u << 7) | (1u << 10) |
                                     ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
                                     ((uint32_t)(BN >> 3) << 17) |
-                                    ((uint32_t)(Cfg<TWO_SM>::TILE_M >> 4) << 24);
+                                    ((uint32_t)(Cfg<TWO_SM, BN>::TILE_M >> 4) << 24);
 };
 
 enum Epi { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GELU_BWD = 2 };
@@ -253,7 +259,7 @@ struct Tile {
   int g, m0, n0, s, kb_lo, kb_hi;
 };
 
-template <int TILE_M, bool WGRAD>
+template <int TILE_M, int BN, bool WGRAD>
 __device__ __forceinline__ Tile decode_tile(const Params& p, int t, int n_tiles_n,
                                             const int* prefix) {
   Tile c;
@@ -303,11 +309,45 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc,
   }
 }
 
+// Row-per-thread results (lane = row, 4 x 16 B = 32 bf16 columns) to global
+// memory through a 2 KB per-warp staging buffer: the warp transposes its
+// 32 rows x 64 B so each store instruction writes 8 rows x 64 B (whole 32 B
+// sectors) instead of 32 rows x 16 B (half sectors, 32 lines per
+// instruction — the small-K limiter).  16-B slot u of row r sits at
+// r * 4 + (u ^ ((r >> 1) & 3)): conflict-free both ways.  Rows whose bit is
+// clear in `row_mask` and 8-column groups at or past `ncols` are not written.
+__device__ __forceinline__ void stage_put(uint4* __restrict__ stg, int lane, int u, uint4 v) {
+  stg[lane * 4 + (u ^ ((lane >> 1) & 3))] = v;
+}
+__device__ __forceinline__ void stage_flush(const uint4* __restrict__ stg, int lane,
+                                            __nv_bfloat16* row0, long long ld, uint32_t row_mask,
+                                            int ncols) {
+  __syncwarp();                       // every lane's row is staged
+  const int j = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = (lane >> 2) + 8 * i;
+    const uint4 v = stg[rr * 4 + (j ^ ((rr >> 1) & 3))];
+    if (((row_mask >> rr) & 1u) && j * 8 < ncols) st_v4(row0 + rr * ld + j * 8, v);
+  }
+}
+// the packed row (16-B slot u = r[4u .. 4u+3]) through the staging buffer
+__device__ __forceinline__ void store_rows_staged(const uint32_t (&r)[32], uint4* __restrict__ stg,
+                                                  int lane, __nv_bfloat16* row0, long long ld,
+                                                  uint32_t row_mask, int ncols) {
+  __syncwarp();                       // the previous flush's reads are done
+#pragma unroll
+  for (int u = 0; u < 4; ++u) stage_put(stg, lane, u, make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]));
+  stage_flush(stg, lane, row0, ld, row_mask, ncols);
+}
+
 // bias / GELU / GELU-backward / residual -> bf16 for 32 columns of one row,
-// or zeros for padding rows
-__device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32],
+// zeros for padding rows.  The packed result replaces the accumulator in
+// place (16-B slot u = r[4u .. 4u+3], already consumed); the pre-activation
+// (aux_out) goes straight into this lane's staging slots `zs`.
+__device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32],
                                                bool row_ok, bool pad_row, long long row_off,
-                                               __nv_bfloat16* orow, int n, const float* sb,
+                                               int n, const float* sb, uint4* zs, int lane,
                                                const __nv_bfloat16* cy0 = nullptr, float cw0 = 0.f,
                                                const __nv_bfloat16* cy1 = nullptr, float cw1 = 0.f) {
   if (n >= p.N || !(row_ok || pad_row)) return;
@@ -316,8 +356,8 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
     const int nn = n + u * 8;
     if (nn < p.N) {
       if (!row_ok) {
-        st_v4(orow + nn, make_uint4(0, 0, 0, 0));
-        if (p.aux_out) st_v4(p.aux_out + row_off + nn, make_uint4(0, 0, 0, 0));
+        r[4 * u] = r[4 * u + 1] = r[4 * u + 2] = r[4 * u + 3] = 0u;
+        if (zs) stage_put(zs, lane, u, make_uint4(0, 0, 0, 0));
         continue;
       }
       float v[8];
@@ -330,10 +370,10 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
         v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
       }
       if (p.epi == EPI_BIAS_GELU) {
-        if (p.aux_out) {
+        if (zs) {
           Vec16<__nv_bfloat16> z;
           z.from_float(v);
-          st_v4(p.aux_out + row_off + nn, z.raw);
+          stage_put(zs, lane, u, z.raw);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
@@ -383,9 +423,12 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] += rf[i];
       }
-      Vec16<__nv_bfloat16> o;
-      o.from_float(v);
-      st_v4(orow + nn, o.raw);
+      Vec16<__nv_bfloat16> ov;
+      ov.from_float(v);
+      r[4 * u] = ov.raw.x;
+      r[4 * u + 1] = ov.raw.y;
+      r[4 * u + 2] = ov.raw.z;
+      r[4 * u + 3] = ov.raw.w;
     }
   }
 }
@@ -395,11 +438,8 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
 // so the 32 values run as straight-line code — the general epilogue_chunk is
 // latency-bound on per-element checks with only 8 epilogue warps per SM.
 template <bool BIAS, bool GELU>
-__device__ __forceinline__ void epilogue_chunk_fast(const uint32_t (&r)[32], bool row_ok,
-                                                    __nv_bfloat16* __restrict__ dst,
+__device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
                                                     const float* __restrict__ sb) {
-  if (!row_ok) return;
-  uint4 o[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     float v[8];
@@ -417,10 +457,11 @@ __device__ __forceinline__ void epilogue_chunk_fast(const uint32_t (&r)[32], boo
     }
     Vec16<__nv_bfloat16> w;
     w.from_float(v);
-    o[u] = w.raw;
+    r[4 * u] = w.raw.x;            // in place: slots 4u..4u+3 are consumed
+    r[4 * u + 1] = w.raw.y;
+    r[4 * u + 2] = w.raw.z;
+    r[4 * u + 3] = w.raw.w;
   }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) st_v4(dst + u * 8, o[u]);
 }
 
 // fp32 wgrad partial: 32 columns of one output row
@@ -439,13 +480,15 @@ __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32
   }
 }
 
-template <bool TWO_SM, bool B_MN, bool WGRAD>
+template <bool TWO_SM, bool B_MN, bool WGRAD, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const Params p) {
-  using C = Cfg<TWO_SM>;
+  using C = Cfg<TWO_SM, BN>;
+  constexpr int ACC_STAGES = C::ACC_STAGES;
+  constexpr int NCH = BN / 64;          // 32-column chunks per epilogue warp
   constexpr bool A_MN = WGRAD;
-  constexpr uint32_t IDESC = Idesc<TWO_SM, A_MN, B_MN>::value;
+  constexpr uint32_t IDESC = Idesc<TWO_SM, A_MN, B_MN, BN>::value;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -459,6 +502,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 2 * ACC_STAGES);
   int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
+  uint4* s_stage = reinterpret_cast<uint4*>(s_bias + EPI_WARPS * 128);   // 2 KB per epilogue warp
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -535,7 +579,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int t = unit; t < total_tiles; t += n_units) {
-      const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
+      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
       const int am = tc.m0 + (int)rank * C::CTA_M;
       const int bn = tc.n0 + (int)rank * C::B_ROWS;
       for_each_kblock<WGRAD>(p, tc, [&](int g, int kb) {
@@ -562,9 +606,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = unit; t < total_tiles; t += n_units, ++it) {
-        const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
+        const int acc = it % ACC_STAGES;
+        const uint32_t acc_phase = (it / ACC_STAGES) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
         if (lane == 0) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -600,7 +644,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== epilogue (both CTAs, each on its own 128 TMEM lanes) =====
     const int ew = warp - 4;
     const int quad = warp & 3;   // TMEM lanes [32*quad, 32*quad+32)
-    const int half = ew >> 2;    // accumulator columns [128*half, 128*half+128)
+    const int half = ew >> 2;    // accumulator columns [BN/2*half, BN/2*(half+1))
     // the fast epilogue covers bias / bias+GELU stores without residual,
     // pre-activation / GELU-backward operands, zero tails or the fused combine
     const bool fast = !WGRAD && !p.residual && !p.aux_out && !p.aux_in && !p.c_k &&
@@ -608,13 +652,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool fast_gelu = p.epi == EPI_BIAS_GELU;
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
-      const Tile tc = decode_tile<C::TILE_M, WGRAD>(p, t, n_tiles_n, s_prefix);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const int row = tc.m0 + (int)rank * C::CTA_M + quad * 32 + lane;
+      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
+      const int acc = it % ACC_STAGES;
+      const uint32_t acc_phase = (it / ACC_STAGES) & 1;
+      const int row_w0 = tc.m0 + (int)rank * C::CTA_M + quad * 32;   // this warp's first row
+      const int row = row_w0 + lane;
       bool row_ok, pad_row = false;
       long long row_off;
-      __nv_bfloat16* orow = nullptr;
+      __nv_bfloat16* orow0 = nullptr;      // row row_w0 of the output / aux
+      __nv_bfloat16* arow0 = nullptr;
       const float* brow = nullptr;
       if (WGRAD) {
         row_ok = row < p.m_out;
@@ -624,21 +670,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         row_ok = row < rows;
         pad_row = p.zero_tail && row < p.cap;
         row_off = ((long long)tc.g * p.cap + row) * p.N;
-        orow = p.out_groups ? p.out_groups[tc.g] + (long long)row * p.N : p.out + row_off;
+        const long long off0 = ((long long)tc.g * p.cap + row_w0) * p.N;
+        orow0 = p.out_groups ? p.out_groups[tc.g] + (long long)row_w0 * p.N : p.out + off0;
+        if (p.aux_out) arow0 = p.aux_out + off0;
         brow = p.bias ? p.bias + (long long)(tc.g % p.n_wgroups) * p.N : nullptr;
       }
       const bool empty = WGRAD && tc.kb_lo >= tc.kb_hi;   // no MMA ran: write zeros
-      // stage this warp's 128 bias columns before waiting for the accumulator
+      // stage this warp's BN/2 bias columns before waiting for the accumulator
       // (the loads overlap the MMAs; the chunk loop reads smem broadcasts)
       float* sbw = s_bias + ew * 128;
       if (!WGRAD && brow) {
-        const int nb = tc.n0 + half * 128 + 4 * lane;
+        const int nb = tc.n0 + half * (BN / 2) + 4 * lane;
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
         if (nb + 3 < p.N) b = *reinterpret_cast<const float4*>(brow + nb);
         else
           for (int i = 0; i < 4 && nb + i < p.N; ++i) (&b.x)[i] = brow[nb + i];
         __syncwarp();        // previous tile's reads of sbw are done
-        *reinterpret_cast<float4*>(sbw + 4 * lane) = b;
+        if (4 * lane < BN / 2) *reinterpret_cast<float4*>(sbw + 4 * lane) = b;
         __syncwarp();
       }
       // fused combine: this row's (token's) routed rows, before the wait
@@ -660,38 +708,44 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      const uint32_t wmask = __ballot_sync(0xffffffffu, row_ok || pad_row);
+      uint4* stg = s_stage + ew * 128;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      // TMEM -> registers in 4 chunks of 32 columns, chunk c+1's tcgen05.ld in
+      // TMEM -> registers in NCH chunks of 32 columns, chunk c+1's tcgen05.ld in
       // flight while chunk c is processed
-      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
+      const uint32_t tbase =
+          tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
       uint32_t ra[32], rb[32];
       SCMOE_TMEM_LD32(tbase, ra);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         uint32_t(&cur)[32] = (c & 1) ? rb : ra;
         uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
-        if (c < 3) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
-        const int n = tc.n0 + half * 128 + c * 32;
+        if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
+        const int n = tc.n0 + half * (BN / 2) + c * 32;
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && n + 32 <= p.N) {
-          __nv_bfloat16* dst = orow + n;
           const float* sb = brow ? sbw + c * 32 : nullptr;
           if (fast_gelu) {
-            if (sb) epilogue_chunk_fast<true, true>(cur, row_ok, dst, sb);
-            else epilogue_chunk_fast<false, true>(cur, row_ok, dst, sb);
+            if (sb) epilogue_chunk_fast<true, true>(cur, sb);
+            else epilogue_chunk_fast<false, true>(cur, sb);
           } else {
-            if (sb) epilogue_chunk_fast<true, false>(cur, row_ok, dst, sb);
-            else epilogue_chunk_fast<false, false>(cur, row_ok, dst, sb);
+            if (sb) epilogue_chunk_fast<true, false>(cur, sb);
+            else epilogue_chunk_fast<false, false>(cur, sb);
           }
-        } else {
-          epilogue_chunk(p, cur, row_ok, pad_row, row_off, orow, n, brow ? sbw + c * 32 : nullptr,
-                         cy0, cw0, cy1, cw1);
+          store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
+        } else if (n < p.N && wmask) {
+          if (arow0) __syncwarp();   // the previous flush's reads are done before z is staged
+          epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
+                         arow0 ? stg : nullptr, lane, cy0, cw0, cy1, cw1);
+          if (arow0) stage_flush(stg, lane, arow0 + n, p.N, wmask, p.N - n);
+          store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, p.N - n);
         }
-        if (c < 3) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == 2) {
+        if (c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == NCH - 2) {
           // the whole accumulator is in registers: hand TMEM back to the MMA warp
           tc_fence_before();
           __syncwarp();
@@ -776,12 +830,12 @@ int make_map(CUtensorMap* map, const void* base, int inner, int outer, int group
   return SCMOE_OK;
 }
 
-template <bool TWO_SM, bool B_MN, bool WGRAD>
+template <bool TWO_SM, bool B_MN, bool WGRAD, int BN>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
            cudaStream_t st) {
-  using C = Cfg<TWO_SM>;
+  using C = Cfg<TWO_SM, BN>;
   static bool attr_set = false;
-  auto kern = gemm_kernel<TWO_SM, B_MN, WGRAD>;
+  auto kern = gemm_kernel<TWO_SM, B_MN, WGRAD, BN>;
   if (!attr_set) {
     SCMOE_CUDA_TRY(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -807,6 +861,24 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
 
 // mode: 0 auto, 1 force 1-SM, 2 force 2-SM (tests / tuning)
 static int g_gemm_mode = 0;
+// tile width: 0 auto, 128 or 256 forced (tests / tuning)
+static int g_gemm_bn = 0;
+
+// Forward / dgrad tile width: 256 unless forced.  Measured on the configs[1]
+// shapes (scripts/ab_gemm_cublas.py train): BN = 128 loses even where it
+// removes a half-empty 256-column tile (n_out = 384: 729 vs 908 TFLOP/s) —
+// the narrower MMA re-reads A from shared memory per 128 columns.
+template <typename F>
+static int pick_bn(F&&, long long) {
+  return g_gemm_bn ? g_gemm_bn : 256;
+}
+
+template <bool TWO_SM, bool B_MN, bool WGRAD>
+static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const sm100::Params& p,
+                     int grid, cudaStream_t st) {
+  return bn == 128 ? sm100::launch<TWO_SM, B_MN, WGRAD, 128>(ma, mb, p, grid, st)
+                   : sm100::launch<TWO_SM, B_MN, WGRAD, 256>(ma, mb, p, grid, st);
+}
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -851,27 +923,28 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
     p.c_k = cs->k;
   }
   const int sms = num_sms();
-  const long long n_tiles_n = (N + BN - 1) / BN;
-  const long long tiles_2sm = (long long)num_groups * ((cap + 255) / 256) * n_tiles_n;
-  const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_2sm >= sms / 2);
+  auto tiles_of = [&](int tile_m, int bn) {
+    return (long long)num_groups * ((cap + tile_m - 1) / tile_m) * ((N + bn - 1) / bn);
+  };
+  const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_of(256, 256) >= sms / 2);
+  const int tile_m = two ? 256 : 128;
+  const long long max_units = two ? sms / 2 : sms;
+  const int bn = pick_bn([&](int b) { return tiles_of(tile_m, b); }, max_units);
+  const long long tiles = tiles_of(tile_m, bn);
+  const long long units = tiles < max_units ? tiles : max_units;
+  if (units <= 0) return SCMOE_OK;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, a, K, cap, num_groups, Cfg<true>::CTA_M);
   if (rc) return rc;
-  const int b_rows = two ? Cfg<true>::B_ROWS : Cfg<false>::B_ROWS;
+  const int b_rows = two ? bn / 2 : bn;
   rc = b_mn ? make_map(&mb, wt, N, K, n_wgroups, BK) : make_map(&mb, wt, K, N, n_wgroups, b_rows);
   if (rc) return rc;
-  if (two) {
-    const long long units = tiles_2sm < sms / 2 ? tiles_2sm : sms / 2;
-    if (units <= 0) return SCMOE_OK;
-    rc = b_mn ? launch<true, true, false>(ma, mb, p, (int)units * 2, st)
-              : launch<true, false, false>(ma, mb, p, (int)units * 2, st);
-  } else {
-    const long long tiles = (long long)num_groups * ((cap + 127) / 128) * n_tiles_n;
-    const int grid = (int)(tiles < sms ? tiles : sms);
-    if (grid <= 0) return SCMOE_OK;
-    rc = b_mn ? launch<false, true, false>(ma, mb, p, grid, st)
-              : launch<false, false, false>(ma, mb, p, grid, st);
-  }
+  if (two)
+    rc = b_mn ? launch_bn<true, true, false>(bn, ma, mb, p, (int)units * 2, st)
+              : launch_bn<true, false, false>(bn, ma, mb, p, (int)units * 2, st);
+  else
+    rc = b_mn ? launch_bn<false, true, false>(bn, ma, mb, p, (int)units, st)
+              : launch_bn<false, false, false>(bn, ma, mb, p, (int)units, st);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
@@ -890,12 +963,23 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
   SCMOE_CHECK_ARG(aligned16(a) && aligned16(b) && aligned16(out) && aligned16(ws),
                   "wgrad operands must be 16-byte aligned");
   const int sms = num_sms();
+  // Tile shape: 2-SM 256x256 when the outputs alone fill the CTA pairs
+  // (configs[2]-size weights); small weights (configs[1]: 384 / 1152 / 1536
+  // wide) run split-K on 1-SM 128x128 tiles with 4 accumulator stages — the
+  // fastest of the four shapes on every configs[1] weight (scripts/ab_wgrad.py:
+  // 546-610 TFLOP/s vs 458-591).
+  const long long tiles_big = (long long)n_wgroups * ((m_out + 255) / 256) * ((n_out + 255) / 256);
+  const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_big >= sms / 2);
+  const int tile_m = two ? 256 : 128;
+  const int bn = g_gemm_bn ? g_gemm_bn : (two ? 256 : 128);
+  const long long max_units = two ? sms / 2 : sms;
   const long long tiles1 =
-      (long long)n_wgroups * ((m_out + 255) / 256) * ((n_out + BN - 1) / BN);
+      (long long)n_wgroups * ((m_out + tile_m - 1) / tile_m) * ((n_out + bn - 1) / bn);
   if (splits <= 0) {
-    // fill the CTA pairs: split the token reduction until ~1 tile per pair
+    // fill the persistent units in ONE wave: floor(units / tiles) splits of
+    // the token reduction (rounding up left a second wave of a few tiles)
     const long long kb_guess = ((long long)num_groups / n_wgroups) * ((cap + BK - 1) / BK);
-    long long s = (sms / 2 + tiles1 - 1) / tiles1;
+    long long s = max_units / tiles1;
     if (s > kb_guess / 4) s = kb_guess / 4;
     splits = (int)(s < 1 ? 1 : (s > 64 ? 64 : s));
   }
@@ -917,8 +1001,9 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
   rc = make_map(&mb, b, n_out, cap, num_groups, BK);
   if (rc) return rc;
   const long long units_all = tiles1 * splits;
-  const long long units = units_all < sms / 2 ? units_all : sms / 2;
-  rc = launch<true, true, true>(ma, mb, p, (int)units * 2, st);
+  const long long units = units_all < max_units ? units_all : max_units;
+  rc = two ? launch_bn<true, true, true>(bn, ma, mb, p, (int)units * 2, st)
+           : launch_bn<false, true, true>(bn, ma, mb, p, (int)units, st);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   if (splits > 1) {
@@ -961,5 +1046,14 @@ extern "C" int scmoe_set_gemm_mode(int mode) {
     return SCMOE_ERR_ARG;
   }
   scmoe::g_gemm_mode = mode;
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_set_gemm_tile_n(int bn) {
+  if (bn != 0 && bn != 128 && bn != 256) {
+    scmoe::set_error("gemm tile width must be 0 (auto), 128 or 256");
+    return SCMOE_ERR_ARG;
+  }
+  scmoe::g_gemm_bn = bn;
   return SCMOE_OK;
 }

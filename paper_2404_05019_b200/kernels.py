@@ -195,6 +195,11 @@ def set_gemm_mode(mode: int) -> None:
     check(lib().scmoe_set_gemm_mode(mode))
 
 
+def set_gemm_tile_n(bn: int) -> None:
+    """0 = auto, 128 or 256 = force the tcgen05 tile width (N per tile)."""
+    check(lib().scmoe_set_gemm_tile_n(bn))
+
+
 # ---------------------------------------------------------------------------
 # training-side entries (K7)
 

@@ -15,8 +15,12 @@ for name, M, Kd, N in shapes:
     wt = (torch.randn(N, Kd, device="cuda") / Kd ** 0.5).bfloat16()
     w = wt.t().contiguous()
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    fns = {"ours": lambda: K.grouped_gemm(a, wt, None, out=out),
-           "cublas": lambda: torch.matmul(a, w, out=out)}
+    def ours(bn):
+        def f():
+            K.set_gemm_tile_n(bn)
+            K.grouped_gemm(a, wt, None, out=out)
+        return f
+    fns = {"ours": ours(0), "ours256": ours(256), "cublas": lambda: torch.matmul(a, w, out=out)}
     for _ in range(3):
         for f in fns.values(): f()
     for r in range(6):

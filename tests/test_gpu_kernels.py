@@ -140,13 +140,17 @@ def _ref_ffn_rows(a, wt, bias, gelu):
     (8, 8, 1024, 2048, 8192), (3, 3, 257, 1024, 264), (16, 16, 64, 384, 1536)])
 @pytest.mark.parametrize("gelu", [False, True])
 @pytest.mark.parametrize("mode", [1, 2])
-def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu, mode):
-    """Both tcgen05 variants (1-SM 128x256, 2-SM cta_group::2 256x256)."""
+@pytest.mark.parametrize("tile_n", [128, 256])
+def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu, mode, tile_n):
+    """Both tcgen05 variants (1-SM 128xBN, 2-SM cta_group::2 256xBN) at both
+    tile widths (BN = 256, and 128 with four accumulator stages)."""
     K.set_gemm_mode(mode)
+    K.set_gemm_tile_n(tile_n)
     try:
         _grouped_gemm_case(G, W, C, Kd, N, gelu, residual=(mode == 2 and gelu))
     finally:
         K.set_gemm_mode(0)
+        K.set_gemm_tile_n(0)
 
 
 def _grouped_gemm_case(G, W, C, Kd, N, gelu, residual):

@@ -32,11 +32,13 @@ def _gelu_grad(z):
 
 
 @pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("tile_n", [128, 256])
 @pytest.mark.parametrize("G,W,C,Kd,N", [(1, 1, 384, 256, 512), (4, 2, 300, 1536, 384),
                                         (8, 8, 256, 384, 1536)])
-def test_dgrad_transposed_weights(mode, G, W, C, Kd, N):
+def test_dgrad_transposed_weights(mode, tile_n, G, W, C, Kd, N):
     """out = a @ w[g % W]  with w stored (W, k_in, n_out) — MN-major tcgen05 B."""
     K.set_gemm_mode(mode)
+    K.set_gemm_tile_n(tile_n)
     try:
         g = torch.Generator(device="cuda").manual_seed(G + N)
         a = torch.randn(G, C, Kd, device="cuda", generator=g).bfloat16()
@@ -55,6 +57,7 @@ def test_dgrad_transposed_weights(mode, G, W, C, Kd, N):
             assert torch.all(out[gi, r:tail_end] == 0)
     finally:
         K.set_gemm_mode(0)
+        K.set_gemm_tile_n(0)
 
 
 def test_forward_preactivation_store():
@@ -71,8 +74,21 @@ def test_forward_preactivation_store():
 
 @pytest.mark.parametrize("G,W,C,M,N,splits", [(1, 1, 4096, 384, 1536, 0), (8, 8, 700, 1536, 384, 0),
                                               (4, 2, 513, 256, 264, 3), (2, 1, 128, 64, 128, 1),
-                                              (16, 2, 300, 384, 1536, 0)])
-def test_grouped_wgrad(G, W, C, M, N, splits):
+                                              (16, 2, 300, 384, 1536, 0), (2, 2, 900, 384, 384, 0)])
+@pytest.mark.parametrize("mode,tile_n", [(0, 0), (1, 128), (2, 128), (1, 256), (2, 256)])
+def test_grouped_wgrad(G, W, C, M, N, splits, mode, tile_n):
+    """Split-K weight gradient, every tile shape: auto (least padding of
+    (m_out, n_out)), 1-SM 128-row and 2-SM 256-row tiles x BN 128 / 256."""
+    K.set_gemm_mode(mode)
+    K.set_gemm_tile_n(tile_n)
+    try:
+        _wgrad_case(G, W, C, M, N, splits)
+    finally:
+        K.set_gemm_mode(0)
+        K.set_gemm_tile_n(0)
+
+
+def _wgrad_case(G, W, C, M, N, splits):
     g = torch.Generator(device="cuda").manual_seed(G * 3 + M)
     a = torch.randn(G, C, M, device="cuda", generator=g).bfloat16()
     b = torch.randn(G, C, N, device="cuda", generator=g).bfloat16()
