@@ -98,6 +98,10 @@ struct Params {
   // per-group output base (expert-parallel return fused into GEMM2): group g's
   // rows go to out_groups[g] + row * N (peer memory), nullptr: out + g*cap*N
   __nv_bfloat16* const* out_groups;
+  // 1 when the epilogue reads a row-major operand (residual or the GELU
+  // pre-activation): the ring runs one stage short and that stage's A slot
+  // (16 KB) holds the per-warp coalesced load buffers
+  int ld_buf;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -316,8 +320,23 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const Tile& tc,
 // instruction — the small-K limiter).  16-B slot u of row r sits at
 // r * 4 + (u ^ ((r >> 1) & 3)): conflict-free both ways.  Rows whose bit is
 // clear in `row_mask` and 8-column groups at or past `ncols` are not written.
+// explicit shared-window accesses (a generic pointer here compiled to
+// generic LD.E / ST.E with address-space resolution on every access)
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ void stage_put(uint4* __restrict__ stg, int lane, int u, uint4 v) {
-  stg[lane * 4 + (u ^ ((lane >> 1) & 3))] = v;
+  sts128(smem_u32(stg + lane * 4 + (u ^ ((lane >> 1) & 3))), v);
 }
 __device__ __forceinline__ void stage_flush(const uint4* __restrict__ stg, int lane,
                                             __nv_bfloat16* row0, long long ld, uint32_t row_mask,
@@ -327,7 +346,7 @@ __device__ __forceinline__ void stage_flush(const uint4* __restrict__ stg, int l
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int rr = (lane >> 2) + 8 * i;
-    const uint4 v = stg[rr * 4 + (j ^ ((rr >> 1) & 3))];
+    const uint4 v = lds128(smem_u32(stg + rr * 4 + (j ^ ((rr >> 1) & 3))));
     if (((row_mask >> rr) & 1u) && j * 8 < ncols) st_v4(row0 + rr * ld + j * 8, v);
   }
 }
@@ -346,8 +365,8 @@ __device__ __forceinline__ void store_rows_staged(const uint32_t (&r)[32], uint4
 // place (16-B slot u = r[4u .. 4u+3], already consumed); the pre-activation
 // (aux_out) goes straight into this lane's staging slots `zs`.
 __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32],
-                                               bool row_ok, bool pad_row, long long row_off,
-                                               int n, const float* sb, uint4* zs, int lane,
+                                               bool row_ok, bool pad_row, int n, const float* sb,
+                                               uint4* zs, int lane, const uint4 (&pre)[4],
                                                const __nv_bfloat16* cy0 = nullptr, float cw0 = 0.f,
                                                const __nv_bfloat16* cy1 = nullptr, float cw1 = 0.f) {
   if (n >= p.N || !(row_ok || pad_row)) return;
@@ -379,7 +398,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
         for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
       } else if (p.epi == EPI_GELU_BWD) {
         Vec16<__nv_bfloat16> zv;
-        zv.raw = ld_nc_v4(p.aux_in + row_off + nn);
+        zv.raw = pre[u];                       // pre-activation, staged load
         float z[8];
         zv.to_float(z);
 #pragma unroll
@@ -417,7 +436,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
       }
       if (p.residual) {
         Vec16<__nv_bfloat16> rv;
-        rv.raw = ld_nc_v4(p.residual + row_off + nn);
+        rv.raw = pre[u];                       // residual, staged load
         float rf[8];
         rv.to_float(rf);
 #pragma unroll
@@ -503,6 +522,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
   uint4* s_stage = reinterpret_cast<uint4*>(s_bias + EPI_WARPS * 128);   // 2 KB per epilogue warp
+  const int ring = C::STAGES - p.ld_buf;                                   // mainloop stages
+  uint4* s_load = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 1) * C::A_BYTES);  // if ld_buf
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -593,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                  WGRAD ? g : g % p.n_wgroups);
         }
         __syncwarp();
-        if (++stage == C::STAGES) {
+        if (++stage == ring) {
           stage = 0;
           phase ^= 1;
         }
@@ -631,7 +652,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           first = false;
           __syncwarp();
-          if (++stage == C::STAGES) {
+          if (++stage == ring) {
             stage = 0;
             phase ^= 1;
           }
@@ -710,6 +731,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       const uint32_t wmask = __ballot_sync(0xffffffffu, row_ok || pad_row);
       uint4* stg = s_stage + ew * 128;
+      // the row-major epilogue operand (residual / pre-activation), 32 rows x
+      // 64 B per chunk: coalesced cp.async into this warp's load buffer
+      // (same swizzle as the store staging), chunk c+1 in flight while chunk c
+      // is processed, chunk 0 issued before the accumulator wait
+      const __nv_bfloat16* lsrc =
+          WGRAD ? nullptr : (p.residual ? p.residual : (p.epi == EPI_GELU_BWD ? p.aux_in : nullptr));
+      const uint32_t lmask = __ballot_sync(0xffffffffu, row_ok);
+      uint4* lbuf = s_load + ew * 128;
+      const long long lrow0 = ((long long)tc.g * p.cap + row_w0) * p.N;
+      auto issue_load = [&](int c) {
+        const int n = tc.n0 + half * (BN / 2) + c * 32;
+        const int j = lane & 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = (lane >> 2) + 8 * i;
+          if (((lmask >> rr) & 1u) && n + j * 8 < p.N) {
+            const uint32_t dst = smem_u32(lbuf + rr * 4 + (j ^ ((rr >> 1) & 3)));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(lsrc + lrow0 + (long long)rr * p.N + n + j * 8)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      if (lsrc && p.ld_buf) {
+        __syncwarp();                  // the previous tile's reads of lbuf are done
+        issue_load(0);
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       // TMEM -> registers in NCH chunks of 32 columns, chunk c+1's tcgen05.ld in
@@ -738,9 +787,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (n < p.N && wmask) {
+          uint4 pre[4];
+          if (lsrc && p.ld_buf) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              pre[u] = lds128(smem_u32(lbuf + lane * 4 + (u ^ ((lane >> 1) & 3))));
+            __syncwarp();
+            if (c + 1 < NCH) issue_load(c + 1);
+          } else if (lsrc) {           // no load buffer (not expected): row-per-thread loads
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              pre[u] = (row_ok && n + u * 8 < p.N) ? ld_nc_v4(lsrc + row_off + n + u * 8)
+                                                  : make_uint4(0, 0, 0, 0);
+          }
           if (arow0) __syncwarp();   // the previous flush's reads are done before z is staged
-          epilogue_chunk(p, cur, row_ok, pad_row, row_off, n, brow ? sbw + c * 32 : nullptr,
-                         arow0 ? stg : nullptr, lane, cy0, cw0, cy1, cw1);
+          epilogue_chunk(p, cur, row_ok, pad_row, n, brow ? sbw + c * 32 : nullptr,
+                         arow0 ? stg : nullptr, lane, pre, cy0, cw0, cy1, cw1);
           if (arow0) stage_flush(stg, lane, arow0 + n, p.N, wmask, p.N - n);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, p.N - n);
         }
@@ -910,6 +974,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
   p.out_groups = (__nv_bfloat16* const*)out_groups;
+  p.ld_buf = (residual || (epi == EPI_GELU_BWD && aux_in)) ? 1 : 0;
   if (cs) {
     SCMOE_CHECK_ARG(num_groups == 1 && epi == EPI_BIAS && cs->k >= 1 && cs->k <= 2 && cs->y &&
                         cs->indices && cs->slots && cs->weights && cs->capacity >= 1 &&
