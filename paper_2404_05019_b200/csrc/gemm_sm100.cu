@@ -31,6 +31,7 @@
 // B, the leader's M=256 MMAs read both CTAs' smem and write both TMEMs; 6
 // stages x 32 KB).
 #include <cuda.h>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -383,8 +384,11 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
       if (sb) {   // this chunk's bias, staged in shared memory (warp broadcast)
-        const float4 b0 = *reinterpret_cast<const float4*>(sb + u * 8);
-        const float4 b1 = *reinterpret_cast<const float4*>(sb + u * 8 + 4);
+        const uint4 b0u = lds128(smem_u32(sb + u * 8)), b1u = lds128(smem_u32(sb + u * 8 + 4));
+        const float4 b0 = make_float4(__uint_as_float(b0u.x), __uint_as_float(b0u.y),
+                                      __uint_as_float(b0u.z), __uint_as_float(b0u.w));
+        const float4 b1 = make_float4(__uint_as_float(b1u.x), __uint_as_float(b1u.y),
+                                      __uint_as_float(b1u.z), __uint_as_float(b1u.w));
         v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
         v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
       }
@@ -465,8 +469,11 @@ __device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
     if (BIAS) {
-      const float4 b0 = *reinterpret_cast<const float4*>(sb + u * 8);
-      const float4 b1 = *reinterpret_cast<const float4*>(sb + u * 8 + 4);
+      const uint4 b0u = lds128(smem_u32(sb + u * 8)), b1u = lds128(smem_u32(sb + u * 8 + 4));
+      const float4 b0 = make_float4(__uint_as_float(b0u.x), __uint_as_float(b0u.y),
+                                    __uint_as_float(b0u.z), __uint_as_float(b0u.w));
+      const float4 b1 = make_float4(__uint_as_float(b1u.x), __uint_as_float(b1u.y),
+                                    __uint_as_float(b1u.z), __uint_as_float(b1u.w));
       v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
       v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
     }
@@ -700,14 +707,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       // stage this warp's BN/2 bias columns before waiting for the accumulator
       // (the loads overlap the MMAs; the chunk loop reads smem broadcasts)
       float* sbw = s_bias + ew * 128;
-      if (!WGRAD && brow) {
+      if (!WGRAD && (brow || fast_gelu)) {   // the GELU path adds staged zeros when bias-free
         const int nb = tc.n0 + half * (BN / 2) + 4 * lane;
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (nb + 3 < p.N) b = *reinterpret_cast<const float4*>(brow + nb);
-        else
-          for (int i = 0; i < 4 && nb + i < p.N; ++i) (&b.x)[i] = brow[nb + i];
+        if (brow) {
+          if (nb + 3 < p.N) b = *reinterpret_cast<const float4*>(brow + nb);
+          else
+            for (int i = 0; i < 4 && nb + i < p.N; ++i) (&b.x)[i] = brow[nb + i];
+        }
         __syncwarp();        // previous tile's reads of sbw are done
-        if (4 * lane < BN / 2) *reinterpret_cast<float4*>(sbw + 4 * lane) = b;
+        if (4 * lane < BN / 2)
+          sts128(smem_u32(sbw + 4 * lane), make_uint4(__float_as_uint(b.x), __float_as_uint(b.y),
+                                                      __float_as_uint(b.z), __float_as_uint(b.w)));
         __syncwarp();
       }
       // fused combine: this row's (token's) routed rows, before the wait
@@ -768,23 +779,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ra[32], rb[32];
       SCMOE_TMEM_LD32(tbase, ra);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        uint32_t(&cur)[32] = (c & 1) ? rb : ra;
-        uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
+      // one chunk: cur holds its accumulator columns, nxt receives chunk c+1's
+      auto chunk = [&](int c, uint32_t(&cur)[32], uint32_t(&nxt)[32]) {
         if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
         const int n = tc.n0 + half * (BN / 2) + c * 32;
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && n + 32 <= p.N) {
-          const float* sb = brow ? sbw + c * 32 : nullptr;
-          if (fast_gelu) {
-            if (sb) epilogue_chunk_fast<true, true>(cur, sb);
-            else epilogue_chunk_fast<false, true>(cur, sb);
-          } else {
-            if (sb) epilogue_chunk_fast<true, false>(cur, sb);
-            else epilogue_chunk_fast<false, false>(cur, sb);
-          }
+          epilogue_chunk_fast<true, true>(cur, sbw + c * 32);   // fast here means GELU
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (n < p.N && wmask) {
           uint4 pre[4];
@@ -817,6 +819,48 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
             else mbar_arrive(&tempty_bar[acc]);
           }
+        }
+      };
+      // Plain / bias stores with every chunk in range: straight-line code.
+      // Everything else (GELU, residual, pre-activation, combine, tails):
+      // chunk pairs in a rolled loop (ra / rb alternate statically) — fully
+      // unrolled it overflowed the instruction cache (ncu: stall_no_inst 38%
+      // of the GELU epilogue's samples).
+      const bool plain = !WGRAD && fast && !fast_gelu && tc.n0 + (half + 1) * (BN / 2) <= p.N;
+      if (plain) {
+        auto plain_chunk = [&](auto bias_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32]) {
+          if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
+          const int n = tc.n0 + half * (BN / 2) + c * 32;
+          epilogue_chunk_fast<decltype(bias_tag)::value, false>(cur, sbw + c * 32);
+          store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
+          if (c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c == NCH - 2) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
+              else mbar_arrive(&tempty_bar[acc]);
+            }
+          }
+        };
+        if (brow) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            if (c & 1) plain_chunk(std::true_type{}, c, rb, ra);
+            else plain_chunk(std::true_type{}, c, ra, rb);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            if (c & 1) plain_chunk(std::false_type{}, c, rb, ra);
+            else plain_chunk(std::false_type{}, c, ra, rb);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < NCH; c += 2) {
+          chunk(c, ra, rb);
+          chunk(c + 1, rb, ra);
         }
       }
     }
