@@ -130,29 +130,30 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return r;
 }
 __device__ __forceinline__ float gelu_erf_fast(float x) {
-  const float z = fabsf(x) * 0.70710678118654752440f;
-  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
+  // gelu(x) = x/2 (1 + erf(x/sqrt2)) = x/2 + |x|/2 erf(|x|/sqrt2); erf by
+  // A&S 7.1.26 in t = 1/(1 + p|x|/sqrt2) (the 1/sqrt2 folded into p and into
+  // the exponent: exp(-x^2/2) = 2^(-x^2 log2(e)/2)); 12 FP ops + 2 MUFU
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752440f, fabsf(x), 1.0f));
   float p = fmaf(1.061405429f, t, -1.453152027f);
   p = fmaf(p, t, 1.421413741f);
   p = fmaf(p, t, -0.284496736f);
   p = fmaf(p, t, 0.254829592f);
   p *= t;
-  const float e = ex2_approx((z * z) * -1.44269504088896340736f);  // exp(-z^2)
+  const float e = ex2_approx((x * x) * -0.72134752044448170368f);   // exp(-x^2/2)
   const float erf_abs = fmaf(-p, e, 1.0f);
   const float hx = 0.5f * x;
-  return fmaf(hx, copysignf(erf_abs, x), hx);
+  return fmaf(fabsf(hx), erf_abs, hx);
 }
 
 // d/dz gelu(z) = Phi(z) + z * phi(z), same erf approximation (shares exp(-z^2/2))
 __device__ __forceinline__ float gelu_grad_fast(float x) {
-  const float z = fabsf(x) * 0.70710678118654752440f;
-  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752440f, fabsf(x), 1.0f));
   float p = fmaf(1.061405429f, t, -1.453152027f);
   p = fmaf(p, t, 1.421413741f);
   p = fmaf(p, t, -0.284496736f);
   p = fmaf(p, t, 0.254829592f);
   p *= t;
-  const float e = ex2_approx((z * z) * -1.44269504088896340736f);  // exp(-x^2/2)
+  const float e = ex2_approx((x * x) * -0.72134752044448170368f);   // exp(-x^2/2)
   const float erf_v = copysignf(fmaf(-p, e, 1.0f), x);
   return fmaf(0.5f, erf_v, 0.5f) + x * e * 0.39894228040143267794f;
 }

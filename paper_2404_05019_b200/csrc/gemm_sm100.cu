@@ -365,6 +365,9 @@ __device__ __forceinline__ void store_rows_staged(const uint32_t (&r)[32], uint4
 // zeros for padding rows.  The packed result replaces the accumulator in
 // place (16-B slot u = r[4u .. 4u+3], already consumed); the pre-activation
 // (aux_out) goes straight into this lane's staging slots `zs`.
+// LEAN: no fused combine and no residual (compiled out): the training
+// FFN epilogues (GELU + pre-activation store, GELU backward, zero tails)
+template <bool LEAN>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32],
                                                bool row_ok, bool pad_row, int n, const float* sb,
                                                uint4* zs, int lane, const uint4 (&pre)[4],
@@ -408,7 +411,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(z[i]);
       }
-      if (p.c_k) {
+      if (!LEAN && p.c_k) {
         // the ScMoE combine, same fp32 sequence as combine_kernel: shared
         // expert row rounded to bf16, routed rows fmaf-accumulated in
         // selection order, then se + routed, then + residual
@@ -438,7 +441,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = one * se[i] + one * rt[i];
       }
-      if (p.residual) {
+      if (!LEAN && p.residual) {
         Vec16<__nv_bfloat16> rv;
         rv.raw = pre[u];                       // residual, staged load
         float rf[8];
@@ -678,6 +681,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool fast = !WGRAD && !p.residual && !p.aux_out && !p.aux_in && !p.c_k &&
                       !p.zero_tail && (p.epi == EPI_BIAS || p.epi == EPI_BIAS_GELU);
     const bool fast_gelu = p.epi == EPI_BIAS_GELU;
+    const bool lean = !p.c_k && !p.residual;     // epilogue_chunk<true>: combine / residual compiled out
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
       const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t lmask = __ballot_sync(0xffffffffu, row_ok);
       uint4* lbuf = s_load + ew * 128;
       const long long lrow0 = ((long long)tc.g * p.cap + row_w0) * p.N;
-      auto issue_load = [&](int c) {
+      auto issue_load = [&](int c) __attribute__((always_inline)) {
         const int n = tc.n0 + half * (BN / 2) + c * 32;
         const int j = lane & 3;
 #pragma unroll
@@ -780,7 +784,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       SCMOE_TMEM_LD32(tbase, ra);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       // one chunk: cur holds its accumulator columns, nxt receives chunk c+1's
-      auto chunk = [&](int c, uint32_t(&cur)[32], uint32_t(&nxt)[32]) {
+      auto chunk = [&](auto lean_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32])
+                       __attribute__((always_inline)) {
         if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
         const int n = tc.n0 + half * (BN / 2) + c * 32;
         if (WGRAD) {
@@ -805,8 +810,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                   : make_uint4(0, 0, 0, 0);
           }
           if (arow0) __syncwarp();   // the previous flush's reads are done before z is staged
-          epilogue_chunk(p, cur, row_ok, pad_row, n, brow ? sbw + c * 32 : nullptr,
-                         arow0 ? stg : nullptr, lane, pre, cy0, cw0, cy1, cw1);
+          if (lean)
+            epilogue_chunk<true>(p, cur, row_ok, pad_row, n, brow ? sbw + c * 32 : nullptr,
+                                 arow0 ? stg : nullptr, lane, pre);
+          else
+            epilogue_chunk<false>(p, cur, row_ok, pad_row, n, brow ? sbw + c * 32 : nullptr,
+                                  arow0 ? stg : nullptr, lane, pre, cy0, cw0, cy1, cw1);
           if (arow0) stage_flush(stg, lane, arow0 + n, p.N, wmask, p.N - n);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, p.N - n);
         }
@@ -828,7 +837,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       // of the GELU epilogue's samples).
       const bool plain = !WGRAD && fast && !fast_gelu && tc.n0 + (half + 1) * (BN / 2) <= p.N;
       if (plain) {
-        auto plain_chunk = [&](auto bias_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32]) {
+        auto plain_chunk = [&](auto bias_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32])
+                               __attribute__((always_inline)) {
           if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
           const int n = tc.n0 + half * (BN / 2) + c * 32;
           epilogue_chunk_fast<decltype(bias_tag)::value, false>(cur, sbw + c * 32);
@@ -859,8 +869,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       } else {
 #pragma unroll 1
         for (int c = 0; c < NCH; c += 2) {
-          chunk(c, ra, rb);
-          chunk(c + 1, rb, ra);
+          chunk(std::true_type{}, c, ra, rb);
+          chunk(std::true_type{}, c + 1, rb, ra);
         }
       }
     }

@@ -32,6 +32,9 @@ calls = {
     "qkv dgrad": (lambda: K.grouped_gemm_ex(dqkv, wqkv, L.W_KN, d), 2 * T * d * 3 * d),
     "o dgrad": (lambda: K.grouped_gemm_ex(x, wo, L.W_KN, d), 2 * T * d * d),
     "bias grad h": (lambda: K.bias_grad(hid), 2 * T * h * 8),
+    "colsum h": (lambda: K.grouped_colsum(hid, rows, T), 2 * T * h * 8),
+    "bias grad d": (lambda: K.bias_grad(dy), 2 * T * d * 8),
+    "colsum d": (lambda: K.grouped_colsum(dy, rows, T), 2 * T * d * 8),
 }
 res_t = {}
 for _ in range(3):
