@@ -463,9 +463,10 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
 // combine): bias and GELU are compile-time, the chunk is known to be in range,
 // so the 32 values run as straight-line code — the general epilogue_chunk is
 // latency-bound on per-element checks with only 8 epilogue warps per SM.
-template <bool BIAS, bool GELU>
+template <bool BIAS, bool GELU, bool AUX = false>
 __device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
-                                                    const float* __restrict__ sb) {
+                                                    const float* __restrict__ sb,
+                                                    uint4* zs = nullptr, int lane = 0) {
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     float v[8];
@@ -481,6 +482,11 @@ __device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
       v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
     }
     if (GELU) {
+      if (AUX) {                   // pre-activation (training), into the staging slots
+        Vec16<__nv_bfloat16> z;
+        z.from_float(v);
+        stage_put(zs, lane, u, z.raw);
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = gelu_erf_fast(v[i]);
     }
@@ -678,10 +684,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int half = ew >> 2;    // accumulator columns [BN/2*half, BN/2*(half+1))
     // the fast epilogue covers bias / bias+GELU stores without residual,
     // pre-activation / GELU-backward operands, zero tails or the fused combine
-    const bool fast = !WGRAD && !p.residual && !p.aux_out && !p.aux_in && !p.c_k &&
-                      !p.zero_tail && (p.epi == EPI_BIAS || p.epi == EPI_BIAS_GELU);
+    const bool fast = !WGRAD && !p.residual && (!p.aux_out || p.epi == EPI_BIAS_GELU) &&
+                      !p.aux_in && !p.c_k && !p.zero_tail &&
+                      (p.epi == EPI_BIAS || p.epi == EPI_BIAS_GELU);
     const bool fast_gelu = p.epi == EPI_BIAS_GELU;
-    const bool lean = !p.c_k && !p.residual;     // epilogue_chunk<true>: combine / residual compiled out
+    const bool lean = !p.c_k && !p.residual;   // epilogue_chunk<true>: combine / residual out
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
       const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
@@ -791,7 +798,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && n + 32 <= p.N) {
-          epilogue_chunk_fast<true, true>(cur, sbw + c * 32);   // fast here means GELU
+          // fast here means GELU (+ the pre-activation store in training)
+          if (arow0) {
+            __syncwarp();              // the previous flush's reads are done before z is staged
+            epilogue_chunk_fast<true, true, true>(cur, sbw + c * 32, stg, lane);
+            stage_flush(stg, lane, arow0 + n, p.N, wmask, 32);
+          } else {
+            epilogue_chunk_fast<true, true>(cur, sbw + c * 32);
+          }
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (n < p.N && wmask) {
           uint4 pre[4];
