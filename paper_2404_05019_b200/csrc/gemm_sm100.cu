@@ -499,6 +499,27 @@ __device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
   }
 }
 
+// GELU backward, every column in range, no bias / residual: dZ = acc *
+// gelu'(z) with z from the staged load; padding rows (zero tails) get zeros
+__device__ __forceinline__ void epilogue_chunk_gelu_bwd(uint32_t (&r)[32], const uint4 (&pre)[4],
+                                                        bool row_ok) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    Vec16<__nv_bfloat16> zv;
+    zv.raw = pre[u];
+    float z[8], v[8];
+    zv.to_float(z);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = row_ok ? __uint_as_float(r[u * 8 + i]) * gelu_grad_fast(z[i]) : 0.f;
+    Vec16<__nv_bfloat16> w;
+    w.from_float(v);
+    r[4 * u] = w.raw.x;
+    r[4 * u + 1] = w.raw.y;
+    r[4 * u + 2] = w.raw.z;
+    r[4 * u + 3] = w.raw.w;
+  }
+}
+
 // fp32 wgrad partial: 32 columns of one output row
 __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32_t (&r)[32],
                                                    bool row_ok, bool zero, long long row_off,
@@ -539,7 +560,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
   uint4* s_stage = reinterpret_cast<uint4*>(s_bias + EPI_WARPS * 128);   // 2 KB per epilogue warp
   const int ring = C::STAGES - p.ld_buf;                                   // mainloop stages
-  uint4* s_load = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 1) * C::A_BYTES);  // if ld_buf
+  // if ld_buf: the lent stage's A slot (and its B slot when >= 16 KB) hold the
+  // per-warp load buffers, NLB chunks in flight
+  constexpr int NLB = C::B_BYTES >= 16384 ? 2 : 1;
+  uint4* s_load0 = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 1) * C::A_BYTES);
+  uint4* s_load1 = reinterpret_cast<uint4*>(smem_b + (C::STAGES - 1) * C::B_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -689,6 +714,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                       (p.epi == EPI_BIAS || p.epi == EPI_BIAS_GELU);
     const bool fast_gelu = p.epi == EPI_BIAS_GELU;
     const bool lean = !p.c_k && !p.residual;   // epilogue_chunk<true>: combine / residual out
+    // GELU backward with the pre-activation staged through the load buffer
+    const bool fast_bwd = !WGRAD && p.epi == EPI_GELU_BWD && p.ld_buf && !p.bias && !p.residual &&
+                          !p.aux_out && !p.c_k;
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
       const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
@@ -754,13 +782,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t wmask = __ballot_sync(0xffffffffu, row_ok || pad_row);
       uint4* stg = s_stage + ew * 128;
       // the row-major epilogue operand (residual / pre-activation), 32 rows x
-      // 64 B per chunk: coalesced cp.async into this warp's load buffer
-      // (same swizzle as the store staging), chunk c+1 in flight while chunk c
-      // is processed, chunk 0 issued before the accumulator wait
+      // 64 B per chunk: coalesced cp.async into this warp's load buffers
+      // (same swizzle as the store staging), chunks c+1 .. c+NLB-1 in flight
+      // while chunk c is processed, the first NLB issued before the
+      // accumulator wait
       const __nv_bfloat16* lsrc =
           WGRAD ? nullptr : (p.residual ? p.residual : (p.epi == EPI_GELU_BWD ? p.aux_in : nullptr));
       const uint32_t lmask = __ballot_sync(0xffffffffu, row_ok);
-      uint4* lbuf = s_load + ew * 128;
+      auto lbuf = [&](int c) { return ((NLB == 2 && (c & 1)) ? s_load1 : s_load0) + ew * 128; };
       const long long lrow0 = ((long long)tc.g * p.cap + row_w0) * p.N;
       auto issue_load = [&](int c) __attribute__((always_inline)) {
         const int n = tc.n0 + half * (BN / 2) + c * 32;
@@ -769,7 +798,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < 4; ++i) {
           const int rr = (lane >> 2) + 8 * i;
           if (((lmask >> rr) & 1u) && n + j * 8 < p.N) {
-            const uint32_t dst = smem_u32(lbuf + rr * 4 + (j ^ ((rr >> 1) & 3)));
+            const uint32_t dst = smem_u32(lbuf(c) + rr * 4 + (j ^ ((rr >> 1) & 3)));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                          "l"(lsrc + lrow0 + (long long)rr * p.N + n + j * 8)
                          : "memory");
@@ -777,9 +806,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       };
+      // chunk c's operand row for this lane: wait for its group, read the
+      // row, refill the buffer with chunk c + NLB
+      auto take_load = [&](int c, uint4(&pre)[4]) __attribute__((always_inline)) {
+        if (NLB == 2 && c + 1 < NCH) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          pre[u] = lds128(smem_u32(lbuf(c) + lane * 4 + (u ^ ((lane >> 1) & 3))));
+        __syncwarp();
+        if (c + NLB < NCH) issue_load(c + NLB);
+      };
       if (lsrc && p.ld_buf) {
-        __syncwarp();                  // the previous tile's reads of lbuf are done
+        asm volatile("cp.async.wait_group 0;" ::: "memory");   // nothing left from the last tile
+        __syncwarp();                  // the previous tile's reads of the buffers are done
         issue_load(0);
+        if (NLB == 2 && NCH > 1) issue_load(1);
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -807,16 +850,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             epilogue_chunk_fast<true, true>(cur, sbw + c * 32);
           }
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
+        } else if (fast_bwd && n + 32 <= p.N) {
+          uint4 pre[4];
+          take_load(c, pre);
+          epilogue_chunk_gelu_bwd(cur, pre, row_ok);
+          store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (n < p.N && wmask) {
           uint4 pre[4];
           if (lsrc && p.ld_buf) {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              pre[u] = lds128(smem_u32(lbuf + lane * 4 + (u ^ ((lane >> 1) & 3))));
-            __syncwarp();
-            if (c + 1 < NCH) issue_load(c + 1);
+            take_load(c, pre);
           } else if (lsrc) {           // no load buffer (not expected): row-per-thread loads
 #pragma unroll
             for (int u = 0; u < 4; ++u)

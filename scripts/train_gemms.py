@@ -27,6 +27,7 @@ calls = {
     "ffn2 dgrad gelu'": (lambda: K.grouped_gemm_ex(dy, w2, L.W_KN, h, aux_in=z,
                                                   epilogue=L.EPI_GELU_BWD, group_rows=rows,
                                                   rows_clip=T, zero_tail=True), 2 * T * d * h),
+    "ffn2 dgrad plain": (lambda: K.grouped_gemm_ex(dy, w2, L.W_KN, h), 2 * T * d * h),
     "ffn1 dgrad": (lambda: K.grouped_gemm_ex(hid, w1, L.W_KN, d, group_rows=rows, rows_clip=T),
                    2 * T * d * h),
     "qkv dgrad": (lambda: K.grouped_gemm_ex(dqkv, wqkv, L.W_KN, d), 2 * T * d * 3 * d),
