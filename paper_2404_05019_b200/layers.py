@@ -205,8 +205,10 @@ class Top1Gate(nn.Module):
                         w_noise_t=self.w_noise_t if self.noise_enabled else None,
                         eps=eps if self.noise_enabled else None,
                         w_split=self.presplit(x_src), stream=stream)
-        dec = GateDecision(g.logits, g.indices, g.weights, g.dropped.bool(), g.slots, g.counts,
-                           g.prob_sum, quota, quota, eps if self.noise_enabled else None)
+        # uint8 0/1 flags reinterpreted as bool: no conversion kernel
+        dec = GateDecision(g.logits, g.indices, g.weights, g.dropped.view(torch.bool), g.slots,
+                           g.counts, g.prob_sum, quota, quota,
+                           eps if self.noise_enabled else None)
         if replay is not None and replay.indices is not None:
             dec = _pin_routing(dec, replay)
         return dec
