@@ -178,6 +178,15 @@ int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out, voi
                         const int32_t* group_rows, int rows_clip, int m_out, int n_out,
                         int splits, void* stream);
 
+/* scmoe_grouped_wgrad with the output in the parameter dtype: out_dtype
+ * SCMOE_F32 or SCMOE_BF16 (the split reduction rounds once to bf16, no
+ * separate conversion pass).  A bf16 out always needs max(splits, 1) splits
+ * of workspace (W x m_out x n_out fp32 each). */
+int scmoe_grouped_wgrad_ex(const void* a, const void* b, int dtype, void* out, int out_dtype,
+                           void* workspace, size_t workspace_bytes, int num_groups, int n_wgroups,
+                           int group_cap, const int32_t* group_rows, int rows_clip, int m_out,
+                           int n_out, int splits, void* stream);
+
 /* rows [rows(g), min(cap, roundup(rows(g), align))) of every group set to 0 */
 int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_cap, int cols,
                      const int32_t* group_rows, int rows_clip, int align, void* stream);

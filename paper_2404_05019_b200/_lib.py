@@ -49,6 +49,8 @@ SIGNATURES = [
     ("scmoe_grouped_wgrad_workspace_bytes", _sz, [_i, _i, _i, _i]),
     ("scmoe_grouped_wgrad", _i, [_vp, _vp, _i, _vp, _vp, _sz, _i, _i, _i, _vp, _i, _i, _i, _i,
                                  _vp]),
+    ("scmoe_grouped_wgrad_ex", _i, [_vp, _vp, _i, _vp, _i, _vp, _sz, _i, _i, _i, _vp, _i, _i, _i,
+                                    _i, _vp]),
     ("scmoe_zero_tails", _i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _vp]),
     ("scmoe_grouped_colsum_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_grouped_colsum", _i, [_vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),

@@ -36,9 +36,10 @@ int grouped_gemm_f32(const float* a, const float* wt, const float* bias, const f
                      float* out, int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
                      int rows_clip, int N, int K, int epi, cudaStream_t st);
 size_t wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out, int splits);
-int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_t ws_bytes,
+int grouped_wgrad_bf16(const void* a, const void* b, void* out, void* ws, size_t ws_bytes,
                        int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st);
+                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st,
+                       bool out_bf16);
 
 namespace {
 
@@ -260,18 +261,29 @@ extern "C" size_t scmoe_grouped_wgrad_workspace_bytes(int n_wgroups, int m_out, 
   return wgrad_workspace_bytes(n_wgroups, m_out, n_out, splits);
 }
 
-extern "C" int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out,
-                                   void* workspace, size_t workspace_bytes, int num_groups,
-                                   int n_wgroups, int group_cap, const int32_t* group_rows,
-                                   int rows_clip, int m_out, int n_out, int splits, void* stream) {
+extern "C" int scmoe_grouped_wgrad_ex(const void* a, const void* b, int dtype, void* out,
+                                      int out_dtype, void* workspace, size_t workspace_bytes,
+                                      int num_groups, int n_wgroups, int group_cap,
+                                      const int32_t* group_rows, int rows_clip, int m_out,
+                                      int n_out, int splits, void* stream) {
   SCMOE_CHECK_ARG(dtype == SCMOE_BF16, "wgrad runs on bf16 operands");
+  SCMOE_CHECK_ARG(out_dtype == SCMOE_F32 || out_dtype == SCMOE_BF16, "wgrad out is fp32 or bf16");
   SCMOE_CHECK_ARG(num_groups >= 1 && n_wgroups >= 1 && num_groups % n_wgroups == 0,
                   "num_groups must be a positive multiple of n_wgroups");
   SCMOE_CHECK_ARG(group_cap >= 1 && m_out >= 1 && n_out >= 1, "bad wgrad shape");
   if (rows_clip <= 0) rows_clip = group_cap;
   return grouped_wgrad_bf16(a, b, out, workspace, workspace_bytes, num_groups, n_wgroups,
                             group_cap, group_rows, rows_clip, m_out, n_out, splits,
-                            (cudaStream_t)stream);
+                            (cudaStream_t)stream, out_dtype == SCMOE_BF16);
+}
+
+extern "C" int scmoe_grouped_wgrad(const void* a, const void* b, int dtype, float* out,
+                                   void* workspace, size_t workspace_bytes, int num_groups,
+                                   int n_wgroups, int group_cap, const int32_t* group_rows,
+                                   int rows_clip, int m_out, int n_out, int splits, void* stream) {
+  return scmoe_grouped_wgrad_ex(a, b, dtype, out, SCMOE_F32, workspace, workspace_bytes,
+                                num_groups, n_wgroups, group_cap, group_rows, rows_clip, m_out,
+                                n_out, splits, stream);
 }
 
 extern "C" int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_cap, int cols,

@@ -951,8 +951,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // sum of split-K partials: out[i] = sum_s part[s][i] (fp32), n multiple of 4
+// (bf16 output: the parameter-dtype gradient directly, no conversion pass)
+template <bool BF16OUT>
 __global__ void reduce_splits_kernel(const float4* __restrict__ part, int splits, long long n4,
-                                     float4* __restrict__ out) {
+                                     void* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 a = part[i];
@@ -960,7 +962,15 @@ __global__ void reduce_splits_kernel(const float4* __restrict__ part, int splits
       const float4 b = part[s * n4 + i];
       a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
     }
-    out[i] = a;
+    if (BF16OUT) {
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      uint2 v;
+      v.x = *reinterpret_cast<const uint32_t*>(&lo);
+      v.y = *reinterpret_cast<const uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[i] = v;
+    } else {
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
   }
 }
 
@@ -1129,9 +1139,12 @@ size_t wgrad_workspace_bytes(int n_wgroups, int m_out, int n_out, int splits) {
   return splits > 1 ? (size_t)splits * n_wgroups * m_out * n_out * sizeof(float) : 0;
 }
 
-int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_t ws_bytes,
+// out is fp32, or bf16 when out_bf16 (then the fp32 result always goes
+// through the workspace: at least one split's worth)
+int grouped_wgrad_bf16(const void* a, const void* b, void* out, void* ws, size_t ws_bytes,
                        int num_groups, int n_wgroups, int cap, const int32_t* group_rows,
-                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st) {
+                       int rows_clip, int m_out, int n_out, int splits, cudaStream_t st,
+                       bool out_bf16) {
   using namespace sm100;
   SCMOE_CHECK_ARG(num_groups <= MAX_GROUPS, "num_groups=%d exceeds %d", num_groups, MAX_GROUPS);
   SCMOE_CHECK_ARG(m_out % 8 == 0 && n_out % 8 == 0, "wgrad needs m_out, n_out multiples of 8");
@@ -1158,7 +1171,8 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
     if (s > kb_guess / 4) s = kb_guess / 4;
     splits = (int)(s < 1 ? 1 : (s > 64 ? 64 : s));
   }
-  SCMOE_CHECK_ARG(splits == 1 || ws_bytes >= wgrad_workspace_bytes(n_wgroups, m_out, n_out, splits),
+  const size_t one_split = (size_t)n_wgroups * m_out * n_out * sizeof(float);
+  SCMOE_CHECK_ARG(ws_bytes >= ((splits > 1 || out_bf16) ? (size_t)splits * one_split : 0),
                   "wgrad workspace too small for %d splits", splits);
   Params p = {};
   p.num_groups = num_groups;
@@ -1169,7 +1183,7 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
   p.m_out = m_out;
   p.splits = splits;
   p.group_rows = group_rows;
-  p.out_f32 = splits > 1 ? (float*)ws : out;
+  p.out_f32 = (splits > 1 || out_bf16) ? (float*)ws : (float*)out;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, a, m_out, cap, num_groups, BK);
   if (rc) return rc;
@@ -1181,9 +1195,12 @@ int grouped_wgrad_bf16(const void* a, const void* b, float* out, void* ws, size_
            : launch_bn<false, true, true>(bn, ma, mb, p, (int)units, st);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
-  if (splits > 1) {
+  if (splits > 1 || out_bf16) {
     const long long n4 = (long long)n_wgroups * m_out * n_out / 4;
-    reduce_splits_kernel<<<sms * 4, 256, 0, st>>>((const float4*)ws, splits, n4, (float4*)out);
+    if (out_bf16)
+      reduce_splits_kernel<true><<<sms * 4, 256, 0, st>>>((const float4*)ws, splits, n4, out);
+    else
+      reduce_splits_kernel<false><<<sms * 4, 256, 0, st>>>((const float4*)ws, splits, n4, out);
     SCMOE_LAUNCH_CHECK();
   }
   return SCMOE_OK;

@@ -236,8 +236,11 @@ def grouped_gemm_ex(a: torch.Tensor, w: torch.Tensor, w_layout: int, out_cols: i
 
 def grouped_wgrad(a: torch.Tensor, b: torch.Tensor, n_wgroups: int = 1,
                   group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0, splits: int = 0,
-                  out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """out[w] = sum_{g = w mod W} a[g, :rows(g)]^T @ b[g, :rows(g)] in fp32."""
+                  out: Optional[torch.Tensor] = None, stream=None,
+                  out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """out[w] = sum_{g = w mod W} a[g, :rows(g)]^T @ b[g, :rows(g)], fp32
+    accumulation; out_dtype bf16 rounds once in the split reduction (the
+    parameter-dtype gradient, no conversion pass)."""
     ensure_device(a)
     a3 = a if a.dim() == 3 else a.unsqueeze(0)
     b3 = b if b.dim() == 3 else b.unsqueeze(0)
@@ -245,13 +248,20 @@ def grouped_wgrad(a: torch.Tensor, b: torch.Tensor, n_wgroups: int = 1,
     N = b3.shape[2]
     if b3.shape[:2] != (G, C):
         raise ValueError("a and b must share (groups, rows)")
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("wgrad output is fp32 or bf16")
     if out is None:
-        out = torch.empty(n_wgroups, M, N, device=a.device, dtype=torch.float32)
+        out = torch.empty(n_wgroups, M, N, device=a.device, dtype=out_dtype)
+    elif out.dtype != out_dtype:
+        raise ValueError("out dtype differs from out_dtype")
     ws_bytes = lib().scmoe_grouped_wgrad_workspace_bytes(n_wgroups, M, N, splits)
+    if out_dtype == torch.bfloat16:
+        ws_bytes = max(ws_bytes, n_wgroups * M * N * 4)
     ws = torch.empty(max(ws_bytes, 16), device=a.device, dtype=torch.uint8)
-    check(lib().scmoe_grouped_wgrad(
-        ptr(_c(a3, "a")), ptr(_c(b3, "b")), dtype_code(a.dtype), ptr(out), ptr(ws), ws_bytes, G,
-        n_wgroups, C, ptr(group_rows), rows_clip, M, N, splits, stream_ptr(stream)))
+    check(lib().scmoe_grouped_wgrad_ex(
+        ptr(_c(a3, "a")), ptr(_c(b3, "b")), dtype_code(a.dtype), ptr(out), dtype_code(out_dtype),
+        ptr(ws), ws_bytes, G, n_wgroups, C, ptr(group_rows), rows_clip, M, N, splits,
+        stream_ptr(stream)))
     return out if (a.dim() == 3 or n_wgroups > 1) else out.view(M, N)
 
 

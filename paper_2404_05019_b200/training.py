@@ -34,6 +34,11 @@ def _as_param_grad(g: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
     return g.to(like.dtype).view(like.shape)
 
 
+def _wgrad_dtype(w: torch.Tensor) -> torch.dtype:
+    """bf16 weights get their gradient straight from the split reduction."""
+    return torch.bfloat16 if w.dtype == torch.bfloat16 else torch.float32
+
+
 class LinearFn(torch.autograd.Function):
     """y = x @ wt^T (+ residual); wt is (n_out, k_in) (bias-free projection)."""
 
@@ -52,7 +57,7 @@ class LinearFn(torch.autograd.Function):
         if ctx.needs_input_grad[0]:
             dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1])
         if ctx.needs_input_grad[1]:
-            dwt = _as_param_grad(K.grouped_wgrad(dy, x), wt)
+            dwt = _as_param_grad(K.grouped_wgrad(dy, x, out_dtype=_wgrad_dtype(wt)), wt)
         return dx, dwt, (dy if ctx.has_res else None)
 
 
@@ -96,8 +101,10 @@ class FFNFn(torch.autograd.Function):
         dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
         dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip)
-        dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
-        dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
+        dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
+                               out_dtype=_wgrad_dtype(w23))
+        dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
+                               out_dtype=_wgrad_dtype(w13))
         # bias gradients as 1^T dy on the tensor cores (sums the source groups
         # of each weight group like the weight gradients)
         db2 = K.bias_grad(dy3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)

@@ -108,6 +108,18 @@ def _wgrad_case(G, W, C, M, N, splits):
         _close(out[w] if out.dim() == 3 else out, ref, rtol=1e-2)
 
 
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_grouped_wgrad_bf16_out(splits):
+    """bf16 output = the fp32 result rounded once (same bits as .to(bf16))."""
+    g = torch.Generator(device="cuda").manual_seed(9 + splits)
+    a = torch.randn(4, 640, 384, device="cuda", generator=g).bfloat16()
+    b = torch.randn(4, 640, 1536, device="cuda", generator=g).bfloat16()
+    f32 = K.grouped_wgrad(a, b, n_wgroups=2, splits=splits)
+    b16 = K.grouped_wgrad(a, b, n_wgroups=2, splits=splits, out_dtype=torch.bfloat16)
+    assert b16.dtype == torch.bfloat16
+    assert torch.equal(b16, f32.to(torch.bfloat16))
+
+
 def test_zero_tails_and_colsum():
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn(3, 300, 128, device="cuda", generator=g).bfloat16()
