@@ -572,6 +572,25 @@ def run_ours(args):
     T = w["seq"] * w["seqs"]
     d, h = w["d"], w["h"]
     sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend)
+    ep_note = None
+    if group is not None and args.ep_backend == "p2p":
+        # map the peer buffers now (allocation + handle exchange); if any rank
+        # cannot, every rank falls back to the NCCL exchange together
+        import torch.distributed as dist
+        ok = 1
+        try:
+            for blk in (sc, t2):
+                if blk is not None:
+                    blk.moe.peer_exchange(blk.moe.gate.quota(T))
+        except Exception as e:  # pragma: no cover - depends on the box
+            print(f"p2p peer mapping failed: {e!r}", file=sys.stderr)
+            ok = 0
+        flags = [None] * dist.get_world_size()
+        dist.all_gather_object(flags, ok)
+        if not all(flags):
+            args.ep_backend = "nccl"
+            ep_note = "p2p peer mapping failed on some rank; NCCL exchange"
+            sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend)
     gen = torch.Generator(device="cuda").manual_seed(99 + rank)
     x = torch.randn(T, d, device="cuda", generator=gen).to(dtype)
 
@@ -712,6 +731,7 @@ def run_ours(args):
                    "tokens_per_gpu": T, "capacity_factor": w["cf"], "shortcut_pos": w["pos"],
                    "combine": w["combine"], "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "ep_backend": args.ep_backend if group is not None else None,
+                   "ep_note": ep_note,
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
         "speedup_vs_top2": med["t2"] / med["sc"] if "t2" in med else None,
         "ab": {"rounds": args.ab_rounds, "steps_per_round": max(3, args.steps // 2),
