@@ -69,6 +69,26 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NTHR) : "memory");
 }
 
+// Debug timeline (build with -DSCMOE_GATE_TRACE): %globaltimer per CTA at
+// entry, first stage landed, last tile published, grid-wide wait done, exit.
+#ifdef SCMOE_GATE_TRACE
+__device__ unsigned long long g_gate_trace[1024][16];
+__device__ unsigned long long g_gate_stages[1024][32];   // stage it landed (consumer warp 0)
+__device__ __forceinline__ void gate_trace_stage(uint32_t it) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 1024 && it < 32) g_gate_stages[blockIdx.x][it] = t;
+}
+__device__ __forceinline__ void gate_trace(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 1024) g_gate_trace[blockIdx.x][i] = t;   // last write wins (last tile)
+}
+#else
+__device__ __forceinline__ void gate_trace(int) {}
+__device__ __forceinline__ void gate_trace_stage(uint32_t) {}
+#endif
+
 // Phase 2, shared by both logit kernels, in two halves so the tensor-core
 // kernel can run the look-back of tile i after the logits of tile i+1:
 //   route_publish — one thread per token: top-k (strict '>', lowest index
@@ -192,7 +212,9 @@ __device__ __forceinline__ void route_publish(
       }
     }
   }
+  if (LOCAL && tid == 0) gate_trace(10);
   consumer_sync<THREADS_, BAR>();
+  if (LOCAL && tid == 0) gate_trace(11);
 
   // per-expert tile aggregate and within-tile warp offsets; publish the
   // aggregate at once so later tiles can make progress
@@ -218,7 +240,9 @@ __device__ __forceinline__ void route_publish(
     }
   }
   if (!LOCAL && tid == 0) rs.tile = tile;
+  if (LOCAL && tid == 0) gate_trace(12);
   consumer_sync<THREADS_, BAR>();
+  if (LOCAL && tid == 0) gate_trace(13);
   if (valid) {
 #pragma unroll
     for (int j = 0; j < SCMOE_MAX_K; ++j) {
@@ -617,6 +641,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkc = (d + GT_KC - 1) / GT_KC;
   if (tid == 0) {
+    gate_trace(0);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], GT_CONSUMERS);
@@ -646,10 +671,12 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
       mbar_wait(&lfull_bar[b], (n >> 1) & 1);
       const int tile = s_logit_tile[b];
       if (tile < 0) break;
+      if (rtid == 0) gate_trace(5);
       route_publish<NMAX, TOK, RT, GT_ROUTE_BASE, 2, true>(
           s_logit[b], rs, tile, exclude, n_tok, N, k, logits, indices, weights, counts, status,
           psum, slots, (n < LCACHE_TILES && k <= 2) ? s_lcache[n] : nullptr);
       __syncwarp();
+      if (rtid == 0) gate_trace(6);
       if (lane == 0) mbar_arrive(&lempty_bar[b]);   // publish read s_logit[b] before its barrier
       // every router thread's writes -> CTA barrier -> one release add (cumulative):
       // no per-thread fence (a __threadfence is a MEMBAR.SC.GPU per thread)
@@ -658,11 +685,13 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctrs + 2) : "memory");
     }
     if (rtid == 0) {
+      gate_trace(2);
       const long long t0 = clock64();
       while (ld_acquire_gpu(ctrs + 2) < (uint32_t)num_tiles) {
         __nanosleep(200);
         if (clock64() - t0 > (40LL << 30)) __trap();   // ~20 s: never hang the GPU
       }
+      gate_trace(3);
     }
     consumer_sync<RT, 2>();
     // the stage ring is idle now: load the whole (tiles, N) count table (and
@@ -739,6 +768,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
         prob_sum[rtid] = fs;
       }
     }
+    if (rtid == 0) gate_trace(4);
     return;
   }
 
@@ -802,6 +832,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
     for (int kc = 0; kc < nkc; ++kc, ++it) {
       const int s = it % S;
       mbar_wait(&full_bar[s], (it / S) & 1);
+      if (it == 0 && tid == 0) gate_trace(1);
+      if (tid == 0) gate_trace_stage(it);
       tile = s_stage_tile[s];
       if (tile < 0) break;
       const uint8_t* st = gsm + (size_t)s * C::STAGEB;
@@ -826,7 +858,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
     const int b = n & 1;
+    if (tid == 0 && tile >= 0) gate_trace(7);
     mbar_wait(&lempty_bar[b], ((n >> 1) & 1) ^ 1);      // routing done with buffer b
+    if (tid == 0 && tile >= 0) gate_trace(8);
     if (tile >= 0) {
       // partial logits, smallest weight part first; C fragment rows g / g+8,
       // experts nt*8 + 2c + {0,1}
@@ -849,6 +883,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
     }
     if (tid == 0) s_logit_tile[b] = tile;
     consumer_sync<GT_CONSUMERS * 32>();   // s_part reads done before the next tile's writes
+    if (tid == 0 && tile >= 0) gate_trace(9);
     if (lane == 0) mbar_arrive(&lfull_bar[b]);
     if (tile < 0) break;
   }
@@ -1086,3 +1121,16 @@ extern "C" int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld
                                slots, dropped, counts, prob_sum, workspace, workspace_bytes,
                                stream);
 }
+
+#ifdef SCMOE_GATE_TRACE
+extern "C" int scmoe_debug_gate_trace(unsigned long long* host, int n_ctas) {
+  return cudaMemcpyFromSymbol(host, scmoe::g_gate_trace, (size_t)n_ctas * 16 * 8) == cudaSuccess
+             ? 0
+             : 1;
+}
+extern "C" int scmoe_debug_gate_stages(unsigned long long* host, int n_ctas) {
+  return cudaMemcpyFromSymbol(host, scmoe::g_gate_stages, (size_t)n_ctas * 32 * 8) == cudaSuccess
+             ? 0
+             : 1;
+}
+#endif
