@@ -350,6 +350,20 @@ def timed(fn, steps, ws, recorder_factory=None):
     return max_over_ranks(ms, ws), recs
 
 
+def block_pair_flops(w, T, kept_rows, n_experts):
+    """Matmul FLOPs of one step of the workload on one rank: attention
+    (QKV 6d^2, O 2d^2 per token; scores + PV 4 S_eff d, S_eff = (S+1)/2
+    causal), the Block-MLP (pair placement only), the shared expert on every
+    token, the routed experts on the kept rows (4 d h each) and the gate."""
+    d, h, S = w["d"], w["h"], w["seq"]
+    s_eff = (S + 1) / 2 if w.get("causal") else S
+    attn = T * (8.0 * d * d + 4.0 * s_eff * d)
+    ffn = 4.0 * d * h
+    pair = not w.get("every_block")
+    return ((2 if pair else 1) * attn + (T * ffn if pair else 0.0) + T * ffn
+            + kept_rows * ffn + 2.0 * T * d * n_experts)
+
+
 def hbm_kernel_times(moe, x, reps: int = 10):
     """Per-launch device time of the HBM-bound hot-path ops (K1 gate, K2
     dispatch, K5 combine) at the bench shape: each op captured in a CUDA graph,
@@ -719,6 +733,11 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # whole-step model FLOPs (all matmuls of the block pair on this rank)
+    n_gate = sc.moe.n_experts
+    step_flops = block_pair_flops(w, T, kept_rows, n_gate)
+    step_tf = step_flops / (ms_sc * 1e-3) / 1e12
+
     value = ws * T / (ms_sc * 1e-3)
     t2_value = ws * T / (ms_t2 * 1e-3) if ms_t2 else None
     line = {
@@ -752,6 +771,11 @@ def run_ours(args):
                      "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
                      "kernel": "scmoe::sm100::grouped_gemm_kernel (routed expert FFN)",
                      "flops_per_launch": flops_per_launch, "peak_source": peak_src},
+        "model_flops": {"per_step_per_gpu": step_flops, "achieved_tflops": step_tf,
+                        "frac_of_sustained": step_tf / peak_tf,
+                        "note": "every matmul of the step: QKV / O / SDPA (causal: half the "
+                                "score matrix), Block-MLP, shared expert, routed experts on "
+                                "the kept rows, gate"},
         "clocks": clocks,
         "hbm_kernels": None if hbm_ops is None else {
             k: dict(v, peak=peaks.get("hbm_gbs"), frac=v["gbps"] / peaks["hbm_gbs"]
