@@ -72,7 +72,7 @@ __device__ __forceinline__ void consumer_sync() {
 // Debug timeline (build with -DSCMOE_GATE_TRACE): %globaltimer per CTA at
 // entry, first stage landed, last tile published, grid-wide wait done, exit.
 #ifdef SCMOE_GATE_TRACE
-__device__ unsigned long long g_gate_trace[1024][16];
+__device__ unsigned long long g_gate_trace[1024][20];
 __device__ unsigned long long g_gate_stages[1024][32];   // stage it landed (consumer warp 0)
 __device__ __forceinline__ void gate_trace_stage(uint32_t it) {
   unsigned long long t;
@@ -128,11 +128,13 @@ __device__ __forceinline__ void route_publish(
     float h[NMAX];
 #pragma unroll
     for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tid][e] : 0.f;
+    if (LOCAL && tid == 0) gate_trace(14);
     if (valid) {
 #pragma unroll
       for (int e = 0; e < NMAX; ++e)
         if (e < N) logits[(long long)t * N + e] = h[e];
     }
+    if (LOCAL && tid == 0) gate_trace(15);
     // top-k: repeated argmax with strict '>' (lowest index wins ties).  An
     // excluded expert (DGMoE distinct-expert constraint, arch.py:453-457) is
     // skipped, so the pick becomes the runner-up exactly when it would clash.
@@ -165,7 +167,10 @@ __device__ __forceinline__ void route_publish(
         selmask |= 1ull << bi;
       }
     }
-    if (valid) {
+    if (valid && k == 1) {          // top-1: the kept-logit softmax is exactly 1
+      indices[t] = sel[0];
+      weights[t] = 1.0f;
+    } else if (valid) {
 #pragma unroll
       for (int j = 0; j < SCMOE_MAX_K; ++j) {
         if (j < k) {
@@ -180,6 +185,7 @@ __device__ __forceinline__ void route_publish(
         }
       }
     }
+    if (LOCAL && tid == 0) gate_trace(16);
     // full-softmax probabilities for the balance-loss mean (arch.py:484-485)
     float mx = -INFINITY;
 #pragma unroll
@@ -193,21 +199,53 @@ __device__ __forceinline__ void route_publish(
       den += ex[e];
     }
     const float inv = 1.f / den;
+    if (LOCAL && tid == 0) gate_trace(17);
     const unsigned lt = (1u << lane) - 1u;
+    if constexpr (NMAX <= 16) {
+      // all experts' ballots first, then their warp sums as one interleaved
+      // butterfly (same xor order as warp_sum: bit-identical) — one expert at
+      // a time was ~1.4 us of dependent shuffles per tile (gate trace)
+      unsigned bal[NMAX];
+      float pv[NMAX];
 #pragma unroll
-    for (int e = 0; e < NMAX; ++e) {
-      if (e < N) {
-        const bool mine = valid && ((selmask >> e) & 1ull);
-        const unsigned b = __ballot_sync(0xffffffffu, mine);
-        const float p = warp_sum(valid ? ex[e] * inv : 0.f);
-        if (lane == 0) {
-          s_wcnt[warp][e] = __popc(b);
-          s_wprob[warp][e] = p;
+      for (int e = 0; e < NMAX; ++e) {
+        bal[e] = __ballot_sync(0xffffffffu, valid && e < N && ((selmask >> e) & 1ull));
+        pv[e] = (valid && e < N) ? ex[e] * inv : 0.f;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int e = 0; e < NMAX; ++e) pv[e] += __shfl_xor_sync(0xffffffffu, pv[e], o);
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e) {
+        if (e < N) {
+          if (lane == 0) {
+            s_wcnt[warp][e] = __popc(bal[e]);
+            s_wprob[warp][e] = pv[e];
+          }
+          if (valid && ((selmask >> e) & 1ull)) {
+#pragma unroll
+            for (int j = 0; j < SCMOE_MAX_K; ++j)
+              if (j < k && sel[j] == e) rank[j] = __popc(bal[e] & lt);
+          }
         }
-        if (mine) {
+      }
+    } else {
 #pragma unroll
-          for (int j = 0; j < SCMOE_MAX_K; ++j)
-            if (j < k && sel[j] == e) rank[j] = __popc(b & lt);
+      for (int e = 0; e < NMAX; ++e) {
+        if (e < N) {
+          const bool mine = valid && ((selmask >> e) & 1ull);
+          const unsigned b = __ballot_sync(0xffffffffu, mine);
+          const float p = warp_sum(valid ? ex[e] * inv : 0.f);
+          if (lane == 0) {
+            s_wcnt[warp][e] = __popc(b);
+            s_wprob[warp][e] = p;
+          }
+          if (mine) {
+#pragma unroll
+            for (int j = 0; j < SCMOE_MAX_K; ++j)
+              if (j < k && sel[j] == e) rank[j] = __popc(b & lt);
+          }
         }
       }
     }
@@ -1124,7 +1162,7 @@ extern "C" int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld
 
 #ifdef SCMOE_GATE_TRACE
 extern "C" int scmoe_debug_gate_trace(unsigned long long* host, int n_ctas) {
-  return cudaMemcpyFromSymbol(host, scmoe::g_gate_trace, (size_t)n_ctas * 16 * 8) == cudaSuccess
+  return cudaMemcpyFromSymbol(host, scmoe::g_gate_trace, (size_t)n_ctas * 20 * 8) == cudaSuccess
              ? 0
              : 1;
 }

@@ -25,12 +25,13 @@ for rep in range(4):
     torch.cuda.synchronize()
     K.gate_topk(x, w, 1, quota, w_split=ws)
     torch.cuda.synchronize()
-buf = np.zeros((ctas, 16), dtype=np.uint64)
+buf = np.zeros((ctas, 20), dtype=np.uint64)
 assert fn(buf.ctypes.data, ctas) == 0
 t0 = buf[:, 0].min()
 r = (buf.astype(np.int64) - int(t0)) / 1e3
 names = ["entry", "stage0", "published", "wait_done", "exit", "rt_got", "rt_done", "mma_done",
-         "lempty_ok", "logits_out", "rp_a", "rp_sync1", "rp_b", "rp_sync2"]
+         "lempty_ok", "logits_out", "rp_a", "rp_sync1", "rp_b", "rp_sync2",
+         "rp_h_loaded", "rp_logits_st", "rp_topk_w", "rp_softmax"]
 for i, n in enumerate(names):
     col = r[:, i]
     print(f"{n:10s} min {col.min():7.2f}  median {np.median(col):7.2f}  max {col.max():7.2f} us")
