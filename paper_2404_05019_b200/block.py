@@ -88,6 +88,13 @@ class _CudnnPackedAttention(torch.autograd.Function):
         return dqkv.view(b * s, 3 * h * hd), None, None, None, None, None
 
 
+def _raise_if_nonfinite(loss: torch.Tensor) -> None:
+    """grad.backward's divergence check (grad.py:84-85): FloatingPointError on
+    a non-finite loss, before any parameter is updated."""
+    if not bool(torch.isfinite(loss.detach()).all()):
+        raise FloatingPointError("non-finite loss")
+
+
 def _use_packed_attention(qkv: torch.Tensor, hd: int) -> bool:
     if not PACKED_ATTENTION or qkv.dtype != torch.bfloat16 or hd > 256 or hd % 8:
         return False
@@ -592,12 +599,15 @@ class ScMoEBlockPair(nn.Module):
 
     # -- training ----------------------------------------------------------------
     def train_step(self, h_in: torch.Tensor, lr: float = 0.01, aux_coeff: float = 0.01,
-                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True):
+                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True,
+                   check_finite: bool = False):
         """One optimisation step of the reference objective (grad.py:52-67):
         loss = mean(out) (or sum((out - target)^2) / T, LossSpec "mse") +
         aux_coeff * aux, backward through the K7 kernels, data-parallel
         all-reduce of the replicated parameters (N > 1), in-place SGD
-        (grad.py:330-331).  Returns the loss (device tensor, no sync)."""
+        (grad.py:330-331).  Returns the loss (device tensor, no sync).
+        check_finite: raise FloatingPointError("non-finite loss") before the
+        update, as grad.backward does (grad.py:84-85) — one host sync."""
         from . import training as TR
         for p in self.parameters():
             p.grad = None
@@ -608,6 +618,8 @@ class ScMoEBlockPair(nn.Module):
             loss = (out.float() - target.float()).pow(2).sum() / out.shape[0]
         loss = loss + aux_coeff * aux
         loss.backward()
+        if check_finite:
+            _raise_if_nonfinite(loss)
         if dp_group is not None or self.ep_group is not None:
             TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else self.ep_group)
         if update:
@@ -740,8 +752,10 @@ class ScMoEModel(nn.Module):
         return h, decs, auxes
 
     def train_step(self, tokens: torch.Tensor, lr: float = 0.01, aux_coeff: float = 0.01,
-                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True):
-        """grad.compute_loss (mean / mse + aux_coeff * sum aux) + SGD."""
+                   target: Optional[torch.Tensor] = None, dp_group=None, update: bool = True,
+                   check_finite: bool = False):
+        """grad.compute_loss (mean / mse + aux_coeff * sum aux) + SGD;
+        check_finite as in ScMoEBlockPair.train_step (grad.py:84-85)."""
         from . import training as TR
         for p in self.parameters():
             p.grad = None
@@ -751,6 +765,8 @@ class ScMoEModel(nn.Module):
         for a in auxes:
             loss = loss + aux_coeff * a
         loss.backward()
+        if check_finite:
+            _raise_if_nonfinite(loss)
         ep = self.blocks[0].ep_group if len(self.blocks) else None
         if dp_group is not None or ep is not None:
             TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else ep)

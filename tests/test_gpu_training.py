@@ -119,3 +119,20 @@ def test_train_step_reduces_loss_and_updates():
     assert losses[-1] < losses[0]
     assert not torch.equal(w_before, blk.moe.experts.w1t.detach())
     assert all(np.isfinite(losses))
+
+
+def test_train_step_nonfinite_loss_raises_before_update():
+    """check_finite: a non-finite loss raises FloatingPointError and leaves the
+    parameters untouched (grad.py:84-85, 322-323)."""
+    T, d, h, N = 256, 128, 256, 4
+    blk = P.ScMoEBlockPair(d, h, N, variant="scmoe", shortcut_pos="pos2", n_heads=2, seq_len=128,
+                           capacity_factor=1.25, dtype=torch.bfloat16,
+                           generator=torch.Generator(device="cuda").manual_seed(7))
+    blk.requires_grad_(True)
+    x = torch.randn(T, d, device="cuda").bfloat16()
+    target = torch.full((T, d), float("inf"), device="cuda").bfloat16()
+    w_before = blk.moe.experts.w1t.detach().clone()
+    with pytest.raises(FloatingPointError, match="non-finite loss"):
+        blk.train_step(x, lr=1e-3, target=target, check_finite=True)
+    assert torch.equal(w_before, blk.moe.experts.w1t.detach())
+    assert torch.isfinite(blk.train_step(x, lr=1e-3, check_finite=True)).item()
