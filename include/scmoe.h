@@ -220,12 +220,6 @@ int scmoe_set_gemm_mode(int mode);
  * multiple of 128 and the narrow tile needs fewer column-waves), 128 or 256. */
 int scmoe_set_gemm_tile_n(int bn);
 
-/* Tuning / test hook: 1 (default) = grouped 2-SM GEMMs with device row counts
- * run each group's whole 256-row tiles on the 2-SM kernel and its remaining
- * rows in 128-row tiles on the 1-SM kernel; 0 = one launch, partial tiles
- * padded. */
-int scmoe_set_gemm_tail_split(int on);
-
 /*
  * Full expert_forward (arch.py:349-351) over groups: GEMM1 (bias+GELU) into
  * `hidden` (num_groups, group_cap, d_hidden), then GEMM2 (bias, + residual

@@ -43,7 +43,6 @@ SIGNATURES = [
                                 _vp]),
     ("scmoe_set_gemm_mode", _i, [_i]),
     ("scmoe_set_gemm_tile_n", _i, [_i]),
-    ("scmoe_set_gemm_tail_split", _i, [_i]),
     ("scmoe_gather_rows", _i, [_vp, _sz, _vp, _vp, _i, _vp, _vp]),
     ("scmoe_grouped_gemm_ex", _i, [_vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                    _i, _i, _i, _i, _i, _vp]),

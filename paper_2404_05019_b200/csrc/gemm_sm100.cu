@@ -81,11 +81,6 @@ enum Epi { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GELU_BWD = 2 };
 
 struct Params {
   int num_groups, n_wgroups, cap, rows_clip, N, K, epi, zero_tail;
-  // row tiling of each group (rows mode): 0 all rows in TILE_M tiles; 1 only
-  // the whole 256-row tiles (2-SM launch); 2 only the rows past them, in
-  // 128-row tiles (1-SM launch) — the split that keeps partial 256-row tiles
-  // of the routed experts off the 2-SM tensor cores
-  int tile_mode;
   int m_out, splits;                       // wgrad only
   const int32_t* group_rows;
   const float* bias;
@@ -294,7 +289,6 @@ __device__ __forceinline__ Tile decode_tile(const Params& p, int t, int n_tiles_
     }
     c.g = lo;
     c.m0 = (r - prefix[lo]) * TILE_M;
-    if (p.tile_mode == 2) c.m0 += group_rows_of(p, lo) / 256 * 256;   // past the whole tiles
     c.s = 0;
     c.kb_lo = 0;
     c.kb_hi = (p.K + BK - 1) / BK;
@@ -620,12 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int base = 0; base < p.num_groups; base += 32) {
         const int g = base + lane;
         int v = 0;
-        if (g < p.num_groups) {
-          const int rg = group_rows_of(p, g);
-          v = p.tile_mode == 1   ? rg / 256
-              : p.tile_mode == 2 ? (rg - rg / 256 * 256 + 127) / 128
-                                 : (rg + C::TILE_M - 1) / C::TILE_M;
-        }
+        if (g < p.num_groups) v = (group_rows_of(p, g) + C::TILE_M - 1) / C::TILE_M;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int u = __shfl_up_sync(0xffffffffu, v, o);
@@ -1058,9 +1047,6 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
 static int g_gemm_mode = 0;
 // tile width: 0 auto, 128 or 256 forced (tests / tuning)
 static int g_gemm_bn = 0;
-// grouped 2-SM launches with device row counts: whole 256-row tiles on the
-// 2-SM kernel, the rest of each group in 128-row tiles on the 1-SM kernel
-static int g_tail_split = 1;
 
 // Forward / dgrad tile width: 256 unless forced.  Measured on the configs[1]
 // shapes (scripts/ab_gemm_cublas.py train): BN = 128 loses even where it
@@ -1138,13 +1124,6 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   const int b_rows = two ? bn / 2 : bn;
   rc = b_mn ? make_map(&mb, wt, N, K, n_wgroups, BK) : make_map(&mb, wt, K, N, n_wgroups, b_rows);
   if (rc) return rc;
-  // routed experts (several groups, rows known only on the device, no zero
-  // tails): a group's last partial 256-row tile would run the 2-SM MMAs on
-  // mostly padding rows (~2048 +- 50 rows per expert at configs[2] leaves a
-  // near-empty ninth tile on half the experts), so those rows go to a second,
-  // 1-SM launch in 128-row tiles
-  const bool split = two && g_tail_split && group_rows && !zero_tail && num_groups > 1 && !cs;
-  if (split) p.tile_mode = 1;
   if (two)
     rc = b_mn ? launch_bn<true, true, false>(bn, ma, mb, p, (int)units * 2, st)
               : launch_bn<true, false, false>(bn, ma, mb, p, (int)units * 2, st);
@@ -1153,19 +1132,6 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
               : launch_bn<false, false, false>(bn, ma, mb, p, (int)units, st);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
-  if (split) {
-    Params q = p;
-    q.tile_mode = 2;
-    CUtensorMap mb1;
-    rc = b_mn ? make_map(&mb1, wt, N, K, n_wgroups, BK) : make_map(&mb1, wt, K, N, n_wgroups, bn);
-    if (rc) return rc;
-    const long long tail_tiles = (long long)num_groups * 2 * ((N + bn - 1) / bn);
-    const int grid = (int)(tail_tiles < sms ? tail_tiles : sms);
-    rc = b_mn ? launch_bn<false, true, false>(bn, ma, mb1, q, grid, st)
-              : launch_bn<false, false, false>(bn, ma, mb1, q, grid, st);
-    if (rc) return rc;
-    SCMOE_LAUNCH_CHECK();
-  }
   return SCMOE_OK;
 }
 
@@ -1272,11 +1238,6 @@ extern "C" int scmoe_set_gemm_mode(int mode) {
     return SCMOE_ERR_ARG;
   }
   scmoe::g_gemm_mode = mode;
-  return SCMOE_OK;
-}
-
-extern "C" int scmoe_set_gemm_tail_split(int on) {
-  scmoe::g_tail_split = on ? 1 : 0;
   return SCMOE_OK;
 }
 

@@ -195,12 +195,6 @@ def set_gemm_mode(mode: int) -> None:
     check(lib().scmoe_set_gemm_mode(mode))
 
 
-def set_gemm_tail_split(on: bool) -> None:
-    """Grouped 2-SM GEMMs: run each group's partial last 256-row tile as
-    128-row tiles on the 1-SM kernel (default on)."""
-    check(lib().scmoe_set_gemm_tail_split(1 if on else 0))
-
-
 def set_gemm_tile_n(bn: int) -> None:
     """0 = auto, 128 or 256 = force the tcgen05 tile width (N per tile)."""
     check(lib().scmoe_set_gemm_tile_n(bn))

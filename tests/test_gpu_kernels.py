@@ -300,40 +300,3 @@ def test_gate_presplit_equals_per_call_split():
     torch.cuda.synchronize()
     assert torch.equal(d2.indices, ref.indices) and torch.equal(d2.slots, ref.slots)
     assert not torch.equal(d1.indices, d2.indices)
-
-
-@pytest.mark.parametrize("residual", [False, True])
-def test_grouped_gemm_tail_split(residual):
-    """Routed-expert shape: whole 256-row tiles on the 2-SM kernel, the rest
-    of each group in 128-row tiles on the 1-SM kernel.  Same rows as one
-    padded launch, rows past each count untouched."""
-    G, C, Kd, N = 8, 2304, 512, 1024
-    g = torch.Generator(device="cuda").manual_seed(21)
-    a = torch.randn(G, C, Kd, device="cuda", generator=g).bfloat16()
-    wt = (torch.randn(G, N, Kd, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
-    bias = torch.randn(G, N, device="cuda", generator=g) * 0.1
-    res = torch.randn(G, C, N, device="cuda", generator=g).bfloat16() if residual else None
-    rows = torch.tensor([2000, 2100, 256, 300, 0, 511, 1, 2048], device="cuda", dtype=torch.int32)
-    outs = []
-    try:
-        K.set_gemm_mode(2)
-        for split in (True, False):
-            K.set_gemm_tail_split(split)
-            out = torch.full((G, C, N), float("nan"), device="cuda", dtype=torch.bfloat16)
-            K.grouped_gemm(a, wt, bias, group_rows=rows, rows_clip=C, gelu=True, out=out,
-                           residual=res)
-            outs.append(out)
-        torch.cuda.synchronize()
-    finally:
-        K.set_gemm_tail_split(True)
-        K.set_gemm_mode(0)
-    for gi, r in enumerate(rows.tolist()):
-        got, pad = outs[0][gi, :r].float(), outs[1][gi, :r].float()
-        assert torch.allclose(got, pad, rtol=1e-2, atol=1e-2), gi
-        if r:
-            ref = _ref_ffn_rows(a[gi, :r], wt[gi], bias[gi], True)
-            if res is not None:
-                ref = ref + res[gi, :r].double()
-            tol = 2e-2 * (ref.abs() + ref.abs().max())
-            assert ((got.double() - ref).abs() <= tol).all(), gi
-        assert torch.isnan(outs[0][gi, r:].float()).all(), gi
