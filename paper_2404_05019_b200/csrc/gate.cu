@@ -124,12 +124,55 @@ __device__ __forceinline__ void route_publish(
   int rank[SCMOE_MAX_K];
   const int t = tile * TOK_ + tid;
   const bool valid = (tid < TOK_) && (t < n_tok);
+  // SPLIT (tensor-core gate, <= 16 experts, >= 2 threads per token): a
+  // second thread per token (tid - TOK_) writes the logits and computes the
+  // full-softmax probability sums while the first runs top-k, ballots and
+  // ranks — the per-token routing of a CTA's last tile is exposed latency
+  // (gate trace).  Same arithmetic and summation order: bit-identical.
+  constexpr bool SPLIT = LOCAL && NMAX <= 16 && THREADS_ >= 2 * TOK_;
+  if (SPLIT && tid >= TOK_ && tid < 2 * TOK_) {
+    const int tok = tid - TOK_;
+    const int tb = tile * TOK_ + tok;
+    const bool vb = tb < n_tok;
+    float h[NMAX];
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tok][e] : 0.f;
+    if (vb) {
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e)
+        if (e < N) logits[(long long)tb * N + e] = h[e];
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e)
+      if (e < N) mx = fmaxf(mx, h[e]);
+    float ex[NMAX];
+    float den = 0.f;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) {
+      ex[e] = (e < N) ? expf(h[e] - mx) : 0.f;
+      den += ex[e];
+    }
+    const float inv = 1.f / den;
+    float pv[NMAX];
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) pv[e] = (vb && e < N) ? ex[e] * inv : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e) pv[e] += __shfl_xor_sync(0xffffffffu, pv[e], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e)
+        if (e < N) s_wprob[tok >> 5][e] = pv[e];
+    }
+  }
   if (tid < TOK_) {
     float h[NMAX];
 #pragma unroll
     for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tid][e] : 0.f;
     if (LOCAL && tid == 0) gate_trace(14);
-    if (valid) {
+    if (!SPLIT && valid) {
 #pragma unroll
       for (int e = 0; e < NMAX; ++e)
         if (e < N) logits[(long long)t * N + e] = h[e];
@@ -187,18 +230,21 @@ __device__ __forceinline__ void route_publish(
     }
     if (LOCAL && tid == 0) gate_trace(16);
     // full-softmax probabilities for the balance-loss mean (arch.py:484-485)
+    // (SPLIT: computed by the token's second thread above)
     float mx = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < NMAX; ++e)
-      if (e < N) mx = fmaxf(mx, h[e]);
     float ex[NMAX];
     float den = 0.f;
+    if constexpr (!SPLIT) {
 #pragma unroll
-    for (int e = 0; e < NMAX; ++e) {
-      ex[e] = (e < N) ? expf(h[e] - mx) : 0.f;
-      den += ex[e];
+      for (int e = 0; e < NMAX; ++e)
+        if (e < N) mx = fmaxf(mx, h[e]);
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e) {
+        ex[e] = (e < N) ? expf(h[e] - mx) : 0.f;
+        den += ex[e];
+      }
     }
-    const float inv = 1.f / den;
+    const float inv = SPLIT ? 0.f : 1.f / den;
     if (LOCAL && tid == 0) gate_trace(17);
     const unsigned lt = (1u << lane) - 1u;
     if constexpr (NMAX <= 16) {
@@ -210,18 +256,20 @@ __device__ __forceinline__ void route_publish(
 #pragma unroll
       for (int e = 0; e < NMAX; ++e) {
         bal[e] = __ballot_sync(0xffffffffu, valid && e < N && ((selmask >> e) & 1ull));
-        pv[e] = (valid && e < N) ? ex[e] * inv : 0.f;
+        if constexpr (!SPLIT) pv[e] = (valid && e < N) ? ex[e] * inv : 0.f;
       }
+      if constexpr (!SPLIT) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int e = 0; e < NMAX; ++e) pv[e] += __shfl_xor_sync(0xffffffffu, pv[e], o);
+          for (int e = 0; e < NMAX; ++e) pv[e] += __shfl_xor_sync(0xffffffffu, pv[e], o);
+      }
 #pragma unroll
       for (int e = 0; e < NMAX; ++e) {
         if (e < N) {
           if (lane == 0) {
             s_wcnt[warp][e] = __popc(bal[e]);
-            s_wprob[warp][e] = pv[e];
+            if constexpr (!SPLIT) s_wprob[warp][e] = pv[e];
           }
           if (valid && ((selmask >> e) & 1ull)) {
 #pragma unroll
