@@ -367,8 +367,8 @@ def block_pair_flops(w, T, kept_rows, n_experts):
 def hbm_kernel_times(moe, x, reps: int = 10):
     """Per-launch device time of the HBM-bound hot-path ops (K1 gate, K2
     dispatch, K5 combine) at the bench shape: each op captured in a CUDA graph,
-    L2 flushed (512 MB read) before every replay, CUDA events around the
-    replay alone, median over `reps`.  Algorithmic bytes:
+    L2 flushed (512 MB read) before every replay, the op's kernel durations
+    from CUPTI (sum per replay, mean over `reps`).  Algorithmic bytes:
     gate T*d*s + T*N*4, dispatch 2*kept*d*s, combine (k+3)*T*d*s."""
     import torch
     from paper_2404_05019_b200 import kernels as K
@@ -405,18 +405,24 @@ def hbm_kernel_times(moe, x, reps: int = 10):
                 fn()
         st.wait_stream(cs)
         torch.cuda.synchronize()
-        ts = []
-        for i in range(reps + 2):
+        for _ in range(2):
             flush.sum()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
             g.replay()
-            e1.record(st)
+        torch.cuda.synchronize()
+        # device time of the op's own kernels (and memset nodes) per replay,
+        # from CUPTI: immune to the graph-launch gap after the flush that
+        # CUDA events around the replay would also count
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(reps):
+                flush.sum()
+                g.replay()
             torch.cuda.synchronize()
-            if i >= 2:
-                ts.append(e0.elapsed_time(e1) * 1e3)
-        us = statistics.median(ts)
-        res_d[name] = {"us": us, "bytes": nbytes, "gbps": nbytes / us / 1e3}
+        dev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+        own = [e for e in dev if "reduce_kernel" not in e.name]   # drop the flush's sum
+        us = sum(getattr(e, "device_time_total", 0.0) or e.cuda_time_total for e in own) / reps
+        res_d[name] = {"us": us, "bytes": nbytes, "gbps": nbytes / us / 1e3,
+                       "kernels": sorted({e.name.split("(")[0][-60:] for e in own})}
     del flush
     return res_d
 
@@ -780,6 +786,9 @@ def run_ours(args):
         "hbm_kernels": None if hbm_ops is None else {
             k: dict(v, peak=peaks.get("hbm_gbs"), frac=v["gbps"] / peaks["hbm_gbs"]
                     if peaks.get("hbm_gbs") else None) for k, v in hbm_ops.items()},
+        "hbm_kernels_note": "CUPTI durations of each op's kernels after a 512 MB read flush of "
+                            "L2; the op's writes can still be draining from L2 when its kernel "
+                            "ends, so frac may exceed 1 against the measured copy peak",
         "gpu_launches": args.steps * own_per_step,
         "launches_per_step": {"scmoe": own_per_step, "library": lib_per_step,
                               "how": "torch.profiler (CUPTI) over one step; 'scmoe' = kernels of "
