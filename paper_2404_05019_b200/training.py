@@ -86,6 +86,9 @@ class FFNFn(torch.autograd.Function):
         ctx.save_for_backward(x3, z, hid, w13, w23, group_rows)
         ctx.meta = (two_d, rows_clip, residual is not None, b1.shape, b2.shape, w1t.shape,
                     w2t.shape)
+        # y = FFN(x) + x (the Block-MLP): the data gradient adds dy in its
+        # GEMM epilogue instead of a separate autograd add
+        ctx.res_is_x = residual is x and group_rows is None
         return y.view(C, d) if two_d else y
 
     @staticmethod
@@ -100,7 +103,9 @@ class FFNFn(torch.autograd.Function):
             K.zero_tails(dy3, group_rows, rows_clip)
         dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
-        dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip)
+        fuse_res = has_res and ctx.res_is_x
+        dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
+                               residual=dy3 if fuse_res else None)
         dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
                                out_dtype=_wgrad_dtype(w23))
         dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
@@ -111,7 +116,7 @@ class FFNFn(torch.autograd.Function):
         db1 = K.bias_grad(dz, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
-                (dy if has_res else None), None, None)
+                (dy if has_res and not fuse_res else None), None, None)
 
 
 class GateFn(torch.autograd.Function):
