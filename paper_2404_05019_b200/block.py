@@ -139,9 +139,12 @@ class Attention(nn.Module):
             raise ValueError(f"{t} tokens do not split into sequences of {s}")
         b, hd = t // s, d // h
         train = torch.is_grad_enabled() and (self.w_qkv_t.requires_grad or x.requires_grad)
+        # out = O(attn(QKV(x))) + x: the residual gradient is added in QKV's
+        # data-gradient GEMM (LinearFn link) when x needs a gradient
+        link = {} if (train and residual is x and x.requires_grad) else None
         if train:
             from .training import LinearFn
-            qkv = LinearFn.apply(x, self.w_qkv_t, None)
+            qkv = LinearFn.apply(x, self.w_qkv_t, None, link)
         else:
             qkv = K.grouped_gemm(x, self.w_qkv_t, None)                    # (T, 3d)
         scale = 1.0 / math.sqrt(d) if h == 1 else 1.0 / math.sqrt(hd)
@@ -159,7 +162,7 @@ class Attention(nn.Module):
             o = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal, scale=scale)
             o = o.permute(0, 2, 1, 3).reshape(t, d).contiguous()
         if train:
-            return LinearFn.apply(o, self.w_o_t, residual)
+            return LinearFn.apply(o, self.w_o_t, residual, link)
         return K.grouped_gemm(o, self.w_o_t, None, residual=residual)
 
 

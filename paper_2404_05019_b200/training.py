@@ -40,13 +40,21 @@ def _wgrad_dtype(w: torch.Tensor) -> torch.dtype:
 
 
 class LinearFn(torch.autograd.Function):
-    """y = x @ wt^T (+ residual); wt is (n_out, k_in) (bias-free projection)."""
+    """y = x @ wt^T (+ residual); wt is (n_out, k_in) (bias-free projection).
+
+    `link` (a dict shared by two LinearFns of one sub-block, or None) moves a
+    residual gradient into a data-gradient GEMM: for h -> QKV ... -> O + h,
+    the O projection (it has the residual) parks dy in the link instead of
+    returning it, and the QKV projection (input h) adds it in its dx GEMM's
+    residual epilogue — the same sum as autograd's add, one kernel fewer.
+    Autograd runs the O projection's backward first (QKV's output feeds it)."""
 
     @staticmethod
-    def forward(ctx, x, wt, residual):
+    def forward(ctx, x, wt, residual, link=None):
         y = K.grouped_gemm(x, wt, None, residual=residual)
         ctx.save_for_backward(x, wt)
         ctx.has_res = residual is not None
+        ctx.link = link
         return y
 
     @staticmethod
@@ -54,11 +62,19 @@ class LinearFn(torch.autograd.Function):
         x, wt = ctx.saved_tensors
         dy = dy.contiguous()
         dx = dwt = None
+        link = ctx.link
+        ctx.link = None
+        if ctx.has_res and link is not None:       # the residual's gradient, parked
+            link["dy"] = dy
+            res_grad = None
+        else:
+            res_grad = dy if ctx.has_res else None
         if ctx.needs_input_grad[0]:
-            dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1])
+            extra = link.pop("dy", None) if (link is not None and not ctx.has_res) else None
+            dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1], residual=extra)
         if ctx.needs_input_grad[1]:
             dwt = _as_param_grad(K.grouped_wgrad(dy, x, out_dtype=_wgrad_dtype(wt)), wt)
-        return dx, dwt, (dy if ctx.has_res else None)
+        return dx, dwt, res_grad, None
 
 
 class FFNFn(torch.autograd.Function):
