@@ -524,7 +524,11 @@ class ScMoEBlockPair(nn.Module):
                                                         residual=env["h_mh_cur"])
                 env["fused"] = True
                 return
-            env["se"] = moe.shared(env["x_cur"])
+            # training: the block residual's gradient (combine) is added in the
+            # shared expert's data-gradient GEMM when x_cur is the residual
+            xc = env["x_cur"]
+            env["link"] = {} if (train and xc is env.get("h_mh_cur") and xc.requires_grad) else None
+            env["se"] = moe.shared(xc, link=env["link"])
 
         def decode():
             dec = env["dec"]
@@ -540,7 +544,8 @@ class ScMoEBlockPair(nn.Module):
                 env["out"] = TR.CombineFn.apply(
                     env["y"], None if std else env["se"], env["w"], None if std else env["x_cur"],
                     None if std else moe.w_cg, env["h_mh_cur"], dec.indices, dec.slots, env["kept"],
-                    dec.capacity, "direct_add" if std else moe.combine_mode)
+                    dec.capacity, "direct_add" if std else moe.combine_mode,
+                    None if std else env.get("link"))
                 return
             if use_ep and env.get("y_ev") is not None:
                 st.wait_event(env["y_ev"])

@@ -282,14 +282,16 @@ class SharedExpert(nn.Module):
 
     def forward(self, x: torch.Tensor, residual: Optional[torch.Tensor] = None,
                 hidden: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
-                stream=None) -> torch.Tensor:
-        """expert_forward(x) (+ residual, fused into the second GEMM's epilogue)."""
+                stream=None, link: Optional[dict] = None) -> torch.Tensor:
+        """expert_forward(x) (+ residual, fused into the second GEMM's epilogue).
+        link (training): a residual gradient of x parked by the combine is
+        added in this FFN's data-gradient GEMM (training.FFNFn)."""
         if x.dtype != self.w1t.dtype:
             raise ValueError(f"input dtype {x.dtype} != expert dtype {self.w1t.dtype}")
         if torch.is_grad_enabled() and (self.w1t.requires_grad or x.requires_grad):
             from .training import FFNFn
             return FFNFn.apply(x, self.w1t, self.b1, self.w2t, self.b2, residual, None,
-                               x.shape[0])
+                               x.shape[0], link)
         return K.expert_ffn(x, self.w1t, self.b1, self.w2t, self.b2, hidden=hidden, out=out,
                             residual=residual, stream=stream)
 
@@ -529,9 +531,14 @@ class ScMoELayer(_RoutedMoE):
                 dec = self.route(src, eps=eps, replay=replay, generator=generator)
             w, aux, y, kept = self.routed_train(src, dec)
             sh = self.shared
-            se = TR.FFNFn.apply(x_cur, sh.w1t, sh.b1, sh.w2t, sh.b2, None, None, x_cur.shape[0])
+            # out = combine(SE(x), ...) + x: the residual gradient goes into the
+            # shared expert's data-gradient GEMM (no separate autograd add)
+            link = {} if (residual is not None and residual is x_cur and x_cur.requires_grad) \
+                else None
+            se = TR.FFNFn.apply(x_cur, sh.w1t, sh.b1, sh.w2t, sh.b2, None, None, x_cur.shape[0],
+                                link)
             out = TR.CombineFn.apply(y, se, w, x_cur, self.w_cg, residual, dec.indices, dec.slots,
-                                     kept, dec.capacity, self.combine_mode)
+                                     kept, dec.capacity, self.combine_mode, link)
             return out, dec, aux
         dec = self.route(src, eps=eps, replay=replay, generator=generator)
         y = self.routed_experts(src, dec)

@@ -85,7 +85,7 @@ class FFNFn(torch.autograd.Function):
     gradients can sum whole 64-row blocks."""
 
     @staticmethod
-    def forward(ctx, x, w1t, b1, w2t, b2, residual, group_rows, rows_clip):
+    def forward(ctx, x, w1t, b1, w2t, b2, residual, group_rows, rows_clip, link=None):
         two_d = x.dim() == 2
         x3 = x.unsqueeze(0) if two_d else x
         w13 = w1t.unsqueeze(0) if w1t.dim() == 2 else w1t
@@ -105,6 +105,9 @@ class FFNFn(torch.autograd.Function):
         # y = FFN(x) + x (the Block-MLP): the data gradient adds dy in its
         # GEMM epilogue instead of a separate autograd add
         ctx.res_is_x = residual is x and group_rows is None
+        # link: a residual gradient of x parked by a later Function (the
+        # ScMoE combine), added here like LinearFn's link
+        ctx.link = link if (group_rows is None and residual is None) else None
         return y.view(C, d) if two_d else y
 
     @staticmethod
@@ -120,8 +123,11 @@ class FFNFn(torch.autograd.Function):
         dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
         fuse_res = has_res and ctx.res_is_x
+        parked = ctx.link.pop("dy", None) if ctx.link is not None else None
+        ctx.link = None
+        extra = dy3 if fuse_res else (parked.view(G, C, d) if parked is not None else None)
         dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
-                               residual=dy3 if fuse_res else None)
+                               residual=extra)
         dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
                                out_dtype=_wgrad_dtype(w23))
         dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
@@ -132,7 +138,7 @@ class FFNFn(torch.autograd.Function):
         db1 = K.bias_grad(dz, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
-                (dy if has_res and not fuse_res else None), None, None)
+                (dy if has_res and not fuse_res else None), None, None, None)
 
 
 class GateFn(torch.autograd.Function):
@@ -193,11 +199,13 @@ class CombineFn(torch.autograd.Function):
     combine (arch.py:380-392) with the routed sum (arch.py:418-433)."""
 
     @staticmethod
-    def forward(ctx, y, se, weights, x_cur, w_cg, residual, indices, slots, kept, capacity, mode):
+    def forward(ctx, y, se, weights, x_cur, w_cg, residual, indices, slots, kept, capacity, mode,
+                link=None):
         out = K.combine(y, indices, slots, weights.contiguous(), capacity, se_out=se, mode=mode,
                         x_cur=x_cur, w_cg=w_cg, residual=residual)
         ctx.save_for_backward(y, se, weights, x_cur, w_cg, indices, slots, kept)
         ctx.meta = (capacity, mode, residual is not None)
+        ctx.link = link          # park the residual gradient for the shared FFN's dx GEMM
         return out
 
     @staticmethod
@@ -238,8 +246,12 @@ class CombineFn(torch.autograd.Function):
             gathered = y[indices.long().clamp(max=n_exp - 1), slots.long().clamp(max=capacity - 1)]
             dro = dout.float() if c_rt is None else dout.float() * c_rt[:, None]
             d_weights = (gathered.float() * dro[:, None, :]).sum(-1) * kept_sel
-        return (dy, d_se, d_weights, d_xcur, d_wcg, (dout if has_res else None),
-                None, None, None, None, None)
+        d_res = dout if has_res else None
+        if has_res and ctx.link is not None:
+            ctx.link["dy"] = dout
+            d_res = None
+        ctx.link = None
+        return (dy, d_se, d_weights, d_xcur, d_wcg, d_res, None, None, None, None, None, None)
 
 
 class ExchangeFn(torch.autograd.Function):
