@@ -97,3 +97,23 @@ def test_bench_reference_arm_prints_one_json_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_model_flops_formula():
+    """bench.py model_flops: matmul FLOPs of the configs[2] block pair, by hand.
+    Per token: 2 x (QKV 6d^2 + O 2d^2 + causal scores/PV 4 d (S+1)/2) +
+    Block-MLP 4dh + shared 4dh + routed 4dh (all kept) + gate 2dN."""
+    import importlib.util, os
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    w = bench.WORKLOADS["gpt3xl"]
+    T, d, h, S, N = 16384, 2048, 8192, 2048, 8
+    per_tok = 2 * (8 * d * d + 4 * d * (S + 1) / 2) + 3 * 4 * d * h + 2 * d * N
+    assert bench.block_pair_flops(w, T, T, N) == pytest.approx(per_tok * T, rel=1e-12)
+    # the every-block placement has no Block-MLP and one attention
+    wb = bench.WORKLOADS["every_block"]
+    d2, h2, S2 = wb["d"], wb["h"], wb["seq"]
+    per_tok2 = 8 * d2 * d2 + 4 * d2 * (S2 + 1) / 2 + 2 * 4 * d2 * h2 + 2 * d2 * 16
+    assert bench.block_pair_flops(wb, 100, 100, 16) == pytest.approx(per_tok2 * 100, rel=1e-12)
