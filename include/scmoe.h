@@ -327,6 +327,21 @@ int scmoe_ep_return_p2p(const void* y, int dtype, const int32_t* recv_counts, in
                         void* const* peer_back, uint32_t* const* peer_flags, uint32_t* epoch_ctr,
                         int max_ctas, void* stream);
 
+/* Gate backward (K7): VJP of the kept-selection weights (k > 1, masked
+ * softmax, tape.py:161-176) and of the balance loss (arch.py:436-439, d_aux a
+ * DEVICE scalar, may be null) through H = src W_gate (+ eps softplus(src
+ * W_noise), arch.py:405-415).  Writes d_src (T, d) in src's dtype (may be
+ * null), d_w_gate (N, d) fp32 and, with noise (w_noise_t, eps, noise_pre =
+ * src W_noise all non-null), d_w_noise (N, d) fp32; weight gradients are
+ * summed in a fixed order through the workspace (deterministic). */
+size_t scmoe_gate_backward_workspace_bytes(int n_tokens, int d_model, int n_experts, int noise);
+int scmoe_gate_backward(const void* src, int dtype, int n_tokens, int d_model, int n_experts,
+                        int k, const float* logits, const int32_t* indices, const float* weights,
+                        const float* d_weights, const int32_t* counts, const float* d_aux,
+                        const float* w_gate_t, const float* w_noise_t, const float* eps,
+                        const float* noise_pre, void* d_src, float* d_w_gate, float* d_w_noise,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

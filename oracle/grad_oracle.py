@@ -59,9 +59,12 @@ def _attention(x, p, prefix, d_model, n_heads=1, seq_len=None, causal=False):
 def pair_loss(p: Dict[str, torch.Tensor], tokens: torch.Tensor, variant: str, pos: Optional[str],
               n_experts: int, k: int, combine_mode: str, pinned_indices, pinned_dropped,
               aux_coeff: float = 0.01, target: Optional[torch.Tensor] = None,
-              n_heads: int = 1, seq_len: Optional[int] = None, causal: bool = False):
+              n_heads: int = 1, seq_len: Optional[int] = None, causal: bool = False,
+              eps=None):
     """Loss of one block pair (blocks 0 and 1) with routing pinned; returns
-    (loss, out)."""
+    (loss, out).  eps (T, N): the noisy gate's recorded draws, H = src W_gate
+    + eps * softplus(src W_noise) (arch.py:405-415), differentiated through
+    (tape.py: mm, mul, softplus)."""
     d = tokens.shape[1]
     h_in = tokens
     h_mh_prev = h_in + _attention(h_in, p, "block0.attn", d, n_heads, seq_len, causal)
@@ -73,6 +76,9 @@ def pair_loss(p: Dict[str, torch.Tensor], tokens: torch.Tensor, variant: str, po
     else:
         src = x_cur
     logits = src @ p["block1.moe.gate.w_gate"]
+    if eps is not None:
+        e = torch.as_tensor(np.asarray(eps), dtype=logits.dtype, device=logits.device)
+        logits = logits + e * torch.nn.functional.softplus(src @ p["block1.moe.gate.w_noise"])
     t = logits.shape[0]
     idx = torch.as_tensor(np.asarray(pinned_indices), dtype=torch.long, device=logits.device)
     drop = torch.as_tensor(np.asarray(pinned_dropped), dtype=torch.bool, device=logits.device)

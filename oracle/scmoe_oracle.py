@@ -565,12 +565,13 @@ def dual_routing(h_cur, h_prev, constraint: bool, capacity_factor: float):
 
 
 def moe_dual_gating(x_cur, x_prev, layer: Layer, capacity_factor: float, constraint: bool,
-                    pinned=None):
+                    pinned=None, eps=None, eps_prev=None):
     """routed_sum(x_cur, w_cur) + routed_sum(x_prev, w_prev); aux from the
     current gating (arch.py:507-533).  pinned = ((idx_cur, drop_cur),
-    (idx_prev, drop_prev)) replays the routing."""
-    h_prev, _ = gate_logits(x_prev, layer.gate)
-    h_cur, _ = gate_logits(x_cur, layer.gate)
+    (idx_prev, drop_prev)) replays the routing; eps / eps_prev are the noisy
+    gate's recorded draws of the two gatings (arch.py:514-515)."""
+    h_prev, _ = gate_logits(x_prev, layer.gate, eps=eps_prev)
+    h_cur, _ = gate_logits(x_cur, layer.gate, eps=eps)
     if pinned is not None:
         dec_cur = decision_from_indices(h_cur, pinned[0][0], pinned[0][1])
         dec_prev = decision_from_indices(h_prev, pinned[1][0], pinned[1][1])

@@ -71,6 +71,9 @@ SIGNATURES = [
     ("scmoe_expert_ffn_to_peers", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                        _i, _i, _i, _vp]),
     ("scmoe_ep_return_p2p", _i, [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
+    ("scmoe_gate_backward_workspace_bytes", _sz, [_i, _i, _i, _i]),
+    ("scmoe_gate_backward", _i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
 ]
 
 _lib = None

@@ -349,8 +349,7 @@ class ScMoEBlockPair(nn.Module):
                     dec = moe.route(src(), eps=eps, replay=replay)
                 env["dec"] = dec
                 env["kept"] = dec.kept_counts().to(torch.int32)
-                env["w"], env["aux"] = TR.GateFn.apply(src(), moe.gate.w_gate_t, dec.logits,
-                                                       dec.indices, dec.counts, dec.weights, dec.k)
+                env["w"], env["aux"] = TR.gate_weights_aux(moe.gate, src(), dec)
             else:
                 env["dec"] = moe.route(src(), eps=eps, replay=replay)
                 if chunks > 1:
@@ -568,7 +567,10 @@ class ScMoEBlockPair(nn.Module):
 
         def dual():
             # DGMoE: preceding gating on h_mh_prev, current on x_cur (arch.py:606-609)
-            out, dc, dp, aux = moe(env["x_cur"], env["h_mh_prev"], residual=env["h_mh_cur"])
+            # eps = the current gating's noise; the preceding one comes from
+            # the replay (eps_prev) or is drawn (arch.py:514-515)
+            out, dc, dp, aux = moe(env["x_cur"], env["h_mh_prev"], residual=env["h_mh_cur"],
+                                   eps=eps, replay=replay)
             env["out"], env["dec"], env["aux"] = out, (dc, dp), aux
 
         ops = dict(attn_prev=attn_prev, mlp_prev=mlp_prev, attn_cur=attn_cur, gate=gate,
@@ -621,7 +623,7 @@ class ScMoEBlockPair(nn.Module):
             p.grad = None
         out, dec, aux = self(h_in)
         if target is None:
-            loss = out.float().mean()
+            loss = out.mean(dtype=torch.float32)      # fp32 accumulation, no fp32 copy of out
         else:
             loss = (out.float() - target.float()).pow(2).sum() / out.shape[0]
         loss = loss + aux_coeff * aux
@@ -629,7 +631,8 @@ class ScMoEBlockPair(nn.Module):
         if check_finite:
             _raise_if_nonfinite(loss)
         if dp_group is not None or self.ep_group is not None:
-            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else self.ep_group)
+            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else self.ep_group,
+                                          experts_sharded=self.ep_group is not None)
         if update:
             TR.sgd_step(self.parameters(), lr)
         return loss.detach()
@@ -768,7 +771,7 @@ class ScMoEModel(nn.Module):
         for p in self.parameters():
             p.grad = None
         out, _, auxes = self(tokens)
-        loss = out.float().mean() if target is None else \
+        loss = out.mean(dtype=torch.float32) if target is None else \
             (out.float() - target.float()).pow(2).sum() / out.shape[0]
         for a in auxes:
             loss = loss + aux_coeff * a
@@ -777,7 +780,8 @@ class ScMoEModel(nn.Module):
             _raise_if_nonfinite(loss)
         ep = self.blocks[0].ep_group if len(self.blocks) else None
         if dp_group is not None or ep is not None:
-            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else ep)
+            TR.allreduce_replicated_grads(self, dp_group if dp_group is not None else ep,
+                                          experts_sharded=ep is not None)
         if update:
             TR.sgd_step(self.parameters(), lr)
         return loss.detach()

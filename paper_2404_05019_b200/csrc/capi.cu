@@ -57,53 +57,110 @@ __global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs
     base[i] = make_uint4(0, 0, 0, 0);
 }
 
-// Column sums over the valid rows of each group, two deterministic passes:
-// pass 1: block (group, row chunk of COLSUM_ROWS, 256-column tile) -> partial
-//         sums (each thread one column, 8 rows in flight, coalesced rows);
-// pass 2: fixed-order sum of the chunk partials.
-constexpr int COLSUM_ROWS = 128;
+// Column sums over the valid rows of each group (bias gradients), two
+// deterministic passes:
+// pass 1: block (256-vector column tile, row stripe, group).  Thread (v, lane)
+//         owns 16-byte column vector v and rows lane, lane + lanes, ... of the
+//         stripe with 8 loads in flight; the lanes' sums are added in a fixed
+//         order through shared memory -> one partial row per stripe.  Stripes
+//         are sized for ~2 blocks per SM so ~6+ MB of loads are in flight.
+// pass 2: block (32 columns x 32 stripe lanes), fixed-order sum of the
+//         stripes' partials.
+constexpr int COLSUM_THREADS = 256;
 
-// each thread owns one 16-byte column vector (8 bf16 / 4 fp32) and keeps 4
-// row loads in flight; cols must be a multiple of the vector width
+int colsum_vec(int dtype) { return dtype == SCMOE_BF16 ? 8 : 4; }
+
+// stripes per group: ~2 blocks per SM over (column tiles x groups)
+int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
+  const int vecs = (cols + vec - 1) / vec;
+  const int col_tiles = (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
+  int st = (2 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
+  return max(1, min(st, (group_cap + 7) / 8));
+}
+
 template <typename T>
-__global__ void colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
-                                      const int32_t* __restrict__ group_rows, int rows_clip,
-                                      int n_chunks, float* __restrict__ part) {
+__global__ void __launch_bounds__(COLSUM_THREADS)
+colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
+                      const int32_t* __restrict__ group_rows, int rows_clip, int stripe_rows,
+                      int n_stripes, float* __restrict__ part) {
   constexpr int VEC = Vec16<T>::N;
-  const int g = blockIdx.z;
-  const int chunk = blockIdx.y;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
-  if (c >= cols) return;
+  constexpr int U = 8;
+  __shared__ float red[COLSUM_THREADS][VEC + 1];
+  const int vecs = cols / VEC;
+  const int vpb = min(vecs, COLSUM_THREADS);              // vectors per column tile
+  const int lanes = COLSUM_THREADS / vpb;
+  const int v = threadIdx.x % vpb, lane = threadIdx.x / vpb;
+  const int g = blockIdx.z, stripe = blockIdx.y;
+  const int cv = blockIdx.x * vpb + v;                     // my column vector
+  const bool active = lane < lanes && cv < vecs;
   const int rows = group_rows ? max(0, min(group_rows[g], rows_clip)) : cap;
-  const int r0 = chunk * COLSUM_ROWS, r1 = min(rows, r0 + COLSUM_ROWS);
-  const T* p = x + ((long long)g * cap) * cols + c;
-  float s[4][VEC] = {};
-  int r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    uint4 v[4];
+  const int r0 = stripe * stripe_rows, r1 = min(rows, r0 + stripe_rows);
+  float s[VEC] = {};
+  if (active) {
+    const T* p = x + ((long long)g * cap) * cols + (long long)cv * VEC;
+    int r = r0 + lane;
+    for (; r + (U - 1) * lanes < r1; r += U * lanes) {
+      uint4 w[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(p + (long long)(r + u) * cols);
+      for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(p + (long long)(r + u * lanes) * cols);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      Vec16<T> w;
-      w.raw = v[u];
+      for (int u = 0; u < U; ++u) {
+        Vec16<T> t;
+        t.raw = w[u];
+        float f[VEC];
+        t.to_float(f);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) s[i] += f[i];
+      }
+    }
+    for (; r < r1; r += lanes) {
+      Vec16<T> t;
+      t.raw = ld_nc_v4(p + (long long)r * cols);
       float f[VEC];
-      w.to_float(f);
+      t.to_float(f);
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) s[u][i] += f[i];
+      for (int i = 0; i < VEC; ++i) s[i] += f[i];
     }
   }
-  for (; r < r1; ++r) {
-    Vec16<T> w;
-    w.raw = ld_nc_v4(p + (long long)r * cols);
-    float f[VEC];
-    w.to_float(f);
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) s[0][i] += f[i];
+  for (int i = 0; i < VEC; ++i) red[threadIdx.x][i] = s[i];
+  __syncthreads();
+  if (lane == 0 && cv < vecs) {
+    float o[VEC] = {};
+    for (int l = 0; l < lanes; ++l)
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) o[i] += red[l * vpb + v][i];
+    float* q = part + ((long long)g * n_stripes + stripe) * cols + (long long)cv * VEC;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) q[i] = o[i];
   }
-  float* o = part + ((long long)g * n_chunks + chunk) * cols + c;
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) o[i] = (s[0][i] + s[1][i]) + (s[2][i] + s[3][i]);
+}
+
+// block (32 columns x 32 stripe lanes): lane y sums stripes y, y+32, ...,
+// then the 32 lane sums are added in a fixed order
+__global__ void colsum_final_kernel(const float* __restrict__ part, int n_stripes, int cols,
+                                    int n_groups, float* __restrict__ out) {
+  __shared__ float red[32][33];
+  const int g = blockIdx.y;
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  float a0 = 0.f, a1 = 0.f;
+  if (c < cols) {
+    const float* p = part + (long long)g * n_stripes * cols + c;
+    int k = threadIdx.y;
+    for (; k + 32 < n_stripes; k += 64) {
+      a0 += p[(long long)k * cols];
+      a1 += p[(long long)(k + 32) * cols];
+    }
+    for (; k < n_stripes; k += 32) a0 += p[(long long)k * cols];
+  }
+  red[threadIdx.y][threadIdx.x] = a0 + a1;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int y = 0; y < 32; ++y) t += red[y][threadIdx.x];
+    out[(long long)g * cols + c] = t;
+  }
 }
 
 // dst[j] = src[ids[j]] for j < min(*n_rows, max_rows); rows of row_bytes
@@ -127,17 +184,6 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_
     for (int u = 0; u < 8; ++u) d[i + u * stride] = v[u];
   }
   for (; i < row_vecs; i += stride) d[i] = s[i];
-}
-
-__global__ void colsum_final_kernel(const float* __restrict__ part, int n_chunks, int cols,
-                                    int n_groups, float* __restrict__ out) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= (long long)n_groups * cols) return;
-  const int g = (int)(i / cols), c = (int)(i - (long long)g * cols);
-  const float* p = part + (long long)g * n_chunks * cols + c;
-  float s = 0.f;
-  for (int k = 0; k < n_chunks; ++k) s += p[(long long)k * cols];
-  out[i] = s;
 }
 
 }  // namespace
@@ -305,8 +351,11 @@ extern "C" int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_
 }
 
 extern "C" size_t scmoe_grouped_colsum_workspace_bytes(int num_groups, int group_cap, int cols) {
-  const size_t chunks = (size_t)((group_cap + COLSUM_ROWS - 1) / COLSUM_ROWS);
-  return chunks * (size_t)num_groups * (size_t)cols * sizeof(float);
+  if (num_groups < 1 || group_cap < 1 || cols < 1) return 0;
+  // large enough for either vector width (bf16 8, fp32 4 per 16 bytes)
+  const size_t st = (size_t)max(colsum_stripes(num_groups, group_cap, cols, 8),
+                                colsum_stripes(num_groups, group_cap, cols, 4));
+  return st * (size_t)num_groups * (size_t)cols * sizeof(float);
 }
 
 extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap,
@@ -319,25 +368,27 @@ extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, in
                                                                           cols),
                   "colsum workspace too small");
   if (rows_clip <= 0) rows_clip = group_cap;
-  const int vec = dtype == SCMOE_BF16 ? 8 : 4;
+  const int vec = colsum_vec(dtype);
   SCMOE_CHECK_ARG(cols % vec == 0 && ((uintptr_t)x & 15) == 0,
                   "colsum needs 16-byte aligned rows (cols multiple of %d)", vec);
-  const int n_chunks = (group_cap + COLSUM_ROWS - 1) / COLSUM_ROWS;
   cudaStream_t st = (cudaStream_t)stream;
   const int vecs = cols / vec;
-  const int threads = vecs < 128 ? ((vecs + 31) / 32) * 32 : 128;
-  dim3 grid((vecs + threads - 1) / threads, n_chunks, num_groups);
+  const int vpb = min(vecs, COLSUM_THREADS);
+  const int col_tiles = (vecs + vpb - 1) / vpb;
+  const int n_stripes = colsum_stripes(num_groups, group_cap, cols, vec);
+  const int stripe_rows = (group_cap + n_stripes - 1) / n_stripes;
+  dim3 grid(col_tiles, n_stripes, num_groups);
   float* part = (float*)workspace;
   if (dtype == SCMOE_BF16)
-    colsum_partial_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
-        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, n_chunks, part);
+    colsum_partial_kernel<__nv_bfloat16><<<grid, COLSUM_THREADS, 0, st>>>(
+        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes,
+        part);
   else
-    colsum_partial_kernel<float><<<grid, threads, 0, st>>>((const float*)x, group_cap, cols,
-                                                       group_rows, rows_clip, n_chunks, part);
+    colsum_partial_kernel<float><<<grid, COLSUM_THREADS, 0, st>>>(
+        (const float*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes, part);
   SCMOE_LAUNCH_CHECK();
-  const long long n = (long long)num_groups * cols;
-  colsum_final_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n_chunks, cols,
-                                                                   num_groups, out);
+  colsum_final_kernel<<<dim3((cols + 31) / 32, num_groups), dim3(32, 32), 0, st>>>(
+      part, n_stripes, cols, num_groups, out);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

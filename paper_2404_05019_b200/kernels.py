@@ -222,11 +222,15 @@ def grouped_gemm_ex(a: torch.Tensor, w: torch.Tensor, w_layout: int, out_cols: i
         raise ValueError(f"weight shape {tuple(w3.shape)} does not match a {tuple(a3.shape)} -> {out_cols}")
     if out is None:
         out = torch.empty(G, C, n_out, device=a.device, dtype=a.dtype)
+    elif out.dtype != a.dtype or out.numel() != G * C * n_out:
+        raise ValueError("out must have the operand dtype and (groups, rows, out_cols) elements")
     for name, t in (("residual", residual), ("aux_in", aux_in), ("aux_out", aux_out)):
         if t is not None:
             _c(t, name)
             if t.numel() != out.numel():
                 raise ValueError(f"{name} must match the output's shape")
+            if t.dtype != a.dtype:     # the C side reads it with a's element type
+                raise ValueError(f"{name} dtype {t.dtype} != operand dtype {a.dtype}")
     check(lib().scmoe_grouped_gemm_ex(
         ptr(_c(a3, "a")), dtype_code(a.dtype), ptr(_c(w3, "w")), w_layout, ptr(bias),
         ptr(residual), ptr(aux_in), ptr(aux_out), ptr(out), G, W, C, ptr(group_rows), rows_clip,
@@ -276,6 +280,38 @@ def gather_rows(src: torch.Tensor, ids: torch.Tensor, n_rows: torch.Tensor, max_
     check(lib().scmoe_gather_rows(ptr(_c(src, "src")), row_bytes, ptr(_c(ids, "ids")),
                                   ptr(n_rows), max_rows, ptr(_c(out, "out")), stream_ptr(stream)))
     return out
+
+
+def gate_backward(src: torch.Tensor, logits: torch.Tensor, indices: torch.Tensor,
+                  weights: torch.Tensor, counts: torch.Tensor, w_gate_t: torch.Tensor,
+                  d_weights: Optional[torch.Tensor] = None, d_aux: Optional[torch.Tensor] = None,
+                  w_noise_t: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
+                  noise_pre: Optional[torch.Tensor] = None, need_src: bool = True,
+                  stream=None):
+    """K7 gate backward (one pass over the tokens): returns (d_src or None,
+    d_w_gate (N, d) fp32, d_w_noise (N, d) fp32 or None)."""
+    ensure_device(src)
+    T, d = src.shape
+    N = logits.shape[1]
+    k = indices.shape[1]
+    noise = w_noise_t is not None
+    f32 = dict(device=src.device, dtype=torch.float32)
+    d_src = torch.empty_like(src) if need_src else None
+    d_wg = torch.empty(N, d, **f32)
+    d_wn = torch.empty(N, d, **f32) if noise else None
+    ws_bytes = lib().scmoe_gate_backward_workspace_bytes(T, d, N, 1 if noise else 0)
+    ws = torch.empty(max(ws_bytes, 16), device=src.device, dtype=torch.uint8)
+    if d_weights is not None:
+        d_weights = _c(d_weights.float(), "d_weights")
+    if d_aux is not None:
+        d_aux = d_aux.detach().float().reshape(1).contiguous()
+    check(lib().scmoe_gate_backward(
+        ptr(_c(src, "src")), dtype_code(src.dtype), T, d, N, k, ptr(_c(logits, "logits")),
+        ptr(_c(indices, "indices")), ptr(_c(weights, "weights")), ptr(d_weights),
+        ptr(_c(counts, "counts")), ptr(d_aux), ptr(_c(w_gate_t, "w_gate_t")), ptr(w_noise_t),
+        ptr(eps), ptr(noise_pre), ptr(d_src), ptr(d_wg), ptr(d_wn), ptr(ws), ws_bytes,
+        stream_ptr(stream)))
+    return d_src, d_wg, d_wn
 
 
 _ONES = {}

@@ -57,10 +57,14 @@ class CapacityConfig:
 
 @dataclass
 class MoEReplay:
-    """arch.MoEReplay (arch.py:315-322): pinned noise draws and routing."""
+    """arch.MoEReplay (arch.py:315-322): pinned noise draws and routing; the
+    *_prev fields are the preceding gating of dual gating (DGMoE)."""
     eps: Optional[object] = None
     indices: Optional[object] = None
     dropped: Optional[object] = None
+    eps_prev: Optional[object] = None
+    indices_prev: Optional[object] = None
+    dropped_prev: Optional[object] = None
 
 
 @dataclass
@@ -243,6 +247,26 @@ def _pin_routing(dec: GateDecision, replay: MoEReplay) -> GateDecision:
                         dec.prob_sum, dec.quota, cap, dec.eps)
 
 
+def _with_capacity(dec: GateDecision, cap: int) -> GateDecision:
+    """The same decision in a dispatch buffer of `cap` rows per expert
+    (cap >= every kept count): dropped selections point past the new end."""
+    if cap == dec.capacity:
+        return dec
+    slots = torch.where(dec.dropped, torch.full_like(dec.slots, cap), dec.slots)
+    return GateDecision(dec.logits, dec.indices, dec.weights, dec.dropped, slots, dec.counts,
+                        dec.prob_sum, dec.quota, cap, dec.eps)
+
+
+def _agree_capacity(dec: GateDecision, group) -> GateDecision:
+    """Pinned routing under expert parallelism: the dispatch capacity is the
+    max over ranks of the pinned kept counts, so the equal-split exchanges
+    agree on the block size."""
+    import torch.distributed as dist
+    caps = [None] * dist.get_world_size(group)
+    dist.all_gather_object(caps, int(dec.capacity), group=group)
+    return _with_capacity(dec, max(caps))
+
+
 # ---------------------------------------------------------------------------
 # experts
 
@@ -408,7 +432,27 @@ class _RoutedMoE(nn.Module):
         self.experts.load_reference(list(layer.experts)[r * el:(r + 1) * el])
 
     def route(self, x_src, eps=None, replay=None, generator=None, stream=None) -> GateDecision:
-        return self.gate(x_src, eps=eps, generator=generator, replay=replay, stream=stream)
+        if self.ep_group is not None:
+            self._check_even_tokens(x_src.shape[0])
+        dec = self.gate(x_src, eps=eps, generator=generator, replay=replay, stream=stream)
+        if self.ep_group is not None and replay is not None and replay.indices is not None:
+            dec = _agree_capacity(dec, self.ep_group)
+        return dec
+
+    def _check_even_tokens(self, t: int) -> None:
+        """The exchanges move equal-split (E, C, d) blocks, C = ceil(cf*T*k/E)
+        from each rank's own T (gating.py:134-135): every rank must route the
+        same token count.  Checked once per new T (one small collective)."""
+        seen = getattr(self, "_even_t", None)
+        if seen == t:
+            return
+        import torch.distributed as dist
+        ts = [None] * dist.get_world_size(self.ep_group)
+        dist.all_gather_object(ts, t, group=self.ep_group)
+        if len(set(ts)) != 1:
+            raise ValueError(f"expert parallelism needs the same token count on every rank, "
+                             f"got {ts}")
+        self._even_t = t
 
     def routed_experts(self, x_src: torch.Tensor, dec: GateDecision, stream=None) -> torch.Tensor:
         """dispatch + expert FFN (+ EP exchange); returns the (N, C, d) expert
@@ -453,11 +497,8 @@ class _RoutedMoE(nn.Module):
         if self.dtype != torch.bfloat16:
             raise NotImplementedError("backward kernels are bf16 only (the fp32 path is a "
                                       "forward parity path)")
-        if self.noise_enabled:
-            raise NotImplementedError("training with the noisy gate is not implemented yet")
         kept = dec.kept_counts().to(torch.int32)
-        w, aux = TR.GateFn.apply(src, self.gate.w_gate_t, dec.logits, dec.indices, dec.counts,
-                                 dec.weights, dec.k)
+        w, aux = TR.gate_weights_aux(self.gate, src, dec)
         buf = TR.DispatchFn.apply(src, dec.indices, dec.slots, kept, self.n_experts, dec.capacity)
         e = self.experts
         if self.ep_group is None:
@@ -624,32 +665,61 @@ class DGMoELayer(_RoutedMoE):
         m._load_reference_common(layer)
         return m
 
-    def route_dual(self, x_cur, x_prev, eps=None, eps_prev=None):
-        dec_prev = self.gate(x_prev, eps=eps_prev)
+    def route_dual(self, x_cur, x_prev, eps=None, eps_prev=None, replay=None, generator=None):
+        """(dec_cur, dec_prev) — dual_routing (arch.py:447-460) or, with the
+        replay's indices and indices_prev, the pinned decisions
+        (arch.py:518-520).  Noise (arch.py:514-515): the replay's draws, the
+        given ones, else fresh draws (preceding gating first, as the
+        reference's rng order)."""
         g = self.gate
+        if replay is not None:
+            eps = replay.eps if replay.eps is not None else eps
+            eps_prev = replay.eps_prev if replay.eps_prev is not None else eps_prev
+        if g.noise_enabled:
+            shape = (x_cur.shape[0], self.n_experts)
+            if eps_prev is None:
+                eps_prev = torch.randn(shape, device=x_cur.device, generator=generator)
+            if eps is None:
+                eps = torch.randn(shape, device=x_cur.device, generator=generator)
+            eps = _as_tensor(eps, x_cur.device, torch.float32)
+            eps_prev = _as_tensor(eps_prev, x_cur.device, torch.float32)
+        else:
+            eps = eps_prev = None
+        pinned = (replay is not None and replay.indices is not None
+                  and replay.indices_prev is not None)
+        if pinned:
+            dec_prev = g(x_prev, eps=eps_prev, replay=MoEReplay(indices=replay.indices_prev,
+                                                                dropped=replay.dropped_prev))
+            dec_cur = g(x_cur, eps=eps, replay=MoEReplay(indices=replay.indices,
+                                                         dropped=replay.dropped))
+            return dec_cur, dec_prev
+        dec_prev = g(x_prev, eps=eps_prev)
         quota = g.quota(x_cur.shape[0])
         excl = dec_prev.indices[:, 0] if self.constraint else None
         o = K.gate_topk(x_cur, g.w_gate_t, 1, quota,
                         w_noise_t=g.w_noise_t if g.noise_enabled else None,
-                        eps=eps if g.noise_enabled else None, exclude=excl)
+                        eps=eps, exclude=excl)
         dec_cur = GateDecision(o.logits, o.indices, o.weights, o.dropped.bool(), o.slots, o.counts,
-                               o.prob_sum, quota, quota, eps if g.noise_enabled else None)
+                               o.prob_sum, quota, quota, eps)
         return dec_cur, dec_prev
 
     def forward(self, x_cur: torch.Tensor, x_prev: torch.Tensor,
-                residual: Optional[torch.Tensor] = None, eps=None, eps_prev=None):
+                residual: Optional[torch.Tensor] = None, eps=None, eps_prev=None,
+                replay: Optional[MoEReplay] = None, generator=None):
         """(out, dec_cur, dec_prev, aux) — moe_dual_gating (arch.py:507-533)."""
-        n, cap = self.n_experts, self.gate.quota(x_cur.shape[0])
+        n = self.n_experts
         train = self.training_path()
         with torch.no_grad():
-            dec_cur, dec_prev = self.route_dual(x_cur, x_prev, eps, eps_prev)
+            dec_cur, dec_prev = self.route_dual(x_cur, x_prev, eps, eps_prev, replay, generator)
+        # one (2N, cap, d) buffer for both dispatches
+        cap = max(dec_cur.capacity, dec_prev.capacity)
+        dec_cur, dec_prev = _with_capacity(dec_cur, cap), _with_capacity(dec_prev, cap)
         idx = torch.cat([dec_cur.indices, dec_prev.indices + n], dim=1).contiguous()
         slots = torch.cat([dec_cur.slots, dec_prev.slots], dim=1).contiguous()
         e = self.experts
         if train:
             from . import training as TR
-            w_cur, aux = TR.GateFn.apply(x_cur, self.gate.w_gate_t, dec_cur.logits,
-                                         dec_cur.indices, dec_cur.counts, dec_cur.weights, 1)
+            w_cur, aux = TR.gate_weights_aux(self.gate, x_cur, dec_cur)
             kc, kp = dec_cur.kept_counts().int(), dec_prev.kept_counts().int()
             buf = torch.cat([TR.DispatchFn.apply(x_cur, dec_cur.indices, dec_cur.slots, kc, n, cap),
                              TR.DispatchFn.apply(x_prev, dec_prev.indices, dec_prev.slots, kp, n,
@@ -663,7 +733,7 @@ class DGMoELayer(_RoutedMoE):
         buf = torch.empty(2 * n, cap, x_cur.shape[1], device=x_cur.device, dtype=x_cur.dtype)
         K.dispatch(x_cur, dec_cur.indices, dec_cur.slots, n, cap, out=buf[:n])
         K.dispatch(x_prev, dec_prev.indices, dec_prev.slots, n, cap, out=buf[n:])
-        rows = torch.cat([dec_cur.counts, dec_prev.counts])
+        rows = torch.cat([dec_cur.kept_counts(), dec_prev.kept_counts()]).to(torch.int32)
         y = self.experts(buf, rows, cap)
         w = torch.cat([dec_cur.weights, dec_prev.weights], dim=1).contiguous()
         out = K.combine(y, idx, slots, w, cap, residual=residual)

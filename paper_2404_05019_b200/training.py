@@ -34,6 +34,25 @@ def _as_param_grad(g: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
     return g.to(like.dtype).view(like.shape)
 
 
+def _park(link: dict, dy: torch.Tensor) -> None:
+    """Park a residual gradient for the data-gradient GEMM of the Function
+    that reads the same input (see LinearFn), tagged with the backward pass
+    that produced it."""
+    link["dy"] = (torch._C._current_graph_task_id(), dy)
+
+
+def _take(link) -> Optional[torch.Tensor]:
+    """The gradient parked in THIS backward pass, or None.  A stale entry
+    (parked by a partial backward, e.g. autograd.grad w.r.t. one weight,
+    whose consumer never ran) is dropped instead of being added twice."""
+    if link is None:
+        return None
+    item = link.pop("dy", None)
+    if item is None or item[0] != torch._C._current_graph_task_id():
+        return None
+    return item[1]
+
+
 def _wgrad_dtype(w: torch.Tensor) -> torch.dtype:
     """bf16 weights get their gradient straight from the split reduction."""
     return torch.bfloat16 if w.dtype == torch.bfloat16 else torch.float32
@@ -63,18 +82,25 @@ class LinearFn(torch.autograd.Function):
         dy = dy.contiguous()
         dx = dwt = None
         link = ctx.link
-        ctx.link = None
         if ctx.has_res and link is not None:       # the residual's gradient, parked
-            link["dy"] = dy
+            _park(link, dy)
             res_grad = None
         else:
             res_grad = dy if ctx.has_res else None
         if ctx.needs_input_grad[0]:
-            extra = link.pop("dy", None) if (link is not None and not ctx.has_res) else None
+            extra = _take(link) if not ctx.has_res else None
             dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1], residual=extra)
         if ctx.needs_input_grad[1]:
             dwt = _as_param_grad(K.grouped_wgrad(dy, x, out_dtype=_wgrad_dtype(wt)), wt)
         return dx, dwt, res_grad, None
+
+
+def _wsum(per_group: torch.Tensor, n_wgroups: int) -> torch.Tensor:
+    """(G, n) per-group sums -> (W, n): group g feeds weight group g % W."""
+    g = per_group.shape[0]
+    if g == n_wgroups:
+        return per_group
+    return per_group.view(g // n_wgroups, n_wgroups, -1).sum(0)
 
 
 class FFNFn(torch.autograd.Function):
@@ -123,8 +149,7 @@ class FFNFn(torch.autograd.Function):
         dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
         fuse_res = has_res and ctx.res_is_x
-        parked = ctx.link.pop("dy", None) if ctx.link is not None else None
-        ctx.link = None
+        parked = _take(ctx.link)
         extra = dy3 if fuse_res else (parked.view(G, C, d) if parked is not None else None)
         dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
                                residual=extra)
@@ -132,10 +157,11 @@ class FFNFn(torch.autograd.Function):
                                out_dtype=_wgrad_dtype(w23))
         dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
                                out_dtype=_wgrad_dtype(w13))
-        # bias gradients as 1^T dy on the tensor cores (sums the source groups
-        # of each weight group like the weight gradients)
-        db2 = K.bias_grad(dy3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
-        db1 = K.bias_grad(dz, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip)
+        # bias gradients: column sums over the valid rows (HBM-bound, 8 row
+        # loads in flight per thread), then the source groups of each weight
+        # group summed like the weight gradients
+        db2 = _wsum(K.grouped_colsum(dy3, group_rows, rows_clip), W)
+        db1 = _wsum(K.grouped_colsum(dz, group_rows, rows_clip), W)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
                 (dy if has_res and not fuse_res else None), None, None, None)
@@ -144,35 +170,51 @@ class FFNFn(torch.autograd.Function):
 class GateFn(torch.autograd.Function):
     """Differentiable part of the gate: returns the kept-selection weights
     (T, k) and aux = N * sum_i f_i P_i (arch.py:436-439, 481-485).  Routing
-    (indices, drops, counts) comes in as constants from the gate kernel."""
+    (indices, drops, counts) comes in as constants from the gate kernel, and
+    so do the probability sums: aux is formed from the kernel's prob_sum, no
+    softmax pass.  With noise (arch.py:405-415) the logits carry
+    eps * softplus(src W_noise) and the backward differentiates through it
+    (noise_pre = src W_noise).  Backward: one kernel (scmoe_gate_backward)."""
 
     @staticmethod
-    def forward(ctx, src, w_gate_t, logits, indices, counts, weights, k):
-        n = logits.shape[1]
-        t = logits.shape[0]
-        f = counts.to(torch.float32) / float(t * k)
-        p = torch.softmax(logits, dim=1)
-        aux = n * (f * p.mean(0)).sum()
-        ctx.save_for_backward(src, w_gate_t, p, f, indices, weights)
-        ctx.k = k
+    def forward(ctx, src, w_gate_t, w_noise_t, logits, indices, counts, weights, prob_sum, k,
+                eps, noise_pre):
+        t, n = logits.shape
+        aux = (counts.to(torch.float32) * prob_sum).sum() * (n / float(t * t * k))
+        ctx.save_for_backward(src, w_gate_t, w_noise_t, logits, indices, counts, weights, eps,
+                              noise_pre)
         return weights.clone(), aux
 
     @staticmethod
     def backward(ctx, d_weights, d_aux):
-        src, w_gate_t, p, f, indices, weights = ctx.saved_tensors
-        t, n = p.shape
-        dlogits = torch.zeros_like(p)
-        if d_aux is not None:
-            # d aux / d h[t, j] = (N / T) p_tj (f_j - <f, p_t>)
-            dlogits += (d_aux * n / t) * p * (f[None, :] - (p * f[None, :]).sum(1, keepdim=True))
-        if d_weights is not None and ctx.k > 1:
-            # masked softmax over the k selected logits (tape.py:161-176)
-            dw = d_weights.float()
-            dsel = weights * (dw - (weights * dw).sum(1, keepdim=True))
-            dlogits.scatter_add_(1, indices.long(), dsel)
-        d_src = (dlogits @ w_gate_t).to(src.dtype)
-        d_w = dlogits.t() @ src.float()
-        return d_src, d_w, None, None, None, None, None
+        src, w_gate_t, w_noise_t, logits, indices, counts, weights, eps, noise_pre = \
+            ctx.saved_tensors
+        noise = noise_pre is not None
+        need_src = ctx.needs_input_grad[0]
+        if d_weights is not None and indices.shape[1] == 1:
+            d_weights = None          # top-1: the weight is identically 1 (zero VJP)
+        if (d_weights is None and d_aux is None) or logits.shape[1] == 1:
+            # one expert: p = f = 1, so the balance loss is constant (zero VJP)
+            return (None,) * 11
+        d_src, d_wg, d_wn = K.gate_backward(
+            src, logits, indices, weights, counts, w_gate_t, d_weights=d_weights, d_aux=d_aux,
+            w_noise_t=w_noise_t if noise else None, eps=eps if noise else None,
+            noise_pre=noise_pre, need_src=need_src)
+        return (d_src if need_src else None, d_wg if ctx.needs_input_grad[1] else None,
+                d_wn if (noise and ctx.needs_input_grad[2]) else None) + (None,) * 8
+
+
+def gate_weights_aux(gate, src: torch.Tensor, dec):
+    """(weights, aux) of a routed decision as differentiable functions of the
+    source rows and the gate (and noise) weights."""
+    noise = gate.noise_enabled and dec.eps is not None
+    noise_pre = None
+    if noise:
+        with torch.no_grad():
+            noise_pre = src.float() @ gate.w_noise_t.t()
+    return GateFn.apply(src, gate.w_gate_t, gate.w_noise_t if noise else None, dec.logits,
+                        dec.indices, dec.counts, dec.weights, dec.prob_sum, dec.k,
+                        dec.eps if noise else None, noise_pre)
 
 
 class DispatchFn(torch.autograd.Function):
@@ -248,9 +290,8 @@ class CombineFn(torch.autograd.Function):
             d_weights = (gathered.float() * dro[:, None, :]).sum(-1) * kept_sel
         d_res = dout if has_res else None
         if has_res and ctx.link is not None:
-            ctx.link["dy"] = dout
+            _park(ctx.link, dout)
             d_res = None
-        ctx.link = None
         return (dy, d_se, d_weights, d_xcur, d_wcg, d_res, None, None, None, None, None, None)
 
 
@@ -273,20 +314,41 @@ class ExchangeFn(torch.autograd.Function):
 def sgd_step(params, lr: float) -> None:
     """In-place SGD (the reference's toy trainer, grad.py:330-331)."""
     with torch.no_grad():
-        ps = [p for p in params if p.grad is not None]
-        if ps:
+        # one multi-tensor launch per (dtype, grad dtype): a mixed list (bf16
+        # weights, fp32 biases) drops torch's foreach to one kernel per tensor
+        groups = {}
+        for p in params:
+            if p.grad is not None:
+                groups.setdefault((p.dtype, p.grad.dtype, p.device), []).append(p)
+        for ps in groups.values():
             torch._foreach_add_(ps, [p.grad for p in ps], alpha=-lr)
 
 
-def allreduce_replicated_grads(module, group=None) -> None:
-    """Data-parallel all-reduce (mean) of the parameters every rank holds a
-    full copy of: everything except the sharded routed experts."""
+def allreduce_replicated_grads(module, group=None, experts_sharded: bool = True) -> None:
+    """Gradient of the mean of the per-rank objectives, (1/G) sum_r loss_r —
+    the objective of training on the ranks' slices together (each rank runs
+    the reference's compute_loss on its own slice, grad.py:52-67).
+
+    * Replicated parameters (gate, shared expert, backbone): every rank holds
+      d loss_r / dp, so they are all-reduced and divided by G.
+    * Sharded routed experts (`experts_sharded`, expert parallelism): the
+      owner's weight-gradient GEMM already sums the rows of every source rank
+      (the reverse exchange brings each rank's dy to the owner), i.e. it holds
+      sum_r d loss_r / dW_e; dividing by G gives the same mean.  Without
+      expert parallelism the experts are replicas and are all-reduced like
+      everything else."""
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
     ws = dist.get_world_size(group)
-    grads = [p.grad for n, p in module.named_parameters()
-             if p.grad is not None and ".experts." not in f".{n}"]
+    named = [(n, p) for n, p in module.named_parameters() if p.grad is not None]
+
+    def sharded(n):
+        return experts_sharded and ".experts." in f".{n}"
+    own = [p.grad for n, p in named if sharded(n)]
+    if own:
+        torch._foreach_div_(own, float(ws))
+    grads = [p.grad for n, p in named if not sharded(n)]
     if not grads:
         return
     flat = torch._utils._flatten_dense_tensors(grads)

@@ -88,3 +88,65 @@ def test_dgmoe_trains():
     losses = [float(blk.train_step(x, lr=2e-3, target=tgt)) for _ in range(6)]
     assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
     assert blk.moe.experts.w1t.grad is not None
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_dgmoe_noise_and_replay(dtype):
+    """Dual gating with the noisy gate: the two gatings' draws (eps, eps_prev)
+    enter the logits (arch.py:514-515); routing is bit-exact on the kernels'
+    logits, the output matches the oracle with the same draws, and a replay
+    of (eps, eps_prev, indices, dropped, indices_prev, dropped_prev) through
+    MoEReplay reproduces the output bit for bit (arch.py:518-520)."""
+    T, d, h, N, cf = 384, 128, 256, 6, 1.0
+    pp = O.init_pair(d, h, N, O.Rng(37).spawn(0), variant="dgmoe", noise_enabled=True)
+    x_cur = O.Rng(37).spawn(1).normal((T, d))
+    x_prev = x_cur + 0.3 * O.Rng(37).spawn(2).normal((T, d))
+    eps = O.Rng(37).spawn(3).normal((T, N))
+    eps_prev = O.Rng(37).spawn(4).normal((T, N))
+    layer = P.DGMoELayer.from_reference(pp.moe, P.CapacityConfig(cf), dtype=dtype)
+    assert layer.noise_enabled
+    xc, xp = _t(x_cur, dtype), _t(x_prev, dtype)
+    out, dc, dp, aux = layer(xc, xp, eps=_t(eps, torch.float32), eps_prev=_t(eps_prev, torch.float32))
+    torch.cuda.synchronize()
+    rc, rp = O.dual_routing(dc.logits.double().cpu().numpy(), dp.logits.double().cpu().numpy(),
+                            True, cf)
+    np.testing.assert_array_equal(dc.indices.long().cpu().numpy(), rc.indices)
+    np.testing.assert_array_equal(dp.indices.long().cpu().numpy(), rp.indices)
+    np.testing.assert_array_equal(dc.dropped.cpu().numpy(), rc.dropped)
+    ref, _, _, raux = O.moe_dual_gating(xc.double().cpu().numpy(), xp.double().cpu().numpy(),
+                                        pp.moe, cf, True, pinned=(_pin(dc), _pin(dp)),
+                                        eps=eps, eps_prev=eps_prev)
+    rtol = 1e-4 if dtype == torch.float32 else 2e-2
+    ok, worst = O.allclose_scaled(out.double().cpu().numpy(), ref, rtol)
+    assert ok, worst
+    # the noise changes routing vs the clean gate
+    clean = O.dual_routing(*(O.gate_logits(z, O.Gate(pp.moe.gate.w_gate, pp.moe.gate.w_noise,
+                                                     1, False))[0]
+                             for z in (xc.double().cpu().numpy(), xp.double().cpu().numpy())),
+                           True, cf)[0]
+    assert (clean.indices != rc.indices).any()
+    # replay: pinned routing and draws through MoEReplay
+    r = P.MoEReplay(eps=eps, indices=dc.indices.long().cpu().numpy(),
+                    dropped=dc.dropped.cpu().numpy(), eps_prev=eps_prev,
+                    indices_prev=dp.indices.long().cpu().numpy(),
+                    dropped_prev=dp.dropped.cpu().numpy())
+    out2, dc2, dp2, _ = layer(xc, xp, replay=r)
+    assert torch.equal(dc2.indices, dc.indices) and torch.equal(dp2.indices, dp.indices)
+    assert torch.equal(out2, out)
+
+
+def test_dgmoe_block_noise_draws():
+    """A noisy DGMoE block pair draws its own noise when none is given (the
+    C API needs w_noise and eps together) and trains."""
+    blk = P.ScMoEBlockPair(128, 256, 4, variant="dgmoe", n_heads=2, seq_len=128,
+                           capacity_factor=1.0, noise_enabled=True, dtype=torch.bfloat16,
+                           generator=torch.Generator(device="cuda").manual_seed(9))
+    x = torch.randn(256, 128, device="cuda").bfloat16()
+    with torch.no_grad():
+        out, (dc, dp), aux = blk(x)
+    assert dc.eps is not None and dp.eps is not None
+    assert torch.isfinite(out.float()).all()
+    blk.requires_grad_(True)
+    loss = blk.train_step(x, lr=1e-3)
+    assert torch.isfinite(loss).item()
+    assert blk.moe.gate.w_noise_t.grad is not None

@@ -59,6 +59,9 @@ def _ref_view(blk, grad=False):
         if moe.w_cg is not None:
             out["block1.moe.cg.w"] = g(moe.w_cg)
     out["block1.moe.gate.w_gate"] = g(moe.gate.w_gate_t).t()
+    wn = g(moe.gate.w_noise_t)
+    out["block1.moe.gate.w_noise"] = (wn if wn is not None
+                                      else torch.zeros_like(moe.gate.w_noise_t)).t()
     return {k: v.double().cpu().numpy() for k, v in out.items()}
 
 
@@ -136,3 +139,126 @@ def test_train_step_nonfinite_loss_raises_before_update():
         blk.train_step(x, lr=1e-3, target=target, check_finite=True)
     assert torch.equal(w_before, blk.moe.experts.w1t.detach())
     assert torch.isfinite(blk.train_step(x, lr=1e-3, check_finite=True)).item()
+
+
+def _check_grads(got, ref_grads, tag):
+    for name, ref in ref_grads.items():
+        if name not in got:
+            continue
+        gv = got[name]
+        bound = RTOL * (np.abs(ref) + np.abs(ref).max() + 1e-30)
+        worst = float((np.abs(gv - ref) / bound).max())
+        assert worst <= 1.0, f"{tag} grad {name}: worst err/bound {worst:.3g}"
+
+
+@pytest.mark.parametrize("variant,k", [("scmoe", 1), ("standard", 2)])
+def test_noisy_gate_gradients(variant, k):
+    """Training with the noisy gate (arch.py:405-415): the logits carry
+    eps * softplus(src W_noise) and the gate's backward differentiates through
+    it — W_gate, W_noise and the source rows get the reference tape's
+    gradients (recorded draws pinned, MoEReplay semantics)."""
+    T, d, h, N = 256, 128, 256, 6
+    pp = O.init_pair(d, h, N, O.Rng(23).spawn(0), variant=variant, k=k, noise_enabled=True)
+    cfg = SimpleNamespace(d_model=d, d_hidden=h, n_experts=N, variant=variant,
+                          shortcut_pos="pos2" if variant == "scmoe" else None, k_routed=k,
+                          combine_mode="direct_add", capacity_factor=1.0, noise_enabled=True,
+                          pre_layernorm=False)
+    blk = P.ScMoEBlockPair.from_reference(cfg, SimpleNamespace(attn=pp.attn_prev, feed=pp.mlp_prev),
+                                          SimpleNamespace(attn=pp.attn_cur, feed=pp.moe),
+                                          dtype=torch.bfloat16)
+    blk.requires_grad_(True)
+    x = torch.as_tensor(O.Rng(23).spawn(1).normal((T, d)), device="cuda").bfloat16()
+    eps = torch.as_tensor(O.Rng(23).spawn(2).normal((T, N)), device="cuda").float()
+    params0 = _ref_view(blk)
+    out, dec, aux = blk(x, eps=eps)
+    loss = out.float().mean() + 0.01 * aux
+    loss.backward()
+    torch.cuda.synchronize()
+    assert dec.eps is not None
+    ref_loss, ref_grads = G.pair_grads(
+        params0, x.double().cpu().numpy(), variant=variant, pos=cfg.shortcut_pos, n_experts=N,
+        k=k, combine_mode="direct_add", pinned_indices=dec.indices.long().cpu().numpy(),
+        pinned_dropped=dec.dropped.cpu().numpy(), eps=eps.double().cpu().numpy())
+    assert float(loss) == pytest.approx(ref_loss, rel=2e-2, abs=1e-3)
+    got = _ref_view(blk, grad=True)
+    assert np.abs(got["block1.moe.gate.w_noise"]).max() > 0
+    _check_grads(got, ref_grads, f"noisy {variant}")
+
+
+def test_configs1_shape_gradients():
+    """configs[1] at its real widths (SwinV2-MoE-S stage 3: d 384, h 1536, 12
+    heads over 12x12 = 144-token windows, cf 1.25) with 8 experts, on a
+    1152-token subsample (8 windows): every parameter's gradient vs the
+    float64 oracle."""
+    T, d, h, N, heads, S = 1152, 384, 1536, 8, 12, 144
+    pp = O.init_pair(d, h, N, O.Rng(29).spawn(0), variant="scmoe")
+    cfg = SimpleNamespace(d_model=d, d_hidden=h, n_experts=N, variant="scmoe",
+                          shortcut_pos="pos2", k_routed=1, combine_mode="direct_add",
+                          capacity_factor=1.25, noise_enabled=False, pre_layernorm=False)
+    blk = P.ScMoEBlockPair.from_reference(cfg, SimpleNamespace(attn=pp.attn_prev, feed=pp.mlp_prev),
+                                          SimpleNamespace(attn=pp.attn_cur, feed=pp.moe),
+                                          dtype=torch.bfloat16, n_heads=heads, seq_len=S)
+    blk.requires_grad_(True)
+    x = torch.as_tensor(O.Rng(29).spawn(1).normal((T, d)), device="cuda").bfloat16()
+    params0 = _ref_view(blk)
+    out, dec, aux = blk(x)
+    loss = out.float().mean() + 0.01 * aux
+    loss.backward()
+    torch.cuda.synchronize()
+    assert int(dec.counts.gt(0).sum()) == N     # every expert gets rows (and gradients)
+    ref_loss, ref_grads = G.pair_grads(
+        params0, x.double().cpu().numpy(), variant="scmoe", pos="pos2", n_experts=N, k=1,
+        combine_mode="direct_add", pinned_indices=dec.indices.long().cpu().numpy(),
+        pinned_dropped=dec.dropped.cpu().numpy(), n_heads=heads, seq_len=S)
+    assert float(loss) == pytest.approx(ref_loss, rel=2e-2, abs=1e-3)
+    _check_grads(_ref_view(blk, grad=True), ref_grads, "configs[1]")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("N,k,noise", [(8, 1, False), (8, 2, True), (12, 2, False),
+                                       (40, 3, True)])
+def test_gate_backward_kernel(dtype, N, k, noise):
+    """scmoe_gate_backward vs float64 autograd of the same objective:
+    d(c_aux * aux + <dw, weights>) through H = src Wg (+ eps softplus(src Wn))."""
+    from paper_2404_05019_b200 import kernels as K
+    T, d = 1001, 256
+    g = torch.Generator(device="cuda").manual_seed(N * 10 + k)
+    src = torch.randn(T, d, device="cuda", generator=g).to(dtype)
+    wg = torch.randn(N, d, device="cuda", generator=g) / 16
+    wn = torch.randn(N, d, device="cuda", generator=g) / 16
+    eps = torch.randn(T, N, device="cuda", generator=g)
+    logits = src.float() @ wg.t()
+    noise_pre = src.float() @ wn.t()
+    if noise:
+        logits = logits + eps * torch.nn.functional.softplus(noise_pre)
+    idx = torch.topk(logits, k, dim=1).indices.to(torch.int32)
+    w = torch.softmax(logits.gather(1, idx.long()), dim=1)
+    counts = torch.bincount(idx.reshape(-1).long(), minlength=N).to(torch.int32)
+    dw = torch.randn(T, k, device="cuda", generator=g)
+    d_aux = torch.tensor(0.37, device="cuda")
+    d_src, d_wg, d_wn = K.gate_backward(
+        src, logits.contiguous(), idx, w.contiguous(), counts, wg, d_weights=dw, d_aux=d_aux,
+        w_noise_t=wn if noise else None, eps=eps if noise else None,
+        noise_pre=noise_pre.contiguous() if noise else None)
+    # float64 autograd reference
+    s64 = src.double().requires_grad_(True)
+    g64 = wg.double().requires_grad_(True)
+    n64 = wn.double().requires_grad_(True)
+    h = s64 @ g64.t()
+    if noise:
+        h = h + eps.double() * torch.nn.functional.softplus(s64 @ n64.t())
+    sel = h.gather(1, idx.long())
+    wsel = torch.softmax(sel, dim=1)
+    f = counts.double() / (T * k)
+    aux = N * (torch.softmax(h, dim=1).mean(0) * f).sum()
+    obj = 0.37 * aux + ((wsel * dw.double()).sum() if k > 1 else 0.0)
+    obj.backward()
+    def close(a, b, tol):
+        b = b.detach()
+        err = (a.double() - b).abs().max().item()
+        assert err <= tol * (b.abs().max().item() + 1e-12), (err, b.abs().max().item())
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-4
+    close(d_src, s64.grad, tol)
+    close(d_wg, g64.grad, 1e-4)
+    if noise:
+        close(d_wn, n64.grad, 1e-4)
