@@ -207,16 +207,31 @@ gate_bwd_kernel(GateBwdArgs a) {
   }
 }
 
-// out[p][j][c] = sum_b part[b][p][j][c], fixed order over b
+// out[p][j][c] = sum_b part[b][p][j][c]: block (32 outputs x 32 lanes), lane
+// y sums blocks y, y+32, ..., then the lane sums are added in a fixed order
 __global__ void gate_bwd_reduce_kernel(const float* __restrict__ part, int n_blocks, long long n,
                                        float* __restrict__ d_wg, float* __restrict__ d_wn,
                                        long long per_plane) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float s = 0.f;
-  for (int b = 0; b < n_blocks; ++b) s += part[(long long)b * n + i];
-  if (i < per_plane) d_wg[i] = s;
-  else d_wn[i - per_plane] = s;
+  __shared__ float red[32][33];
+  const long long i = blockIdx.x * 32ll + threadIdx.x;
+  float s0 = 0.f, s1 = 0.f;
+  if (i < n) {
+    int b = threadIdx.y;
+    for (; b + 32 < n_blocks; b += 64) {
+      s0 += part[(long long)b * n + i];
+      s1 += part[(long long)(b + 32) * n + i];
+    }
+    for (; b < n_blocks; b += 32) s0 += part[(long long)b * n + i];
+  }
+  red[threadIdx.y][threadIdx.x] = s0 + s1;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < n) {
+    float s = 0.f;
+#pragma unroll 8
+    for (int y = 0; y < 32; ++y) s += red[y][threadIdx.x];
+    if (i < per_plane) d_wg[i] = s;
+    else d_wn[i - per_plane] = s;
+  }
 }
 
 template <typename T, int NMAX>
@@ -283,7 +298,7 @@ extern "C" int scmoe_gate_backward(const void* src, int dtype, int T, int d, int
   SCMOE_LAUNCH_CHECK();
   const long long per_plane = (long long)N * d;
   const long long n = per_plane * (noise ? 2 : 1);
-  gate_bwd_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+  gate_bwd_reduce_kernel<<<(unsigned)((n + 31) / 32), dim3(32, 32), 0, st>>>(
       (const float*)workspace, tb_used, n, d_w_gate, d_w_noise, per_plane);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;

@@ -56,6 +56,18 @@ def exposed_comm_ms(spans: Sequence[Span]) -> float:
     return comm * (1.0 - comm_overlap_fraction(spans))
 
 
+def window_makespan_ms(spans: Sequence[Span], window_ops: Sequence[str]) -> float:
+    """Measured counterpart of sched.slot_makespan: device time from the
+    first start to the last end of the overlap window's ops, the routed
+    expert and both exchanges (max(pre, t_disp) + t_expert + max(post,
+    t_comb) when the schedule is realised exactly)."""
+    names = set(window_ops) | {"expert"} | set(COMM_KINDS)
+    sel = [s for s in spans if s.op in names]
+    if not sel:
+        return 0.0
+    return max(s.end_ms for s in sel) - min(s.start_ms for s in sel)
+
+
 class Recorder:
     """Records (start, end) event pairs per op; `spans()` syncs once."""
 
