@@ -216,6 +216,11 @@ int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_sr
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);
 
+/* Tuning / test hook: epilogue warps of the forward / dgrad tcgen05 GEMM,
+ * 0 = auto (16 for K <= 1024 tiles with an elementwise epilogue, else 8),
+ * 8 or 16 forced. */
+int scmoe_set_gemm_epilogue_warps(int warps);
+
 /* Tuning / test hook: tcgen05 tile width, 0 = auto (128 when n_out is an odd
  * multiple of 128 and the narrow tile needs fewer column-waves), 128 or 256. */
 int scmoe_set_gemm_tile_n(int bn);
@@ -341,6 +346,39 @@ int scmoe_gate_backward(const void* src, int dtype, int n_tokens, int d_model, i
                         const float* w_gate_t, const float* w_noise_t, const float* eps,
                         const float* noise_pre, void* d_src, float* d_w_gate, float* d_w_noise,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Windowed multi-head attention (the configs[1] backbone: 144-token windows,
+ * 12 heads of 32), forward and backward on the packed QKV projection:
+ * qkv (T, 3*H*hd) bf16 rows [q | k | v], heads contiguous hd-wide slices;
+ * windows of seq_len consecutive rows (T % seq_len == 0), O = softmax(Q K^T
+ * scale (+ causal mask)) V per window and head (arch.py:354-358 generalised
+ * to heads / windows), out (T, H*hd) bf16, lse (T, H) fp32 base-2 row
+ * log-sum-exp of the scaled scores (may be null in the forward).  The
+ * backward writes dqkv (T, 3*H*hd) in the packed layout from qkv, out, dout
+ * and lse.  Supported: seq_len % 16 == 0, 16 <= seq_len <= 192, hd 32 or 64
+ * (scmoe_window_attention_supported). */
+int scmoe_window_attention_supported(int seq_len, int head_dim);
+int scmoe_window_attention_fwd(const void* qkv, int n_tokens, int n_heads, int head_dim,
+                               int seq_len, float scale, int causal, void* out, float* lse,
+                               void* stream);
+int scmoe_window_attention_bwd(const void* qkv, const void* out, const void* dout,
+                               const float* lse, int n_tokens, int n_heads, int head_dim,
+                               int seq_len, float scale, int causal, void* dqkv, void* stream);
+
+/* Training FFN elementwise GELU passes (exact-erf GELU, numkit.py:96-99;
+ * tape.py:137-142), bf16 (num_groups, group_cap, cols) buffers, rows(g) =
+ * min(group_rows[g], rows_clip) (all rows when group_rows is null), rows_pad(g)
+ * = min(group_cap, roundup(rows(g), 64)):
+ *   scmoe_gelu_fwd: h = gelu(z) on rows < rows(g), zeros up to rows_pad(g);
+ *   scmoe_gelu_bwd: dz = dh * gelu'(z) on rows < rows(g), zeros up to
+ *     rows_pad(g), and (bias_grad non-null) bias_grad[g][c] = sum of dz over
+ *     the valid rows, fixed-order (deterministic) through the workspace. */
+int scmoe_gelu_fwd(const void* z, void* h, int num_groups, int group_cap, int cols,
+                   const int32_t* group_rows, int rows_clip, void* stream);
+size_t scmoe_gelu_bwd_workspace_bytes(int num_groups, int group_cap, int cols);
+int scmoe_gelu_bwd(const void* dh, const void* z, void* dz, float* bias_grad, int num_groups,
+                   int group_cap, int cols, const int32_t* group_rows, int rows_clip,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -43,6 +43,7 @@ SIGNATURES = [
                                 _vp]),
     ("scmoe_set_gemm_mode", _i, [_i]),
     ("scmoe_set_gemm_tile_n", _i, [_i]),
+    ("scmoe_set_gemm_epilogue_warps", _i, [_i]),
     ("scmoe_gather_rows", _i, [_vp, _sz, _vp, _vp, _i, _vp, _vp]),
     ("scmoe_grouped_gemm_ex", _i, [_vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                    _i, _i, _i, _i, _i, _vp]),
@@ -71,6 +72,13 @@ SIGNATURES = [
     ("scmoe_expert_ffn_to_peers", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                        _i, _i, _i, _vp]),
     ("scmoe_ep_return_p2p", _i, [_vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
+    ("scmoe_window_attention_supported", _i, [_i, _i]),
+    ("scmoe_window_attention_fwd", _i, [_vp, _i, _i, _i, _i, ctypes.c_float, _i, _vp, _vp, _vp]),
+    ("scmoe_window_attention_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, ctypes.c_float, _i,
+                                        _vp, _vp]),
+    ("scmoe_gelu_fwd", _i, [_vp, _vp, _i, _i, _i, _vp, _i, _vp]),
+    ("scmoe_gelu_bwd_workspace_bytes", _sz, [_i, _i, _i]),
+    ("scmoe_gelu_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _sz, _vp]),
     ("scmoe_gate_backward_workspace_bytes", _sz, [_i, _i, _i, _i]),
     ("scmoe_gate_backward", _i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),

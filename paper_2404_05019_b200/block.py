@@ -51,6 +51,35 @@ def layer_norm(x: torch.Tensor) -> torch.Tensor:
 
 PACKED_ATTENTION = True     # training attention through flash-attn's packed-QKV kernels
 ATTN_TRAIN = "cudnn_packed"  # "cudnn_packed" | "flash_packed" | "autograd"
+# windows of <= 192 rows (configs[1]: 144) run our own attention kernels on
+# the packed QKV projection (csrc/attention.cu), training and inference
+WINDOW_ATTENTION = True
+
+
+class _WindowAttention(torch.autograd.Function):
+    """Attention core on libscmoe's windowed kernels: reads the packed (T, 3d)
+    QKV rows, returns O as (T, d) rows (the O projection's input), saves the
+    row log-sum-exp; the backward writes dQKV straight into the packed
+    layout.  No head permutes, no layout copies."""
+
+    @staticmethod
+    def forward(ctx, qkv, h, s, causal, scale):
+        o, lse = K.window_attention_fwd(qkv, h, s, scale, causal)
+        ctx.save_for_backward(qkv, o, lse)
+        ctx.meta = (h, s, causal, scale)
+        return o
+
+    @staticmethod
+    def backward(ctx, g):
+        qkv, o, lse = ctx.saved_tensors
+        h, s, causal, scale = ctx.meta
+        dqkv = K.window_attention_bwd(qkv, o, g.contiguous(), lse, h, s, scale, causal)
+        return dqkv, None, None, None, None
+
+
+def _use_window_attention(qkv: torch.Tensor, s: int, hd: int) -> bool:
+    return (WINDOW_ATTENTION and qkv.dtype == torch.bfloat16
+            and K.window_attention_supported(s, hd))
 
 
 class _CudnnPackedAttention(torch.autograd.Function):
@@ -148,7 +177,12 @@ class Attention(nn.Module):
         else:
             qkv = K.grouped_gemm(x, self.w_qkv_t, None)                    # (T, 3d)
         scale = 1.0 / math.sqrt(d) if h == 1 else 1.0 / math.sqrt(hd)
-        if train and ATTN_TRAIN == "cudnn_packed" and qkv.dtype == torch.bfloat16:
+        if _use_window_attention(qkv, s, hd):
+            if train:
+                o = _WindowAttention.apply(qkv, h, s, self.causal, scale)
+            else:
+                o = K.window_attention_fwd(qkv, h, s, scale, self.causal, need_lse=False)[0]
+        elif train and ATTN_TRAIN == "cudnn_packed" and qkv.dtype == torch.bfloat16:
             o = _CudnnPackedAttention.apply(qkv, b, s, h, self.causal, scale)
         elif train and ATTN_TRAIN == "flash_packed" and _use_packed_attention(qkv, hd):
             # training: flash-attn's packed-QKV kernels read (B, S, 3, H, hd) and

@@ -74,7 +74,7 @@ int colsum_vec(int dtype) { return dtype == SCMOE_BF16 ? 8 : 4; }
 int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
   const int vecs = (cols + vec - 1) / vec;
   const int col_tiles = (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
-  int st = (2 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
+  int st = (6 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
   return max(1, min(st, (group_cap + 7) / 8));
 }
 

@@ -40,8 +40,13 @@ namespace scmoe {
 namespace sm100 {
 
 constexpr int BK = 64;
+// epilogue warps: 8 (the default: large-K tiles are MMA-bound) or 16 (small-K
+// tiles with elementwise-heavy epilogues — GELU, GELU backward, the
+// pre-activation store, residuals — where the epilogue's issue rate, not the
+// MMA, paces the tile; twice the warps hide twice the latency)
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 128 + EPI_WARPS * 32;
+template <int E> struct Threads { static constexpr int value = 128 + E * 32; };
+constexpr int THREADS = Threads<EPI_WARPS>::value;
 constexpr int TMEM_COLS = 512;                   // 512 / BN accumulator stages
 constexpr int MAX_GROUPS = 1024;
 constexpr int MN_BOX = 64;                       // MN-major TMA box: 64 (mn) x 64 (k)
@@ -50,8 +55,9 @@ constexpr int MN_BOX_BYTES = MN_BOX * BK * 2;    // 8 KB
 // BN_ = 256 (default) or 128: the narrow tile for n_out = 384-style widths
 // (configs[1]) that would leave half a 256-column tile idle; it also doubles
 // the accumulator stages (4 x 128 TMEM columns) for small-K tiles.
-template <bool TWO_SM, int BN_ = 256>
+template <bool TWO_SM, int BN_ = 256, int E_ = 8>
 struct Cfg {
+  static constexpr int E = E_;                            // epilogue warps
   static constexpr int BN = BN_;
   static constexpr int ACC_STAGES = TMEM_COLS / BN;
   static constexpr int CTA_M = 128;                       // rows of A per CTA
@@ -60,12 +66,13 @@ struct Cfg {
   static constexpr int A_BYTES = CTA_M * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024 / STAGE_BYTES) < 8 ? (192 * 1024 / STAGE_BYTES) : 8;
-  // + per-epilogue-warp bias slice (8 warps x 128 fp32), staged once per tile
+  static constexpr int RING_BYTES = E_ == 8 ? 192 * 1024 : 176 * 1024;
+  static constexpr int STAGES = (RING_BYTES / STAGE_BYTES) < 8 ? (RING_BYTES / STAGE_BYTES) : 8;
+  // + per-epilogue-warp bias slice (E warps x 128 fp32), staged once per tile
   static constexpr size_t MISC = 256 + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 16;
   // + per-epilogue-warp 2 KB store-transpose staging
   static constexpr size_t SMEM =
-      1024 + (size_t)STAGES * STAGE_BYTES + MISC + 8 * 128 * 4 + EPI_WARPS * 2048;
+      1024 + (size_t)STAGES * STAGE_BYTES + MISC + E_ * 128 * 4 + E_ * 2048;
 };
 
 // instruction descriptor: D fp32, A/B bf16, M = TILE_M, N = 256, operand majors
@@ -536,13 +543,19 @@ __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32
   }
 }
 
-template <bool TWO_SM, bool B_MN, bool WGRAD, int BN>
-__global__ void __launch_bounds__(THREADS, 1)
+template <bool TWO_SM, bool B_MN, bool WGRAD, int BN, int E = EPI_WARPS>
+__global__ void __launch_bounds__(Threads<E>::value, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const Params p) {
-  using C = Cfg<TWO_SM, BN>;
+  using C = Cfg<TWO_SM, BN, E>;
   constexpr int ACC_STAGES = C::ACC_STAGES;
-  constexpr int NCH = BN / 64;          // 32-column chunks per epilogue warp
+  constexpr int PARTS = E / 4;          // epilogue warps per TMEM lane quadrant
+  constexpr int COLS_W = BN / PARTS;    // accumulator columns per epilogue warp
+  constexpr int NCH = COLS_W / 32;      // 32-column chunks per epilogue warp
+  // 8 warps: chunk c+1's tcgen05.ld in flight while chunk c is processed;
+  // 16 warps (register cap 102): one chunk in registers, the other warps
+  // hide the load latency
+  constexpr bool PREFETCH = E == 8;
   constexpr bool A_MN = WGRAD;
   constexpr uint32_t IDESC = Idesc<TWO_SM, A_MN, B_MN, BN>::value;
   extern __shared__ uint8_t smem_raw[];
@@ -558,11 +571,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 2 * ACC_STAGES);
   int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
-  uint4* s_stage = reinterpret_cast<uint4*>(s_bias + EPI_WARPS * 128);   // 2 KB per epilogue warp
+  uint4* s_stage = reinterpret_cast<uint4*>(s_bias + E * 128);   // 2 KB per epilogue warp
   const int ring = C::STAGES - p.ld_buf;                                   // mainloop stages
   // if ld_buf: the lent stage's A slot (and its B slot when >= 16 KB) hold the
-  // per-warp load buffers, NLB chunks in flight
-  constexpr int NLB = C::B_BYTES >= 16384 ? 2 : 1;
+  // per-warp load buffers, NLB chunks in flight (16 warps: one chunk each,
+  // warps 0-7 in the A slot, 8-15 in the B slot)
+  constexpr int NLB = E == 16 ? 1 : (C::B_BYTES >= 16384 ? 2 : 1);
+  static_assert(E == 8 || C::B_BYTES >= 16384, "16 epilogue warps need a 16 KB B slot");
   uint4* s_load0 = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 1) * C::A_BYTES);
   uint4* s_load1 = reinterpret_cast<uint4*>(smem_b + (C::STAGES - 1) * C::B_BYTES);
 
@@ -582,7 +597,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], (TWO_SM ? 2 : 1) * EPI_WARPS);
+      mbar_init(&tempty_bar[s], (TWO_SM ? 2 : 1) * E);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -706,7 +721,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== epilogue (both CTAs, each on its own 128 TMEM lanes) =====
     const int ew = warp - 4;
     const int quad = warp & 3;   // TMEM lanes [32*quad, 32*quad+32)
-    const int half = ew >> 2;    // accumulator columns [BN/2*half, BN/2*(half+1))
+    const int part = ew >> 2;    // accumulator columns [COLS_W*part, COLS_W*(part+1))
     // the fast epilogue covers bias / bias+GELU stores without residual,
     // pre-activation / GELU-backward operands, zero tails or the fused combine
     const bool fast = !WGRAD && !p.residual && (!p.aux_out || p.epi == EPI_BIAS_GELU) &&
@@ -747,7 +762,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // (the loads overlap the MMAs; the chunk loop reads smem broadcasts)
       float* sbw = s_bias + ew * 128;
       if (!WGRAD && (brow || fast_gelu)) {   // the GELU path adds staged zeros when bias-free
-        const int nb = tc.n0 + half * (BN / 2) + 4 * lane;
+        const int nb = tc.n0 + part * COLS_W + 4 * lane;
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
         if (brow) {
           if (nb + 3 < p.N) b = *reinterpret_cast<const float4*>(brow + nb);
@@ -755,7 +770,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int i = 0; i < 4 && nb + i < p.N; ++i) (&b.x)[i] = brow[nb + i];
         }
         __syncwarp();        // previous tile's reads of sbw are done
-        if (4 * lane < BN / 2)
+        if (4 * lane < COLS_W)
           sts128(smem_u32(sbw + 4 * lane), make_uint4(__float_as_uint(b.x), __float_as_uint(b.y),
                                                       __float_as_uint(b.z), __float_as_uint(b.w)));
         __syncwarp();
@@ -789,10 +804,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const __nv_bfloat16* lsrc =
           WGRAD ? nullptr : (p.residual ? p.residual : (p.epi == EPI_GELU_BWD ? p.aux_in : nullptr));
       const uint32_t lmask = __ballot_sync(0xffffffffu, row_ok);
-      auto lbuf = [&](int c) { return ((NLB == 2 && (c & 1)) ? s_load1 : s_load0) + ew * 128; };
+      auto lbuf = [&](int c) {
+        if (E == 16) return (ew < 8 ? s_load0 + ew * 128 : s_load1 + (ew - 8) * 128);
+        return ((NLB == 2 && (c & 1)) ? s_load1 : s_load0) + ew * 128;
+      };
       const long long lrow0 = ((long long)tc.g * p.cap + row_w0) * p.N;
       auto issue_load = [&](int c) __attribute__((always_inline)) {
-        const int n = tc.n0 + half * (BN / 2) + c * 32;
+        const int n = tc.n0 + part * COLS_W + c * 32;
         const int j = lane & 3;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -829,15 +847,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       // TMEM -> registers in NCH chunks of 32 columns, chunk c+1's tcgen05.ld in
       // flight while chunk c is processed
       const uint32_t tbase =
-          tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
+          tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + part * COLS_W;
       uint32_t ra[32], rb[32];
+      auto release_acc = [&]() __attribute__((always_inline)) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+      };
       SCMOE_TMEM_LD32(tbase, ra);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (NCH == 1) release_acc();   // the whole accumulator slice is in registers
       // one chunk: cur holds its accumulator columns, nxt receives chunk c+1's
       auto chunk = [&](auto lean_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32])
                        __attribute__((always_inline)) {
-        if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
-        const int n = tc.n0 + half * (BN / 2) + c * 32;
+        if (PREFETCH) {
+          if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
+        } else if (c > 0) {
+          SCMOE_TMEM_LD32(tbase + c * 32, cur);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c == NCH - 1) release_acc();
+        }
+        const int n = tc.n0 + part * COLS_W + c * 32;
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && n + 32 <= p.N) {
@@ -875,58 +908,55 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (arow0) stage_flush(stg, lane, arow0 + n, p.N, wmask, p.N - n);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, p.N - n);
         }
-        if (c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == NCH - 2) {
-          // the whole accumulator is in registers: hand TMEM back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
-            else mbar_arrive(&tempty_bar[acc]);
-          }
-        }
+        if (PREFETCH && c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // the whole accumulator is in registers: hand TMEM back to the MMA warp
+        if (PREFETCH && c == NCH - 2) release_acc();
       };
       // Plain / bias stores with every chunk in range: straight-line code.
       // Everything else (GELU, residual, pre-activation, combine, tails):
       // chunk pairs in a rolled loop (ra / rb alternate statically) — fully
       // unrolled it overflowed the instruction cache (ncu: stall_no_inst 38%
       // of the GELU epilogue's samples).
-      const bool plain = !WGRAD && fast && !fast_gelu && tc.n0 + (half + 1) * (BN / 2) <= p.N;
+      const bool plain = !WGRAD && fast && !fast_gelu && tc.n0 + (part + 1) * COLS_W <= p.N;
       if (plain) {
         auto plain_chunk = [&](auto bias_tag, int c, uint32_t(&cur)[32], uint32_t(&nxt)[32])
                                __attribute__((always_inline)) {
-          if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
-          const int n = tc.n0 + half * (BN / 2) + c * 32;
+          if (PREFETCH) {
+            if (c < NCH - 1) SCMOE_TMEM_LD32(tbase + (c + 1) * 32, nxt);
+          } else if (c > 0) {
+            SCMOE_TMEM_LD32(tbase + c * 32, cur);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (c == NCH - 1) release_acc();
+          }
+          const int n = tc.n0 + part * COLS_W + c * 32;
           epilogue_chunk_fast<decltype(bias_tag)::value, false>(cur, sbw + c * 32);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
-          if (c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (c == NCH - 2) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (TWO_SM) mbar_arrive_cluster_tmem(&tempty_bar[acc], 0);
-              else mbar_arrive(&tempty_bar[acc]);
-            }
-          }
+          if (PREFETCH && c < NCH - 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (PREFETCH && c == NCH - 2) release_acc();
         };
         if (brow) {
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (c & 1) plain_chunk(std::true_type{}, c, rb, ra);
+            if (PREFETCH && (c & 1)) plain_chunk(std::true_type{}, c, rb, ra);
             else plain_chunk(std::true_type{}, c, ra, rb);
           }
         } else {
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (c & 1) plain_chunk(std::false_type{}, c, rb, ra);
+            if (PREFETCH && (c & 1)) plain_chunk(std::false_type{}, c, rb, ra);
             else plain_chunk(std::false_type{}, c, ra, rb);
           }
         }
       } else {
+        if (PREFETCH) {
 #pragma unroll 1
-        for (int c = 0; c < NCH; c += 2) {
-          chunk(std::true_type{}, c, ra, rb);
-          chunk(std::true_type{}, c + 1, rb, ra);
+          for (int c = 0; c < NCH; c += 2) {
+            chunk(std::true_type{}, c, ra, rb);
+            if (NCH > 1) chunk(std::true_type{}, c + 1, rb, ra);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < NCH; ++c) chunk(std::true_type{}, c, ra, ra);
         }
       }
     }
@@ -1014,12 +1044,12 @@ int make_map(CUtensorMap* map, const void* base, int inner, int outer, int group
   return SCMOE_OK;
 }
 
-template <bool TWO_SM, bool B_MN, bool WGRAD, int BN>
+template <bool TWO_SM, bool B_MN, bool WGRAD, int BN, int E = EPI_WARPS>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
            cudaStream_t st) {
-  using C = Cfg<TWO_SM, BN>;
+  using C = Cfg<TWO_SM, BN, E>;
   static bool attr_set = false;
-  auto kern = gemm_kernel<TWO_SM, B_MN, WGRAD, BN>;
+  auto kern = gemm_kernel<TWO_SM, B_MN, WGRAD, BN, E>;
   if (!attr_set) {
     SCMOE_CUDA_TRY(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -1027,7 +1057,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(Threads<E>::value);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1059,9 +1089,22 @@ static int pick_bn(F&&, long long) {
 
 template <bool TWO_SM, bool B_MN, bool WGRAD>
 static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const sm100::Params& p,
-                     int grid, cudaStream_t st) {
+                     int grid, cudaStream_t st, bool wide_epi = false) {
+  if constexpr (!WGRAD) {
+    if (wide_epi && bn == 256) return sm100::launch<TWO_SM, B_MN, WGRAD, 256, 16>(ma, mb, p, grid, st);
+  }
   return bn == 128 ? sm100::launch<TWO_SM, B_MN, WGRAD, 128>(ma, mb, p, grid, st)
                    : sm100::launch<TWO_SM, B_MN, WGRAD, 256>(ma, mb, p, grid, st);
+}
+
+// 16 epilogue warps: small-K forward / dgrad tiles (the MMA of a K <= 1024
+// tile is shorter than an 8-warp epilogue of 128 x BN outputs) whose
+// epilogue does elementwise work or reads a row-major operand.  Tuning hook
+// g_gemm_epi: 0 auto, 8 or 16 forced.
+static int g_gemm_epi = 0;
+static bool wide_epilogue(int K, int epi, bool aux_out, bool residual) {
+  if (g_gemm_epi) return g_gemm_epi == 16;
+  return K <= 1024 && (epi != 0 || aux_out || residual);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -1124,12 +1167,14 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   const int b_rows = two ? bn / 2 : bn;
   rc = b_mn ? make_map(&mb, wt, N, K, n_wgroups, BK) : make_map(&mb, wt, K, N, n_wgroups, b_rows);
   if (rc) return rc;
+  const bool wide = !cs && !out_groups && wide_epilogue(K, epi, aux_out != nullptr,
+                                                         residual != nullptr);
   if (two)
-    rc = b_mn ? launch_bn<true, true, false>(bn, ma, mb, p, (int)units * 2, st)
-              : launch_bn<true, false, false>(bn, ma, mb, p, (int)units * 2, st);
+    rc = b_mn ? launch_bn<true, true, false>(bn, ma, mb, p, (int)units * 2, st, wide)
+              : launch_bn<true, false, false>(bn, ma, mb, p, (int)units * 2, st, wide);
   else
-    rc = b_mn ? launch_bn<false, true, false>(bn, ma, mb, p, (int)units, st)
-              : launch_bn<false, false, false>(bn, ma, mb, p, (int)units, st);
+    rc = b_mn ? launch_bn<false, true, false>(bn, ma, mb, p, (int)units, st, wide)
+              : launch_bn<false, false, false>(bn, ma, mb, p, (int)units, st, wide);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
@@ -1238,6 +1283,15 @@ extern "C" int scmoe_set_gemm_mode(int mode) {
     return SCMOE_ERR_ARG;
   }
   scmoe::g_gemm_mode = mode;
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_set_gemm_epilogue_warps(int e) {
+  if (e != 0 && e != 8 && e != 16) {
+    scmoe::set_error("gemm epilogue warps must be 0 (auto), 8 or 16");
+    return SCMOE_ERR_ARG;
+  }
+  scmoe::g_gemm_epi = e;
   return SCMOE_OK;
 }
 

@@ -195,6 +195,11 @@ def set_gemm_mode(mode: int) -> None:
     check(lib().scmoe_set_gemm_mode(mode))
 
 
+def set_gemm_epilogue_warps(e: int) -> None:
+    """0 = auto (16 for small-K elementwise-heavy tiles), 8 or 16 forced."""
+    check(lib().scmoe_set_gemm_epilogue_warps(e))
+
+
 def set_gemm_tile_n(bn: int) -> None:
     """0 = auto, 128 or 256 = force the tcgen05 tile width (N per tile)."""
     check(lib().scmoe_set_gemm_tile_n(bn))
@@ -312,6 +317,75 @@ def gate_backward(src: torch.Tensor, logits: torch.Tensor, indices: torch.Tensor
         ptr(eps), ptr(noise_pre), ptr(d_src), ptr(d_wg), ptr(d_wn), ptr(ws), ws_bytes,
         stream_ptr(stream)))
     return d_src, d_wg, d_wn
+
+
+def gelu_fwd(z: torch.Tensor, group_rows: Optional[torch.Tensor] = None, rows_clip: int = 0,
+             out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """h = gelu(z) (exact erf) on each group's valid rows, zero-padded tails."""
+    ensure_device(z)
+    z3 = z if z.dim() == 3 else z.unsqueeze(0)
+    G, C, H = z3.shape
+    if z.dtype != torch.bfloat16:
+        raise ValueError("gelu_fwd is bf16")
+    if out is None:
+        out = torch.empty_like(z3)
+    check(lib().scmoe_gelu_fwd(ptr(_c(z3, "z")), ptr(_c(out, "out")), G, C, H, ptr(group_rows),
+                               rows_clip, stream_ptr(stream)))
+    return out if z.dim() == 3 else out.view(C, H)
+
+
+def gelu_bwd(dh: torch.Tensor, z: torch.Tensor, group_rows: Optional[torch.Tensor] = None,
+             rows_clip: int = 0, bias_grad: bool = True, stream=None):
+    """(dz = dh * gelu'(z) with zero-padded tails, per-group bias gradient
+    sum_rows dz (G, H) fp32 or None)."""
+    ensure_device(dh)
+    d3 = dh if dh.dim() == 3 else dh.unsqueeze(0)
+    z3 = z if z.dim() == 3 else z.unsqueeze(0)
+    G, C, H = d3.shape
+    if z3.shape != d3.shape or dh.dtype != torch.bfloat16 or z.dtype != torch.bfloat16:
+        raise ValueError("gelu_bwd: dh and z must be bf16 of one shape")
+    dz = torch.empty_like(d3)
+    db = torch.empty(G, H, device=dh.device, dtype=torch.float32) if bias_grad else None
+    ws_bytes = lib().scmoe_gelu_bwd_workspace_bytes(G, C, H) if bias_grad else 0
+    ws = torch.empty(max(ws_bytes, 16), device=dh.device, dtype=torch.uint8)
+    check(lib().scmoe_gelu_bwd(ptr(_c(d3, "dh")), ptr(_c(z3, "z")), ptr(dz), ptr(db), G, C, H,
+                               ptr(group_rows), rows_clip, ptr(ws), ws_bytes, stream_ptr(stream)))
+    return (dz if dh.dim() == 3 else dz.view(C, H)), db
+
+
+def window_attention_supported(seq_len: int, head_dim: int) -> bool:
+    return bool(lib().scmoe_window_attention_supported(seq_len, head_dim))
+
+
+def window_attention_fwd(qkv: torch.Tensor, n_heads: int, seq_len: int, scale: float,
+                         causal: bool = False, need_lse: bool = True, stream=None):
+    """Windowed attention on the packed (T, 3d) projection -> (out (T, d),
+    lse (T, H) fp32 base-2 or None)."""
+    ensure_device(qkv)
+    T, d3 = qkv.shape
+    d = d3 // 3
+    out = torch.empty(T, d, device=qkv.device, dtype=qkv.dtype)
+    lse = torch.empty(T, n_heads, device=qkv.device, dtype=torch.float32) if need_lse else None
+    if qkv.dtype != torch.bfloat16:
+        raise ValueError("window attention is bf16")
+    check(lib().scmoe_window_attention_fwd(ptr(_c(qkv, "qkv")), T, n_heads, d // n_heads, seq_len,
+                                           float(scale), 1 if causal else 0, ptr(out), ptr(lse),
+                                           stream_ptr(stream)))
+    return out, lse
+
+
+def window_attention_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
+                         lse: torch.Tensor, n_heads: int, seq_len: int, scale: float,
+                         causal: bool = False, stream=None) -> torch.Tensor:
+    """dqkv (T, 3d) in the packed layout."""
+    ensure_device(qkv)
+    T, d3 = qkv.shape
+    dqkv = torch.empty_like(qkv)
+    check(lib().scmoe_window_attention_bwd(
+        ptr(_c(qkv, "qkv")), ptr(_c(out, "out")), ptr(_c(dout, "dout")), ptr(_c(lse, "lse")), T,
+        n_heads, d3 // 3 // n_heads, seq_len, float(scale), 1 if causal else 0, ptr(dqkv),
+        stream_ptr(stream)))
+    return dqkv
 
 
 _ONES = {}

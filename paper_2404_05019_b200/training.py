@@ -95,6 +95,12 @@ class LinearFn(torch.autograd.Function):
         return dx, dwt, res_grad, None
 
 
+# training FFN GELU: separate full-occupancy elementwise passes (True) or the
+# GEMM epilogues (False); at d = 384 the K = 384 tiles make the GEMMs'
+# elementwise epilogues the bottleneck (csrc/gelu.cu)
+SPLIT_GELU = True
+
+
 def _wsum(per_group: torch.Tensor, n_wgroups: int) -> torch.Tensor:
     """(G, n) per-group sums -> (W, n): group g feeds weight group g % W."""
     g = per_group.shape[0]
@@ -118,10 +124,17 @@ class FFNFn(torch.autograd.Function):
         w23 = w2t.unsqueeze(0) if w2t.dim() == 2 else w2t
         G, C, d = x3.shape
         h = w13.shape[1]
-        z = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
-        hid = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), aux_out=z,
-                                epilogue=_lib.EPI_BIAS_GELU, group_rows=group_rows,
-                                rows_clip=rows_clip, zero_tail=group_rows is not None)
+        if SPLIT_GELU:
+            # plain bias GEMM -> z, then h = gelu(z) as a full-occupancy pass
+            # (zero-padded tails for the weight gradients)
+            z = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), epilogue=_lib.EPI_BIAS,
+                                  group_rows=group_rows, rows_clip=rows_clip)
+            hid = K.gelu_fwd(z, group_rows, rows_clip)
+        else:
+            z = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
+            hid = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), aux_out=z,
+                                    epilogue=_lib.EPI_BIAS_GELU, group_rows=group_rows,
+                                    rows_clip=rows_clip, zero_tail=group_rows is not None)
         res3 = None if residual is None else residual.view(G, C, d)
         y = K.grouped_gemm_ex(hid, w23, _NK, d, bias=b2.view(-1, d), residual=res3,
                               group_rows=group_rows, rows_clip=rows_clip)
@@ -146,8 +159,15 @@ class FFNFn(torch.autograd.Function):
         grouped = group_rows is not None
         if grouped:
             K.zero_tails(dy3, group_rows, rows_clip)
-        dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
-                               group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+        if SPLIT_GELU:
+            # plain data-gradient GEMM -> dh, then dz = dh * gelu'(z) with the
+            # bias gradient (column sums of dz) in the same pass
+            dh = K.grouped_gemm_ex(dy3, w23, _KN, h, group_rows=group_rows, rows_clip=rows_clip)
+            dz, db1_g = K.gelu_bwd(dh, z, group_rows, rows_clip)
+        else:
+            dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
+                                   group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+            db1_g = None
         fuse_res = has_res and ctx.res_is_x
         parked = _take(ctx.link)
         extra = dy3 if fuse_res else (parked.view(G, C, d) if parked is not None else None)
@@ -161,7 +181,7 @@ class FFNFn(torch.autograd.Function):
         # loads in flight per thread), then the source groups of each weight
         # group summed like the weight gradients
         db2 = _wsum(K.grouped_colsum(dy3, group_rows, rows_clip), W)
-        db1 = _wsum(K.grouped_colsum(dz, group_rows, rows_clip), W)
+        db1 = _wsum(db1_g if db1_g is not None else K.grouped_colsum(dz, group_rows, rows_clip), W)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
                 (dy if has_res and not fuse_res else None), None, None, None)

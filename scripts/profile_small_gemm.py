@@ -10,6 +10,7 @@ a = torch.randn(M, Kd, device="cuda").bfloat16()
 wt = (torch.randn(N, Kd, device="cuda") / Kd ** 0.5).bfloat16()
 b = torch.zeros(N, device="cuda")
 mode = sys.argv[1] if len(sys.argv) > 1 else "plain"
+K.set_gemm_epilogue_warps(int(os.environ.get("SCMOE_EPI", "0")))
 gelu = mode == "gelu"
 if mode == "gbwd":        # training dgrad: dZ = (dY . W2) * gelu'(z), configs[1] shape
     from paper_2404_05019_b200 import _lib as L
