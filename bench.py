@@ -342,12 +342,13 @@ def run_reference(args):
 # our arm
 
 
-def build_blocks(w, ws, rank, dtype, group, ep_backend="nccl"):
+def build_blocks(w, ws, rank, dtype, group, ep_backend="nccl", p2p_ctas=16, sm_budget=True):
     import torch
     import paper_2404_05019_b200 as P
     n_exp = w["n_experts"] or max(ws, 1)
     common = dict(n_heads=w["heads"], seq_len=w["seq"], causal=w["causal"], dtype=dtype,
-                  capacity_factor=w["cf"], ep_group=group, ep_backend=ep_backend)
+                  capacity_factor=w["cf"], ep_group=group, ep_backend=ep_backend,
+                  p2p_ctas=p2p_ctas)
     # every-block placement (arch.py:632-663): one Transformer block whose
     # feed is the MoE layer; otherwise the Block-MLP + Block-MoE pair
     cls = P.ScMoEBlock if w.get("every_block") else P.ScMoEBlockPair
@@ -358,6 +359,9 @@ def build_blocks(w, ws, rank, dtype, group, ep_backend="nccl"):
     if n_exp >= 2:      # one expert in total (configs[1] shape at N=1) has no top-2
         gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
         t2 = cls(w["d"], w["h"], n_exp, variant="standard", k_routed=2, generator=gen, **common)
+    for b in (sc, t2):
+        if b is not None:
+            b.overlap_sm_budget = sm_budget
     return sc, t2, n_exp
 
 
@@ -533,6 +537,29 @@ def run_a2a_sweep(args):
     return 0
 
 
+def kernel_intervals(step):
+    """(name, start_us, end_us) of every kernel one step executes (CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step(None)
+        torch.cuda.synchronize()
+    out = []
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            out.append((ev.name, float(ev.time_range.start), float(ev.time_range.end)))
+    return out
+
+
+def _is_comm_kernel(name: str) -> bool:
+    return ("ep_dispatch_p2p" in name or "ep_return_p2p" in name or "nccl" in name.lower())
+
+
+def _is_wait_kernel(name: str) -> bool:
+    return "ep_wait" in name
+
+
 def count_launches(step):
     """(kernels of libscmoe.so, other kernels) launched by one step."""
     import torch
@@ -705,7 +732,8 @@ def run_ours(args):
         group = dist.group.WORLD
     T = w["seq"] * w["seqs"]
     d, h = w["d"], w["h"]
-    sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend)
+    sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend, args.p2p_ctas,
+                                 not args.no_sm_budget)
     ep_note = None
     if group is not None and args.ep_backend == "p2p":
         # map the peer buffers now (allocation + handle exchange); if any rank
@@ -724,7 +752,8 @@ def run_ours(args):
         if not all(flags):
             args.ep_backend = "nccl"
             ep_note = "p2p peer mapping failed on some rank; NCCL exchange"
-            sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend)
+            sc, t2, n_exp = build_blocks(w, ws, rank, dtype, group, args.ep_backend,
+                                         args.p2p_ctas, not args.no_sm_budget)
     gen = torch.Generator(device="cuda").manual_seed(99 + rank)
     x = torch.randn(T, d, device="cuda", generator=gen).to(dtype)
 
@@ -767,9 +796,15 @@ def run_ours(args):
                 if t2 is not None:
                     g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
                     run.update(lt2=lambda r: g_lt2.replay())
+            elif args.ep_backend == "p2p":
+                # the bare layer's p2p exchange (ScMoELayer._p2p_routed) is
+                # graph-safe too (device-side epochs)
+                g_lsc = CapturedStep(lambda xx: sc.moe(xx, src)[0], [x])
+                run.update(lsc=lambda r: g_lsc.replay())
+                if t2 is not None:
+                    g_lt2 = CapturedStep(lambda xx: t2.moe(xx)[0], [x])
+                    run.update(lt2=lambda r: g_lt2.replay())
             else:
-                # the bare layer's EP path is the NCCL exchange (the p2p
-                # exchange lives in the block's scheduled forward): eager
                 run.update(lsc=lambda r: sc.moe(x, src))
                 if t2 is not None:
                     run.update(lt2=lambda r: t2.moe(x))
@@ -811,6 +846,39 @@ def run_ours(args):
             torch.cuda.synchronize()
             barrier(ws)
             e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+
+        # expert parallelism: overlap measured on KERNEL execution intervals
+        # (CUPTI) of one step, and — on one rank — the step-time cost of the
+        # exchange itself: the EP block vs a local block with the same
+        # weights, interleaved graph replays
+        kov = None
+        ep_delta = None
+        if group is not None:
+            from paper_2404_05019_b200.timeline import kernel_overlap
+            iv = kernel_intervals(run["sc"])
+            frac, comm_us, exp_us = kernel_overlap(iv, _is_comm_kernel, _is_wait_kernel)
+            kov = {"fraction": frac, "comm_kernel_us": comm_us, "exposed_us": exp_us,
+                   "comm_kernels": sorted({n.split("(")[0][-40:] for n, _, _ in iv
+                                           if _is_comm_kernel(n)})}
+            if ws == 1 and use_graphs:
+                loc, _, _ = build_blocks(w, 1, rank, dtype, None)
+                with torch.no_grad():
+                    src_p = dict(sc.named_parameters())
+                    for name_, prm in loc.named_parameters():
+                        prm.copy_(src_p[name_])
+                    loc.slot = sc.slot
+                g_loc = CapturedStep(fwd(loc), [x])
+                ts = {"ep": [], "local": []}
+                for _ in range(max(3, args.ab_rounds)):
+                    ts["ep"].append(timed(run["sc"], max(3, args.steps // 2), ws)[0])
+                    ts["local"].append(timed(lambda r: g_loc.replay(), max(3, args.steps // 2),
+                                             ws)[0])
+                m_ep, m_loc = statistics.median(ts["ep"]), statistics.median(ts["local"])
+                ep_delta = {"ep_ms": m_ep, "local_ms": m_loc, "delta_ms": m_ep - m_loc,
+                            "note": "one rank: the exchange is a local HBM copy; delta = step "
+                                    "time the EP path adds over the same block without "
+                                    "exchange (interleaved graph replays, medians)"}
+                del loc, g_loc
 
         hbm_ops = hbm_kernel_times(sc.moe, x) if not args.no_hbm_ops else None
         # our kernels per step, counted from CUPTI over one step (graph replay)
@@ -875,6 +943,8 @@ def run_ours(args):
                    "tokens_per_gpu": T, "capacity_factor": w["cf"], "shortcut_pos": w["pos"],
                    "combine": w["combine"], "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "ep_backend": args.ep_backend if group is not None else None,
+                   "p2p_ctas": args.p2p_ctas if group is not None else None,
+                   "window_sm_budget": (not args.no_sm_budget) if group is not None else None,
                    "ep_note": ep_note,
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
         "speedup_vs_top2": med["t2"] / med["sc"] if "t2" in med else None,
@@ -892,6 +962,7 @@ def run_ours(args):
         "comm": {"overlap_fraction": overlap, "exposed_ms": exposed, "comm_ms": comm_ms,
                  "expert_slot": choice.slot, "schedule_costs_ms": json.loads(sc.last_costs.to_json()),
                  "makespan_predicted_ms": choice.makespan, "makespan_measured_ms": mk_meas,
+                 "kernel_overlap": kov, "ep_vs_local": ep_delta,
                  "makespan_note": "sched.slot_makespan (sched.py:83-85) of the chosen slot from "
                                   "the calibrated costs vs the measured device span of the "
                                   "window ops + expert + exchanges (eager steps, median)"},
@@ -968,6 +1039,11 @@ def main():
     ap.add_argument("--ep-backend", choices=("p2p", "nccl"), default="p2p",
                     help="expert-parallel exchange: our peer-memory kernels or NCCL all-to-all")
     ap.add_argument("--no-hbm-ops", action="store_true")
+    ap.add_argument("--p2p-ctas", type=int, default=16,
+                    help="CTAs of the side-stream exchange kernels (and SMs the window GEMMs "
+                         "leave free while one is in flight)")
+    ap.add_argument("--no-sm-budget", action="store_true",
+                    help="window GEMMs keep every SM while an exchange is in flight")
     ap.add_argument("--cpu-tokens", type=int, default=512)
     ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--ref-tokens", type=int, default=512)

@@ -216,6 +216,14 @@ int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_sr
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);
 
+/* SMs the persistent forward / dgrad GEMMs may occupy, 0 = all (default).
+ * The ScMoE block lowers it to (SMs - p2p_ctas) for the window operators
+ * that run while a peer-memory exchange kernel is in flight on the side
+ * stream, so the exchange executes concurrently (distsim.py:330-387 overlap
+ * made real on one device).  Host-side state read at launch (captured into
+ * CUDA graphs as launched). */
+int scmoe_set_gemm_sm_budget(int sms);
+
 /* Tuning / test hook: epilogue warps of the forward / dgrad tcgen05 GEMM,
  * 0 = auto (16 for K <= 1024 tiles with an elementwise epilogue, else 8),
  * 8 or 16 forced. */

@@ -211,7 +211,7 @@ class ScMoEBlockPair(nn.Module):
                  noise_enabled: bool = False, pre_layernorm: bool = False, n_heads: int = 1,
                  seq_len: Optional[int] = None, causal: bool = False, dtype=torch.bfloat16,
                  device=None, generator=None, ep_group=None, dgmoe_constraint: bool = True,
-                 chunks: int = 1, ep_backend: str = "nccl", p2p_ctas: int = 32,
+                 chunks: int = 1, ep_backend: str = "nccl", p2p_ctas: int = 16,
                  p2p_return: str = "fused"):
         super().__init__()
         if chunks < 1:
@@ -228,6 +228,8 @@ class ScMoEBlockPair(nn.Module):
         # the sources' back buffers over peer memory, tile by tile; "push" — a
         # separate copy kernel on the comm stream after the FFN
         self.ep_backend, self.p2p_ctas, self.p2p_return = ep_backend, p2p_ctas, p2p_return
+        # reserve p2p_ctas SMs for the exchange kernels during the window
+        self.overlap_sm_budget = True
         self._xchg = None
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
@@ -309,6 +311,14 @@ class ScMoEBlockPair(nn.Module):
         set per layer, re-created when the per-rank capacity changes)."""
         self._xchg = self.moe.peer_exchange(capacity)
         return self._xchg
+
+    def _window_sm_budget(self) -> int:
+        """SMs left to the window GEMMs while an exchange is in flight (0:
+        all, when overlap_sm_budget is off)."""
+        if not self.overlap_sm_budget:
+            return 0
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        return max(2, sms - max(self.p2p_ctas, 2))
 
     def comm_stream(self) -> torch.cuda.Stream:
         if self._comm_stream is None:
@@ -609,9 +619,23 @@ class ScMoEBlockPair(nn.Module):
 
         ops = dict(attn_prev=attn_prev, mlp_prev=mlp_prev, attn_cur=attn_cur, gate=gate,
                    encode=encode, expert=expert, shared=shared, decode=decode, dual=dual)
+        # while an exchange kernel is in flight on the comm stream (dispatch:
+        # from encode to the expert; push-form return: from the expert to
+        # decode), the window ops' persistent GEMMs leave p2p_ctas SMs free so
+        # the exchange runs concurrently instead of queueing behind them
+        budget = self._window_sm_budget() if (use_ep and not train and chunks == 1) else 0
+        in_flight = False
         for name in self.order():
+            if name == "expert":   # NCCL combine / push return run behind the expert
+                in_flight = (not p2p) or self.p2p_return == "push"
             with rec.op(name, "compute", st):
-                ops[name]()
+                if in_flight and budget and name not in ("expert", "decode"):
+                    with K.gemm_sm_budget(budget):
+                        ops[name]()
+                else:
+                    ops[name]()
+            if name == "encode":
+                in_flight = True
         dec = env["dec"]
         if self.variant == "dgmoe":
             res = (env["out"], dec, env["aux"])       # decision = (current, preceding)
@@ -688,6 +712,20 @@ class ScMoEBlockPair(nn.Module):
                   if self._PAIR or n not in ("attn_prev", "mlp_prev")]
         comm_d = durs.get("dispatch", 0.0)
         comm_c = durs.get("combine", 0.0)
+        if (self.ep_group is not None and self.ep_backend == "p2p" and self.p2p_return == "fused"
+                and comm_c == 0.0):
+            # the fused return travels inside the expert's GEMM2 epilogue and
+            # has no span of its own: measure the same transfer as the
+            # push-form return kernel so Eq. 10 sees t_comb > 0
+            self.p2p_return = "push"
+            try:
+                for _ in range(repeats):
+                    rec = Recorder()
+                    self.forward(h_in, recorder=rec)
+                    d = rec.durations().get("combine", 0.0)
+                    comm_c = d if comm_c == 0.0 else min(comm_c, d)
+            finally:
+                self.p2p_return = "fused"
         expert_ms = durs.get("expert", 0.0)
         if self.ep_group is not None:
             # the compute-stream "expert" span includes waiting on the

@@ -63,14 +63,14 @@ __global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs
 //         owns 16-byte column vector v and rows lane, lane + lanes, ... of the
 //         stripe with 8 loads in flight; the lanes' sums are added in a fixed
 //         order through shared memory -> one partial row per stripe.  Stripes
-//         are sized for ~2 blocks per SM so ~6+ MB of loads are in flight.
+//         are sized for ~6 blocks per SM: short, latency-bound row loops.
 // pass 2: block (32 columns x 32 stripe lanes), fixed-order sum of the
 //         stripes' partials.
 constexpr int COLSUM_THREADS = 256;
 
 int colsum_vec(int dtype) { return dtype == SCMOE_BF16 ? 8 : 4; }
 
-// stripes per group: ~2 blocks per SM over (column tiles x groups)
+// stripes per group: ~6 blocks per SM over (column tiles x groups)
 int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
   const int vecs = (cols + vec - 1) / vec;
   const int col_tiles = (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;

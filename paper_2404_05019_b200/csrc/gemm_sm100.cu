@@ -1075,6 +1075,16 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
 
 // mode: 0 auto, 1 force 1-SM, 2 force 2-SM (tests / tuning)
 static int g_gemm_mode = 0;
+// SMs the persistent forward / dgrad GEMMs may occupy (0 = all): while a
+// peer-memory exchange kernel is in flight on the side stream, the window
+// GEMMs leave its CTAs room to run concurrently instead of queueing behind
+// a grid that holds every SM (one CTA per SM, 384-640 threads, ~220 KB smem)
+static int g_gemm_sm_budget = 0;
+static int gemm_sms() {
+  const int all = num_sms();
+  if (g_gemm_sm_budget <= 0 || g_gemm_sm_budget >= all) return all;
+  return g_gemm_sm_budget < 2 ? 2 : (g_gemm_sm_budget & ~1);   // CTA pairs for cta_group::2
+}
 // tile width: 0 auto, 128 or 256 forced (tests / tuning)
 static int g_gemm_bn = 0;
 
@@ -1150,7 +1160,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
     p.c_cap = cs->capacity;
     p.c_k = cs->k;
   }
-  const int sms = num_sms();
+  const int sms = gemm_sms();
   auto tiles_of = [&](int tile_m, int bn) {
     return (long long)num_groups * ((cap + tile_m - 1) / tile_m) * ((N + bn - 1) / bn);
   };
@@ -1283,6 +1293,15 @@ extern "C" int scmoe_set_gemm_mode(int mode) {
     return SCMOE_ERR_ARG;
   }
   scmoe::g_gemm_mode = mode;
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_set_gemm_sm_budget(int sms) {
+  if (sms < 0) {
+    scmoe::set_error("gemm SM budget must be >= 0 (0 = all SMs)");
+    return SCMOE_ERR_ARG;
+  }
+  scmoe::g_gemm_sm_budget = sms;
   return SCMOE_OK;
 }
 

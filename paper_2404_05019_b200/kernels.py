@@ -195,6 +195,22 @@ def set_gemm_mode(mode: int) -> None:
     check(lib().scmoe_set_gemm_mode(mode))
 
 
+class gemm_sm_budget:
+    """Context manager: persistent GEMMs launched inside use at most `sms`
+    SMs (None / 0 = all) — room for a concurrent exchange kernel."""
+
+    def __init__(self, sms: Optional[int]):
+        self.sms = int(sms or 0)
+
+    def __enter__(self):
+        check(lib().scmoe_set_gemm_sm_budget(self.sms))
+        return self
+
+    def __exit__(self, *exc):
+        check(lib().scmoe_set_gemm_sm_budget(0))
+        return False
+
+
 def set_gemm_epilogue_warps(e: int) -> None:
     """0 = auto (16 for small-K elementwise-heavy tiles), 8 or 16 forced."""
     check(lib().scmoe_set_gemm_epilogue_warps(e))

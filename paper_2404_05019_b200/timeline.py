@@ -68,6 +68,27 @@ def window_makespan_ms(spans: Sequence[Span], window_ops: Sequence[str]) -> floa
     return max(s.end_ms for s in sel) - min(s.start_ms for s in sel)
 
 
+def kernel_overlap(intervals, is_comm, is_idle=lambda name: False):
+    """comm_overlap_fraction on KERNEL EXECUTION intervals (CUPTI start / end
+    of every kernel of one step, same device clock): the share of the
+    exchange kernels' execution time during which a compute kernel was also
+    executing.  Unlike the event spans, a comm kernel queued behind a grid
+    that holds every SM does not count as hidden.  `is_idle` drops kernels
+    that only wait (the flag-spin waits on the compute stream).
+    intervals: [(name, start_us, end_us)].  Returns (fraction, comm_us,
+    exposed_us)."""
+    comp = _union([(a, b) for n, a, b in intervals if not is_comm(n) and not is_idle(n)])
+    total = hidden = 0.0
+    for n, a, b in intervals:
+        if not is_comm(n):
+            continue
+        total += b - a
+        for x, y in comp:
+            hidden += max(0.0, min(y, b) - max(x, a))
+    frac = 1.0 if total == 0.0 else hidden / total
+    return frac, total, total - hidden
+
+
 class Recorder:
     """Records (start, end) event pairs per op; `spans()` syncs once."""
 
