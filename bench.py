@@ -715,6 +715,142 @@ def bench_training(args, ws, rank, group):
     return res
 
 
+_KEEPALIVE = []     # CUDA graphs and the peer buffers they captured
+
+
+def bench_offload(args, w, tokens, n_experts=None, seq_len=None):
+    """Memory-limited inference (paper App. A.3; reference offload.py:109-182,
+    simulate_decode): the routed experts in pinned host memory, migrated per
+    step.  For each token count (decode-size first): the block-pair latency
+    resident (GpuOnly), with blocking migration and with async migration
+    issued at the shortcut gate point, each engine (copy engine / SM
+    gather); the migration alone (activated experts only); stall =
+    latency(mode) - latency(resident) and overlap = (migration - stall) /
+    migration — the reference's OffloadReport fields, measured.  Eager steps
+    (the copy engine reads the activated-expert list back), CUDA events,
+    medians of interleaved rounds."""
+    import statistics
+    import torch
+    import paper_2404_05019_b200 as P
+    dev = torch.device("cuda")
+    n_exp = n_experts or w["n_experts"]
+
+    def make():
+        return P.ScMoEBlockPair(w["d"], w["h"], n_exp, variant="scmoe",
+                                shortcut_pos=w["pos"], combine_mode=w["combine"],
+                                n_heads=w["heads"], seq_len=seq_len, causal=w["causal"],
+                                capacity_factor=w["cf"], dtype=torch.bfloat16,
+                                generator=torch.Generator(device=dev).manual_seed(5))
+    res_blk = make()
+    torch.cuda.synchronize()
+    m0 = torch.cuda.memory_allocated()
+    arms = {"resident": res_blk}
+    for mode in ("blocking", "async"):
+        for eng in ("copy", "sm"):
+            blk = make()
+            blk.enable_offload(mode, eng)
+            arms[f"{mode}_{eng}"] = blk
+    torch.cuda.synchronize()
+    params = lambda b: sum(p.numel() * p.element_size() for p in b.parameters())
+    off_blk = arms["async_copy"]
+    expert_bytes = off_blk.offload.host_bytes() // n_exp
+    rows = []
+    for T in tokens:
+        g = torch.Generator(device=dev).manual_seed(11 + T)
+        x = torch.randn(T, w["d"], device=dev, generator=g).bfloat16()
+        ms = {k: [] for k in arms}
+        mig = []
+        with torch.no_grad():
+            for blk in arms.values():
+                for _ in range(2):
+                    blk(x)
+            torch.cuda.synchronize()
+            dec = off_blk.moe.route(x)
+            plan = off_blk.offload.plan(dec)
+            n_act = int(plan.n_active.item())
+            for _ in range(max(3, args.ab_rounds)):
+                for k, blk in arms.items():
+                    ms[k].append(timed(lambda r, blk=blk: blk(x), max(3, args.steps // 4), 1)[0])
+                # the migration alone (copy engine, activated experts only)
+                mig.append(timed(lambda r: off_blk.offload.migrate(off_blk.offload.plan(dec)),
+                                 max(3, args.steps // 4), 1)[0])
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            off_blk(x)
+            torch.cuda.synchronize()
+            peak_step = torch.cuda.max_memory_allocated() - base
+        med = {k: statistics.median(v) for k, v in ms.items()}
+        m_mig = statistics.median(mig)
+        lat0 = med["resident"]
+        row = {"tokens": T, "activated_experts": n_act,
+               "migration_bytes": n_act * expert_bytes, "migration_ms": m_mig,
+               "migration_gbps": n_act * expert_bytes / (m_mig * 1e-3) / 1e9,
+               "latency_ms": med, "modes": {}}
+        for k in arms:
+            if k == "resident":
+                continue
+            stall = max(0.0, med[k] - lat0)
+            row["modes"][k] = {"latency_ms": med[k], "stall_ms": stall,
+                               "overlap_fraction": (max(0.0, min(1.0, (m_mig - stall) / m_mig))
+                                                    if m_mig > 0 else 1.0)}
+        row["step_peak_extra_bytes"] = peak_step
+        rows.append(row)
+    return {"workload": w["name"] + ", routed experts offloaded", "n_experts": n_exp,
+            "seq_len": seq_len,
+            "expert_bytes": expert_bytes,
+            "device_param_bytes": {"resident": params(res_blk), "offloaded": params(off_blk)},
+            "rows": rows,
+            "note": "reference OffloadReport fields measured (offload.py:154-182): stall = "
+                    "latency - resident latency, overlap = (migration - stall) / migration; "
+                    "copy = cudaMemcpyAsync on the copy engine (expert list read back to the "
+                    "host), sm = gather kernel over the host link; eager steps"}
+
+
+def bench_pipeline(args, sc, t2, x, ws, use_graphs, fwd):
+    """ScMoE and top-2 block pairs with the exchange in 1 and n chunks
+    (`--pipeline-chunks`), each chunk count captured as its own CUDA graph on
+    the p2p backend (its own peer exchange: flags / epoch per chunk), eager on
+    NCCL; interleaved rounds, medians.  The exchanges the graphs captured are
+    kept alive for the graphs' lifetime."""
+    import statistics
+    from paper_2404_05019_b200.runtime import CapturedStep
+    counts = [1] + [int(c) for c in args.pipeline_chunks.split(",") if int(c) > 1]
+    keep = [b.moe._xchg for b in (sc, t2) if b is not None and getattr(b.moe, "_xchg", None)]
+    arms = {}
+    for c in counts:
+        for name, blk in (("scmoe", sc), ("top2", t2)):
+            if blk is None:
+                continue
+            blk.chunks = c
+            if use_graphs:
+                g = CapturedStep(fwd(blk), [x])
+                keep += [g, blk.moe._xchg]
+                arms[(name, c)] = (lambda r, g=g: g.replay())
+            else:
+                def eager(r, blk=blk, c=c):
+                    blk.chunks = c
+                    return blk(x)
+                arms[(name, c)] = eager
+    times = {k: [] for k in arms}
+    for _ in range(max(3, args.ab_rounds)):
+        for k, fn in arms.items():
+            times[k].append(timed(fn, max(3, args.steps // 2), ws)[0])
+    for blk in (sc, t2):
+        if blk is not None:
+            blk.chunks = 1
+    med = {k: statistics.median(v) for k, v in times.items()}
+    out = {"chunks": counts, "cuda_graph": use_graphs,
+           "scmoe_ms": {str(c): med[("scmoe", c)] for c in counts},
+           "top2_ms": {str(c): med.get(("top2", c)) for c in counts},
+           "note": "block-pair step per chunk count (medians of interleaved rounds); one "
+                   "exchange per chunk, chunk c's expert starts when its rows landed"}
+    if t2 is not None:
+        best_t2 = min(med[("top2", c)] for c in counts)
+        out["speedup_vs_best_top2"] = best_t2 / med[("scmoe", 1)]
+    _KEEPALIVE.extend(keep)
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_2404_05019_b200 as P
@@ -884,8 +1020,24 @@ def run_ours(args):
         # our kernels per step, counted from CUPTI over one step (graph replay)
         own_per_step, lib_per_step = count_launches(run["sc"])
 
+        # chunked pipelining (standard_pipeline / scmoe_overlap_pipeline,
+        # distsim.py:277-300, 358-364) under expert parallelism: the same
+        # blocks with their exchanges split into n chunks, interleaved rounds
+        pipeline = None
+        if group is not None and args.pipeline_chunks:
+            pipeline = bench_pipeline(args, sc, t2, x, ws, use_graphs, fwd)
+
     # ---- configs[1]: SwinV2-MoE-S stage-3 ScMoE block, bf16 training step ----
     training = None if args.no_training else bench_training(args, ws, rank, group)
+    offload = None
+    if ws == 1 and group is None and args.offload_tokens and not w.get("every_block"):
+        with torch.no_grad():
+            # configs[2] at decode sizes (one expert = 67 MB: the migration
+            # dwarfs any window) and the configs[1] shape with 8 experts
+            # (2.4 MB each: the window can hide it)
+            offload = {"gpt3xl": bench_offload(args, w, args.offload_tokens),
+                       "swinv2s_e8": bench_offload(args, WORKLOADS["swinv2s"], [1152, 18432],
+                                                   n_experts=8, seq_len=144)}
     clk.__exit__(None, None, None)
     clocks = clk.summary()
 
@@ -988,6 +1140,8 @@ def run_ours(args):
                               "how": "torch.profiler (CUPTI) over one step; 'scmoe' = kernels of "
                                      "libscmoe.so, library = cuDNN SDPA / torch copies"},
         "training": training,
+        "pipeline": pipeline,
+        "offload": offload,
     }
     if e2e_ms is not None:
         line["e2e"] = {"value": ws * T / (e2e_ms * 1e-3), "unit": "tokens/s",
@@ -1039,6 +1193,12 @@ def main():
     ap.add_argument("--ep-backend", choices=("p2p", "nccl"), default="p2p",
                     help="expert-parallel exchange: our peer-memory kernels or NCCL all-to-all")
     ap.add_argument("--no-hbm-ops", action="store_true")
+    ap.add_argument("--offload-tokens", type=lambda v: [int(t) for t in v.split(",") if t],
+                    default=[8, 2048],
+                    help="token counts of the expert-offload latency rows (empty to skip)")
+    ap.add_argument("--pipeline-chunks", default="2,4",
+                    help="chunk counts timed under expert parallelism (chunked pipelining); "
+                         "empty to skip")
     ap.add_argument("--p2p-ctas", type=int, default=16,
                     help="CTAs of the side-stream exchange kernels (and SMs the window GEMMs "
                          "leave free while one is in flight)")

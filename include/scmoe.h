@@ -205,6 +205,15 @@ int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap
 int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_t* ids,
                       const int32_t* n_rows, int max_rows, void* dst, void* stream);
 
+/* Expert migration on the COPY ENGINE (offload.py:109-182, the H2D transfer
+ * of the activated experts): dst[j] = src[ids[j]] for j < n_rows, rows of
+ * row_bytes, as cudaMemcpyAsync on `stream` (runs of consecutive ids merged
+ * into one copy).  ids is a HOST array (the caller read the activated-expert
+ * list back); no SM time is spent, so the copies overlap persistent GEMMs
+ * that hold every SM.  src: pinned host (or device) memory. */
+int scmoe_copy_rows(const void* src, size_t row_bytes, const int32_t* ids, int n_rows, void* dst,
+                    void* stream);
+
 /* Attention layout glue (training): n_src (<= 3) bf16 tensors (B, H, S, hd),
  * element strides[3*i .. 3*i+2] = (b, h, s) of source i, hd contiguous, packed
  * into dst (B, S, n_src, H, hd) contiguous — dq/dk/dv into the packed QKV

@@ -46,6 +46,7 @@ SIGNATURES = [
     ("scmoe_set_gemm_epilogue_warps", _i, [_i]),
     ("scmoe_set_gemm_sm_budget", _i, [_i]),
     ("scmoe_gather_rows", _i, [_vp, _sz, _vp, _vp, _i, _vp, _vp]),
+    ("scmoe_copy_rows", _i, [_vp, _sz, _vp, _i, _vp, _vp]),
     ("scmoe_grouped_gemm_ex", _i, [_vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                    _i, _i, _i, _i, _i, _vp]),
     ("scmoe_grouped_wgrad_workspace_bytes", _sz, [_i, _i, _i, _i]),

@@ -306,10 +306,11 @@ class ScMoEBlockPair(nn.Module):
     def _feed(self, h):
         return layer_norm(h) if self.pre_layernorm else h
 
-    def peer_exchange(self, capacity: int):
+    def peer_exchange(self, capacity: int, chunks: int = 1):
         """Peer-mapped buffers of the p2p backend — the MoE layer's own (one
-        set per layer, re-created when the per-rank capacity changes)."""
-        self._xchg = self.moe.peer_exchange(capacity)
+        set per layer, re-created when the per-rank capacity or the chunk
+        count changes)."""
+        self._xchg = self.moe.peer_exchange(capacity, chunks)
         return self._xchg
 
     def _window_sm_budget(self) -> int:
@@ -329,7 +330,14 @@ class ScMoEBlockPair(nn.Module):
         if self.variant == "dgmoe":
             return ["attn_prev", "mlp_prev", "attn_cur", "dual"]
         if self.variant == "scmoe":
-            o = sched.issue_order(self.shortcut_pos, self.slot if self.slot is not None else 0)
+            slot = self.slot
+            if slot is None:
+                # async expert offload: the expert after the whole window, so
+                # the migration started at the gate point has the window to
+                # hide behind (offload.py overlap_window); otherwise slot 0
+                async_off = self.offload is not None and self.offload_mode == "async"
+                slot = len(sched.WINDOW_OPS[self.shortcut_pos]) if async_off else 0
+            o = sched.issue_order(self.shortcut_pos, slot)
         else:
             o = sched.sequential_order()
             if self.variant == "standard":
@@ -384,8 +392,6 @@ class ScMoEBlockPair(nn.Module):
         if off is not None and (use_ep or chunks > 1):
             raise NotImplementedError("expert offload is a single-GPU, unchunked inference mode")
         p2p = use_ep and self.ep_backend == "p2p" and not train
-        if p2p and chunks > 1:
-            raise NotImplementedError("chunked pipelining runs on the nccl backend")
 
         def gate():
             if train:
@@ -399,18 +405,25 @@ class ScMoEBlockPair(nn.Module):
                 if chunks > 1:
                     env["cr"] = ep_mod.chunk_routing(env["dec"], chunks)
                 if off is not None:
-                    # activated experts -> device slots; async migration starts
-                    # here, at the (shortcut) gate point
+                    # activated experts -> device slots; the async migration
+                    # starts at the (shortcut) gate point: issued once the
+                    # next op is queued (the copy engine's host readback of
+                    # the expert list then never idles the GPU)
                     env["plan"] = off.plan(env["dec"])
-                    if self.offload_mode == "async":
-                        env["bufs"], env["mig_ev"] = off.migrate_async(env["plan"])
+                    env["mig_pending"] = self.offload_mode == "async"
 
         def encode_offload():
             dec, plan = env["dec"], env["plan"]
             env["buf"] = K.dispatch(src(), plan.slot_idx, dec.slots, plan.n_slots, dec.capacity)
 
+        def start_migration():
+            env["bufs"], env["mig_ev"] = off.migrate_async(env["plan"])
+            env["mig_pending"] = False
+
         def expert_offload():
             dec, plan = env["dec"], env["plan"]
+            if env.get("mig_pending"):     # no window op between the gate and the expert
+                start_migration()
             if self.offload_mode == "async":
                 st.wait_event(env["mig_ev"])
                 bufs = env["bufs"]
@@ -419,8 +432,27 @@ class ScMoEBlockPair(nn.Module):
             env["y"] = off.ffn(env["buf"], plan, bufs, dec.capacity)
 
         def encode_chunked():
-            # chunk-major buffer (chunks, E, Cc, d): chunk c's exchange is contiguous
             idx2, slot2, cc, rows = env["cr"]
+            if p2p:
+                # chunk c's kept rows straight to their owners, one p2p
+                # exchange per chunk (own flags / epoch): the owner starts
+                # chunk c's expert while chunk c+1 is still in flight
+                dec = env["dec"]
+                xg = self.peer_exchange(cc, chunks)
+                sl = ep_mod.chunk_slots(dec, chunks, cc)
+                cs.wait_stream(st)
+                env["disp_evs"] = []
+                for c in range(chunks):
+                    with rec.op(f"dispatch{c}", "comm", cs):
+                        xg.dispatch(src(), dec.indices, sl[c], rows[c], max_ctas=self.p2p_ctas,
+                                    stream=cs, chunk=c)
+                        ev = torch.cuda.Event()
+                        ev.record(cs)
+                    env["disp_evs"].append(ev)
+                sl.record_stream(cs)
+                rows.record_stream(cs)
+                return
+            # chunk-major buffer (chunks, E, Cc, d): chunk c's exchange is contiguous
             buf = K.dispatch(src(), idx2, slot2, chunks * moe.n_experts, cc)
             env["buf"] = buf.view(chunks, moe.n_experts, cc, -1)
             if use_ep:
@@ -433,6 +465,21 @@ class ScMoEBlockPair(nn.Module):
 
         def expert_chunked():
             idx2, slot2, cc, rows = env["cr"]
+            if p2p:
+                xg = self._xchg
+                for c in range(chunks):
+                    st.wait_event(env["disp_evs"][c])
+                    if self.p2p_return == "fused":
+                        xg.expert_ffn_to_peers(moe.experts, stream=st, chunk=c)
+                    else:
+                        xg.expert_ffn(moe.experts, signal=False, stream=st, chunk=c)
+                        cs.wait_stream(st)
+                        with rec.op(f"combine{c}", "comm", cs):
+                            xg.push_back(max_ctas=self.p2p_ctas, stream=cs, chunk=c)
+                            ev = torch.cuda.Event()
+                            ev.record(cs)
+                        env.setdefault("y_evs", []).append(ev)
+                return
             y = torch.empty_like(env["buf"])
             evs = []
             for c in range(chunks):
@@ -452,6 +499,16 @@ class ScMoEBlockPair(nn.Module):
         def decode_chunked():
             dec = env["dec"]
             idx2, slot2, cc, rows = env["cr"]
+            if p2p:
+                # every chunk's rows are back in the chunk-major back buffer
+                for ev in env.get("y_evs", []):      # push form: join the comm stream
+                    st.wait_event(ev)
+                kw = dict(residual=env["h_mh_cur"], stream=st)
+                if self.variant != "standard":
+                    kw.update(se_out=env["se"], mode=moe.combine_mode, x_cur=env["x_cur"],
+                              w_cg=moe.w_cg)
+                env["out"] = self._xchg.combine_local(idx2, slot2, dec.weights, **kw)
+                return
             for ev in env.get("y_evs", []):
                 st.wait_event(ev)
             if self.variant == "standard":
@@ -623,7 +680,7 @@ class ScMoEBlockPair(nn.Module):
         # from encode to the expert; push-form return: from the expert to
         # decode), the window ops' persistent GEMMs leave p2p_ctas SMs free so
         # the exchange runs concurrently instead of queueing behind them
-        budget = self._window_sm_budget() if (use_ep and not train and chunks == 1) else 0
+        budget = self._window_sm_budget() if (use_ep and not train and (chunks == 1 or p2p)) else 0
         in_flight = False
         for name in self.order():
             if name == "expert":   # NCCL combine / push return run behind the expert
@@ -636,6 +693,8 @@ class ScMoEBlockPair(nn.Module):
                     ops[name]()
             if name == "encode":
                 in_flight = True
+            elif env.get("mig_pending") and name != "gate":
+                start_migration()
         dec = env["dec"]
         if self.variant == "dgmoe":
             res = (env["out"], dec, env["aux"])       # decision = (current, preceding)
@@ -648,20 +707,25 @@ class ScMoEBlockPair(nn.Module):
         return res
 
     # -- memory-limited inference -----------------------------------------------
-    def enable_offload(self, mode: str = "async") -> "ScMoEBlockPair":
+    def enable_offload(self, mode: str = "async", engine: str = "copy") -> "ScMoEBlockPair":
         """Move the routed experts to pinned host memory (offload.py).  "async"
         starts the migration at the gate point (needs the ScMoE shortcut
         routing to overlap anything), "blocking" right before the expert
-        computation, "none" keeps them resident."""
-        from .offload import MODES, ExpertOffload
+        computation, "none" keeps them resident.  engine: "copy" (copy-engine
+        transfers, the expert list read back to the host) or "sm" (gather
+        kernel, no host round trip, graph-capturable)."""
+        from .offload import ENGINES, MODES, ExpertOffload
         if mode not in MODES:
             raise ConfigError(f"unknown offload mode {mode!r}")
+        if engine not in ENGINES:
+            raise ConfigError(f"unknown migration engine {engine!r}")
         if mode == "none":
             return self
         if self.variant == "dgmoe" or self.ep_group is not None:
             raise ConfigError("expert offload supports single-GPU ScMoE / shared / top-k layers")
         if self.offload is None:
-            self.offload = ExpertOffload(self.moe.experts, self.moe.k_routed)
+            self.offload = ExpertOffload(self.moe.experts, self.moe.k_routed, engine)
+        self.offload.engine = engine
         self.offload_mode = mode
         return self
 

@@ -409,6 +409,23 @@ extern "C" int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_
   return SCMOE_OK;
 }
 
+extern "C" int scmoe_copy_rows(const void* src, size_t row_bytes, const int32_t* ids,
+                               int n_rows, void* dst, void* stream) {
+  SCMOE_CHECK_ARG(src && dst && (ids || n_rows == 0) && n_rows >= 0, "bad copy_rows arguments");
+  const char* s = (const char*)src;
+  char* d = (char*)dst;
+  for (int j = 0; j < n_rows;) {
+    SCMOE_CHECK_ARG(ids[j] >= 0, "copy_rows: negative row id %d", ids[j]);
+    int run = 1;                    // consecutive source rows -> one transfer
+    while (j + run < n_rows && ids[j + run] == ids[j] + run) ++run;
+    SCMOE_CUDA_TRY(cudaMemcpyAsync(d + (size_t)j * row_bytes, s + (size_t)ids[j] * row_bytes,
+                                   (size_t)run * row_bytes, cudaMemcpyDefault,
+                                   (cudaStream_t)stream));
+    j += run;
+  }
+  return SCMOE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Attention layout glue for training (block.py _CudnnPackedAttention): up to
 // three (B, H, S, hd) tensors with arbitrary strides (hd contiguous) packed

@@ -104,6 +104,19 @@ def chunk_routing(dec, n_chunks: int):
     return idx2, slot2, cc, rows
 
 
+def chunk_slots(dec, n_chunks: int, cc: int) -> torch.Tensor:
+    """(n_chunks, T, k) int32: selection slots within chunk c (slot - c*cc) for
+    the kept selections that fall in chunk c, cc (dropped) for every other —
+    the per-chunk routing of the p2p dispatch, whose kernel sends only rows
+    with slot < capacity."""
+    s = dec.slots.long()
+    kept = s < dec.capacity
+    chunk = torch.div(s, cc, rounding_mode="floor")
+    c = torch.arange(n_chunks, device=s.device)[:, None, None]
+    mine = kept[None] & (chunk[None] == c)
+    return torch.where(mine, s[None] - c * cc, torch.full_like(s[None], cc)).to(torch.int32)
+
+
 def expert_parallel_ffn(experts, buf: torch.Tensor, dec, group=None) -> torch.Tensor:
     """Synchronous EP path of one layer (exchange, local grouped FFN,
     exchange back) on the current stream."""

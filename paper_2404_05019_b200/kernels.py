@@ -303,6 +303,23 @@ def gather_rows(src: torch.Tensor, ids: torch.Tensor, n_rows: torch.Tensor, max_
     return out
 
 
+def copy_rows(src: torch.Tensor, ids_host: torch.Tensor, n_rows: int, out: torch.Tensor,
+              stream=None) -> torch.Tensor:
+    """out[j] = src[ids_host[j]] for j < n_rows on the copy engine
+    (cudaMemcpyAsync on `stream`); ids_host is a host int32 tensor."""
+    ensure_device(out)
+    if src.is_cuda is False and not src.is_pinned():
+        raise ValueError("host-side source rows must be in pinned memory")
+    if ids_host.is_cuda or ids_host.dtype != torch.int32:
+        raise ValueError("copy_rows takes the row ids as a host int32 tensor")
+    if n_rows > out.shape[0] or n_rows > ids_host.numel():
+        raise ValueError("copy_rows: more rows than the output / id list holds")
+    row_bytes = src[0].numel() * src.element_size()
+    check(lib().scmoe_copy_rows(ptr(_c(src, "src")), row_bytes, ptr(ids_host), int(n_rows),
+                                ptr(_c(out, "out")), stream_ptr(stream)))
+    return out
+
+
 def gate_backward(src: torch.Tensor, logits: torch.Tensor, indices: torch.Tensor,
                   weights: torch.Tensor, counts: torch.Tensor, w_gate_t: torch.Tensor,
                   d_weights: Optional[torch.Tensor] = None, d_aux: Optional[torch.Tensor] = None,

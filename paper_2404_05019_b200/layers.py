@@ -467,14 +467,16 @@ class _RoutedMoE(nn.Module):
         from . import ep
         return ep.expert_parallel_ffn(self.experts, buf, dec, self.ep_group)
 
-    def peer_exchange(self, capacity: int):
+    def peer_exchange(self, capacity: int, chunks: int = 1):
         """Peer-mapped buffers of the p2p backend (re-created when the
-        capacity, i.e. the per-rank token count, changes)."""
+        per-chunk capacity, i.e. the per-rank token count, or the chunk count
+        changes)."""
         from .ep_p2p import PeerExchange
-        if self._xchg is None or self._xchg.capacity != capacity:
+        x = self._xchg
+        if x is None or x.capacity != capacity or x.chunks != chunks:
             self._xchg = PeerExchange.from_group(self.ep_group, self.experts.n_experts, capacity,
                                                  self.d_model, self.dtype,
-                                                 self.gate.w_gate_t.device)
+                                                 self.gate.w_gate_t.device, chunks=chunks)
         return self._xchg
 
     def _p2p_routed(self, x_src, dec, stream=None) -> torch.Tensor:

@@ -4,9 +4,17 @@
 The attention blocks, dense MLPs, gates and the shared expert stay resident.
 Routed-expert weights live in pinned host memory, and the device keeps
 S = min(N, T*k) expert slots. After the gate, the activated experts are
-compacted into slots on the device, and a gather kernel (scmoe_gather_rows)
-pulls their weights over the host link straight from the pinned buffers. The
-activated-expert list never leaves the GPU, so there is no host round trip.
+compacted into slots on the device.  Two migration engines:
+
+  "copy" (default): the activated-expert list (S int32) is read back into
+      pinned memory right after the gate, and the weights move as
+      cudaMemcpyAsync transfers on the COPY ENGINE (scmoe_copy_rows).  No SM
+      time: the transfer runs beside persistent GEMMs that hold every SM.
+      The host waits for the list only once the first window op is queued,
+      so the GPU never idles on the readback.
+  "sm": a gather kernel (scmoe_gather_rows) pulls the rows over the host
+      link; the list never leaves the GPU (no host round trip, CUDA-graph
+      capturable), but the kernel needs SMs the window GEMMs occupy.
 
   blocking : migrate right before the expert computation, on the compute
              stream (offload.py "OffloadBlocking")
@@ -23,12 +31,16 @@ weights, experts renumbered into slots.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from typing import Optional
 
 import torch
 
 from . import kernels as K
 
 MODES = ("none", "blocking", "async")
+
+
+ENGINES = ("copy", "sm")
 
 
 @dataclass
@@ -38,12 +50,17 @@ class SlotPlan:
     n_active: torch.Tensor   # (1,) int32 on the device
     rows: torch.Tensor       # (S,) int32 kept rows of slot s
     n_slots: int
+    host: Optional[torch.Tensor] = None      # pinned (S + 1,) int32: [n_active, ids...]
+    host_ev: Optional[torch.cuda.Event] = None
 
 
 class ExpertOffload:
     """Host-resident copies of a RoutedExperts module plus device slots."""
 
-    def __init__(self, experts, k_routed: int):
+    def __init__(self, experts, k_routed: int, engine: str = "copy"):
+        if engine not in ENGINES:
+            raise ValueError(f"unknown migration engine {engine!r}")
+        self.engine = engine
         self.experts = experts
         self.k = k_routed
         self.n = experts.n_experts
@@ -84,12 +101,31 @@ class ExpertOffload:
         rows.scatter_(0, slot_of.long(), kept.to(torch.int32))
         n_active = active.sum().to(torch.int32).reshape(1)
         slot_idx = slot_of[dec.indices.long()].to(torch.int32).contiguous()
-        return SlotPlan(slot_idx, ids[:s_cnt].contiguous(), n_active, rows[:s_cnt].contiguous(),
+        plan = SlotPlan(slot_idx, ids[:s_cnt].contiguous(), n_active, rows[:s_cnt].contiguous(),
                         s_cnt)
+        if self.engine == "copy":
+            # the activated-expert list to the host, queued right behind the gate
+            dev_l = torch.cat([n_active, plan.ids])
+            plan.host = torch.empty(s_cnt + 1, dtype=torch.int32, pin_memory=True)
+            plan.host.copy_(dev_l, non_blocking=True)
+        # the plan (and every earlier use of the slot buffers) is complete here:
+        # the migration waits on this, not on the window ops queued after it
+        plan.host_ev = torch.cuda.Event()
+        plan.host_ev.record()
+        return plan
 
     def migrate(self, plan: SlotPlan, stream=None):
-        """Pull the activated experts' weights into the slots (4 gathers)."""
+        """Bring the activated experts' weights into the slots: 4 copy-engine
+        transfers per run of consecutive experts ("copy": waits on the host for
+        the readback of the expert list) or 4 gather kernels ("sm")."""
         bufs = self.slot_buffers(plan.n_slots)
+        if self.engine == "copy":
+            plan.host_ev.synchronize()
+            n = int(plan.host[0])
+            ids = plan.host[1:]
+            for src, dst in zip(self.host, bufs):
+                K.copy_rows(src, ids, n, dst, stream=stream)
+            return bufs
         for src, dst in zip(self.host, bufs):
             K.gather_rows(src, plan.ids, plan.n_active, plan.n_slots, dst, stream=stream)
         return bufs
@@ -97,8 +133,7 @@ class ExpertOffload:
     def migrate_async(self, plan: SlotPlan):
         """Issue the migration on the copy stream after the gate; returns
         (buffers, event the expert computation must wait on)."""
-        cur = torch.cuda.current_stream(self.device)
-        self.copy_stream.wait_stream(cur)
+        self.copy_stream.wait_event(plan.host_ev)
         with torch.cuda.stream(self.copy_stream):
             bufs = self.migrate(plan, stream=self.copy_stream)
             ev = torch.cuda.Event()

@@ -24,7 +24,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, variant, q):
+def _worker(rank, world, port, variant, q, chunks=1):
     import sys
     sys.path.insert(0, ROOT)
     try:
@@ -39,7 +39,8 @@ def _worker(rank, world, port, variant, q):
                   capacity_factor=1.25, dtype=torch.bfloat16)
         loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(5),
                                **kw)
-        epb = P.ScMoEBlockPair(d, h, N, ep_group=dist.group.WORLD, ep_backend="p2p", **kw)
+        epb = P.ScMoEBlockPair(d, h, N, ep_group=dist.group.WORLD, ep_backend="p2p",
+                               chunks=chunks, **kw)
         e_l = N // world
         with torch.no_grad():
             src = dict(loc.named_parameters())
@@ -82,14 +83,17 @@ def _worker(rank, world, port, variant, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("variant", ["scmoe", "standard"])
-def test_p2p_ep_two_processes(variant):
+@pytest.mark.parametrize("variant,chunks", [("scmoe", 1), ("standard", 1), ("scmoe", 2),
+                                            ("standard", 3)])
+def test_p2p_ep_two_processes(variant, chunks):
+    """chunks > 1: chunked pipelining across the processes (one exchange per
+    chunk, chunk-major return rows)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     world, port = 2, _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, variant, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, variant, q, chunks)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}

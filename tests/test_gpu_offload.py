@@ -46,13 +46,33 @@ def test_gather_rows_from_pinned_host():
                       torch.empty(1, 8, device="cuda").bfloat16())
 
 
+def test_copy_rows_copy_engine():
+    """scmoe_copy_rows: host-known row ids, cudaMemcpyAsync per run of
+    consecutive ids (copy engine, no kernel)."""
+    from paper_2404_05019_b200 import kernels as K
+    src = torch.randn(12, 33, 40).bfloat16().pin_memory()
+    ids = torch.tensor([7, 8, 9, 2, 11, 0, 5], dtype=torch.int32)
+    out = torch.full((7, 33, 40), 7.0, device="cuda").bfloat16()
+    K.copy_rows(src, ids, 5, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:5].cpu(), src[ids[:5].long()])
+    assert torch.all(out[5:] == 7.0)
+    K.copy_rows(src.cuda(), ids, 7, out)          # device sources too
+    assert torch.equal(out.cpu(), src[ids.long()])
+    with pytest.raises(ValueError):
+        K.copy_rows(src, ids.cuda(), 1, out)       # ids must be on the host
+    with pytest.raises(ValueError):
+        K.copy_rows(src, ids, 8, out)
+
+
 @pytest.mark.parametrize("variant,k,cf", [("scmoe", 1, 1.25), ("standard", 2, 1.0),
                                           ("shared", 2, 0.5)])
 @pytest.mark.parametrize("mode", ["blocking", "async"])
+@pytest.mark.parametrize("engine", ["copy", "sm"])
 @pytest.mark.parametrize("T", [3, 64, 1024])
-def test_offload_equals_resident(variant, k, cf, mode, T):
+def test_offload_equals_resident(variant, k, cf, mode, engine, T):
     ref = _pair(variant, k, cf)
-    off = _pair(variant, k, cf).enable_offload(mode)
+    off = _pair(variant, k, cf).enable_offload(mode, engine)
     assert off.offload.host_bytes() > 0
     x = torch.randn(T, 256, device="cuda").bfloat16()
     with torch.no_grad():

@@ -74,9 +74,37 @@ def test_peer_exchange_layout_and_tables():
     bases = [1 << 40, 2 << 40, 3 << 40, 4 << 40]
     x.set_peer_bases(bases)
     for i, o in enumerate(offs):
-        assert x.tables[i].tolist() == [b + o for b in bases]
+        assert x.tables[0, i].tolist() == [b + o for b in bases]
     with pytest.raises(ValueError):
         x.set_peer_bases(bases[:2])
+
+
+def test_peer_exchange_chunked_layout():
+    """Chunked pipelining on the p2p backend: `chunks` independent exchanges
+    in one storage; chunk c's region i starts c * size_i / chunks after the
+    region, back rows are chunk-major (chunks * E, C, d) — the numbering of
+    ep.chunk_routing — and the fused-return targets of chunk c point into the
+    source's back rows of chunk c."""
+    from paper_2404_05019_b200.ep_p2p import PeerExchange
+    world, e_l, cc, d, n = 2, 4, 30, 64, 3
+    G = world * e_l
+    sizes, offs, total = PeerExchange.layout(world, e_l, cc, d, torch.bfloat16, chunks=n)
+    assert sizes == [n * G * cc * d * 2] * 3 + [n * G * 4, n * 2 * world * 4]
+    x = PeerExchange(world, 1, e_l, cc, d, torch.bfloat16, "cpu", chunks=n)
+    assert x.back.shape == (n * G, cc, d) and x.part("back", 2).shape == (G, cc, d)
+    assert x.part("recv_counts", 1).numel() == G and x.epoch.numel() == 4 * n
+    bases = [1 << 40, 2 << 40]
+    x.set_peer_bases(bases)
+    for c in range(n):
+        for i, o in enumerate(offs):
+            assert x.tables[c, i].tolist() == [b + o + c * sizes[i] // n for b in bases]
+        row = cc * d * 2
+        for g in range(G):
+            src, el = divmod(g, e_l)
+            assert x.group_out[c, g].item() == (bases[src] + offs[2] + c * sizes[2] // n +
+                                                (1 * e_l + el) * row)
+    with pytest.raises(ValueError):
+        PeerExchange(world, 0, e_l, cc, d, torch.bfloat16, "cpu", chunks=0)
 
 
 def test_bench_reference_arm_prints_one_json_line():
