@@ -296,7 +296,7 @@ class ScMoEBlockPair(nn.Module):
                                               device=device, ep_group=ep_group)
         elif cfg.variant == "dgmoe":
             ref = DGMoELayer.from_reference(layer, cap, constraint=m.moe.constraint, dtype=dtype,
-                                            device=device)
+                                            device=device, ep_group=ep_group)
         else:
             ref = ScMoELayer.from_reference(layer, cap, dtype=dtype, device=device,
                                             ep_group=ep_group)

@@ -650,20 +650,19 @@ class DGMoELayer(_RoutedMoE):
                  generator: Optional[torch.Generator] = None, ep_group=None):
         if n_experts < 2:
             raise ConfigError("dual gating needs at least 2 experts")
-        if ep_group is not None:
-            raise NotImplementedError("DGMoE under expert parallelism is not implemented")
         super().__init__(d_model, d_hidden, n_experts, 1, capacity_factor, noise_enabled,
                          dtype, device, generator, ep_group)
         self.constraint = dgmoe_constraint
 
     @classmethod
     def from_reference(cls, layer, capacity=None, constraint: bool = True, dtype=torch.bfloat16,
-                       device=None):
+                       device=None, ep_group=None):
         d, n = np.asarray(layer.gate.w_gate).shape
         h = np.asarray(layer.experts[0].w1).shape[1]
         cf = capacity.capacity_factor if capacity is not None else 2.0
         m = cls(d, h, n, capacity_factor=cf, dgmoe_constraint=constraint,
-                noise_enabled=bool(layer.gate.noise_enabled), dtype=dtype, device=device)
+                noise_enabled=bool(layer.gate.noise_enabled), dtype=dtype, device=device,
+                ep_group=ep_group)
         m._load_reference_common(layer)
         return m
 
@@ -720,6 +719,8 @@ class DGMoELayer(_RoutedMoE):
         slots = torch.cat([dec_cur.slots, dec_prev.slots], dim=1).contiguous()
         e = self.experts
         if train:
+            if self.ep_group is not None:
+                raise NotImplementedError("DGMoE training under expert parallelism")
             from . import training as TR
             w_cur, aux = TR.gate_weights_aux(self.gate, x_cur, dec_cur)
             kc, kp = dec_cur.kept_counts().int(), dec_prev.kept_counts().int()
@@ -732,6 +733,8 @@ class DGMoELayer(_RoutedMoE):
             out = TR.CombineFn.apply(y, None, w, None, None, residual, idx, slots,
                                      rows, cap, "direct_add")
             return out, dec_cur, dec_prev, aux
+        if self.ep_group is not None:
+            return self._forward_ep(x_cur, x_prev, dec_cur, dec_prev, cap, residual)
         buf = torch.empty(2 * n, cap, x_cur.shape[1], device=x_cur.device, dtype=x_cur.dtype)
         K.dispatch(x_cur, dec_cur.indices, dec_cur.slots, n, cap, out=buf[:n])
         K.dispatch(x_prev, dec_prev.indices, dec_prev.slots, n, cap, out=buf[n:])
@@ -739,4 +742,35 @@ class DGMoELayer(_RoutedMoE):
         y = self.experts(buf, rows, cap)
         w = torch.cat([dec_cur.weights, dec_prev.weights], dim=1).contiguous()
         out = K.combine(y, idx, slots, w, cap, residual=residual)
+        return out, dec_cur, dec_prev, dec_cur.aux_loss()
+
+    def _forward_ep(self, x_cur, x_prev, dec_cur, dec_prev, cap, residual):
+        """Expert parallelism (inference): the two gatings become ONE routing
+        of 2T rows (x_cur then x_prev, top-1 each) over the N experts with
+        2*cap slots per expert — the preceding gating's kept rows of expert e
+        sit right after the current gating's (slot' = kept_cur[e] + slot), so
+        every expert's rows stay contiguous — and go through the layer's EP
+        exchange (NCCL or p2p) unchanged.  The combine gathers
+        w_cur * y[e_cur, s_cur] + w_prev * y[e_prev, s'_prev] in the local
+        path's selection order, so the result equals the local layer bit for
+        bit (GEMM rows are independent of their position)."""
+        self._check_even_tokens(x_cur.shape[0])
+        n, cap2 = self.n_experts, 2 * cap
+        kc = dec_cur.kept_counts().to(torch.int32)
+        kp = dec_prev.kept_counts().to(torch.int32)
+        s_cur, s_prev = dec_cur.slots, dec_prev.slots
+        drop = torch.full_like(s_cur, cap2)
+        slot_cur = torch.where(s_cur < cap, s_cur, drop)
+        slot_prev = torch.where(s_prev < cap, kc[dec_prev.indices.long()] + s_prev, drop)
+        idx2 = torch.cat([dec_cur.indices, dec_prev.indices]).contiguous()        # (2T, 1)
+        slot2 = torch.cat([slot_cur, slot_prev]).contiguous()
+        both = GateDecision(torch.cat([dec_cur.logits, dec_prev.logits]), idx2,
+                            torch.cat([dec_cur.weights, dec_prev.weights]), slot2 >= cap2, slot2,
+                            kc + kp, dec_cur.prob_sum, cap2, cap2)
+        x2 = torch.cat([x_cur, x_prev])
+        y = self.routed_experts(x2, both)                       # (N, 2 cap, d), global experts
+        idx = torch.cat([dec_cur.indices, dec_prev.indices], dim=1).contiguous()
+        slots = torch.cat([slot_cur, slot_prev], dim=1).contiguous()
+        w = torch.cat([dec_cur.weights, dec_prev.weights], dim=1).contiguous()
+        out = K.combine(y, idx, slots, w, cap2, residual=residual)
         return out, dec_cur, dec_prev, dec_cur.aux_loss()

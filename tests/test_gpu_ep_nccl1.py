@@ -172,3 +172,27 @@ def test_ep_p2p_chunked_equals_local(variant, chunks, ret):
             ref, _, _ = loc(x)
             torch.cuda.synchronize()
             assert torch.equal(out, ref), it
+
+
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+@pytest.mark.parametrize("constraint", [True, False])
+def test_ep_dgmoe_equals_local(backend, constraint):
+    """DGMoE (dual gating, arch.py:507-533) under expert parallelism: both
+    gatings' rows travel as one 2T-row routing with 2*cap slots per expert;
+    the block output and both decisions equal the local block's bit for bit."""
+    import torch.distributed as dist
+    T, d, h, N = 1024, 256, 512, 8
+    kw = dict(variant="dgmoe", n_heads=4, seq_len=256, capacity_factor=1.0,
+              dtype=torch.bfloat16, dgmoe_constraint=constraint)
+    loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(8), **kw)
+    epb = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(8),
+                           ep_group=dist.group.WORLD, ep_backend=backend, **kw)
+    for it in range(2):
+        x = torch.randn(T, d, device="cuda").bfloat16()
+        with torch.no_grad():
+            a, (dca, dpa), _ = loc(x)
+            b, (dcb, dpb), _ = epb(x)
+        torch.cuda.synchronize()
+        assert torch.equal(dca.indices, dcb.indices) and torch.equal(dpa.slots, dpb.slots)
+        assert int(dpa.dropped.sum()) > 0 or int(dca.dropped.sum()) > 0   # cf 1.0 drops
+        assert torch.equal(a, b), it

@@ -34,7 +34,7 @@ def _worker(rank, world, port, variant, q, chunks=1):
                                 world_size=world)
         import paper_2404_05019_b200 as P
         T, d, h, N = 512, 256, 512, 4 * world
-        kw = dict(variant=variant, k_routed=1 if variant == "scmoe" else 2,
+        kw = dict(variant=variant, k_routed=2 if variant == "standard" else 1,
                   shortcut_pos="pos2" if variant == "scmoe" else None, n_heads=4, seq_len=256,
                   capacity_factor=1.25, dtype=torch.bfloat16)
         loc = P.ScMoEBlockPair(d, h, N, generator=torch.Generator(device="cuda").manual_seed(5),
@@ -66,7 +66,7 @@ def _worker(rank, world, port, variant, q, chunks=1):
         with torch.no_grad():
             x = torch.randn(T, d, device="cuda", generator=torch.Generator(device="cuda")
                             .manual_seed(7 + rank)).bfloat16()
-            if variant == "scmoe":
+            if variant in ("scmoe", "dgmoe"):
                 a = loc.moe(x, x.flip(0))[0]
                 b = epl(x, x.flip(0))[0]
             else:
@@ -84,7 +84,7 @@ def _worker(rank, world, port, variant, q, chunks=1):
 
 
 @pytest.mark.parametrize("variant,chunks", [("scmoe", 1), ("standard", 1), ("scmoe", 2),
-                                            ("standard", 3)])
+                                            ("standard", 3), ("dgmoe", 1)])
 def test_p2p_ep_two_processes(variant, chunks):
     """chunks > 1: chunked pipelining across the processes (one exchange per
     chunk, chunk-major return rows)."""
