@@ -221,6 +221,10 @@ int scmoe_copy_rows(const void* src, size_t row_bytes, const int32_t* ids, int n
 int scmoe_pack_heads(const void* const* srcs, const long long* strides, int n_src, int B, int H,
                      int S, int hd, int dtype, void* dst, void* stream);
 
+/* Experiment hook: bit 0 = epilogue operands (residual / pre-activation)
+ * read row-per-thread instead of staged through cp.async buffers. */
+int scmoe_set_gemm_flags(int flags);
+
 /* Tuning / test hook: 0 = pick the tcgen05 variant by problem size, 1 = force
  * the 1-SM 128x256 kernel, 2 = force the 2-SM (cta_group::2) 256x256 kernel. */
 int scmoe_set_gemm_mode(int mode);

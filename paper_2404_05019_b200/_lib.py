@@ -43,6 +43,7 @@ SIGNATURES = [
                                 _vp]),
     ("scmoe_set_gemm_mode", _i, [_i]),
     ("scmoe_set_gemm_tile_n", _i, [_i]),
+    ("scmoe_set_gemm_flags", _i, [_i]),
     ("scmoe_set_gemm_epilogue_warps", _i, [_i]),
     ("scmoe_set_gemm_sm_budget", _i, [_i]),
     ("scmoe_gather_rows", _i, [_vp, _sz, _vp, _vp, _i, _vp, _vp]),

@@ -110,6 +110,7 @@ struct Params {
   // pre-activation): the ring runs one stage short and that stage's A slot
   // (16 KB) holds the per-warp coalesced load buffers
   int ld_buf;
+  int dbg;                                 // experiment flags (g_gemm_flags)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -527,6 +528,39 @@ __device__ __forceinline__ void epilogue_chunk_gelu_bwd(uint32_t (&r)[32], const
   }
 }
 
+// residual (+ bias), every column in range: out = acc (+ b) + res, straight
+// line (the general epilogue_chunk is instruction-cache bound here: the
+// residual GEMMs of the training step ran ~10 us per tile slower through it)
+template <bool BIAS>
+__device__ __forceinline__ void epilogue_chunk_res(uint32_t (&r)[32], const float* __restrict__ sb,
+                                                   const uint4 (&pre)[4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[u * 8 + i]);
+    if (BIAS) {
+      const uint4 b0u = lds128(smem_u32(sb + u * 8)), b1u = lds128(smem_u32(sb + u * 8 + 4));
+      v[0] += __uint_as_float(b0u.x); v[1] += __uint_as_float(b0u.y);
+      v[2] += __uint_as_float(b0u.z); v[3] += __uint_as_float(b0u.w);
+      v[4] += __uint_as_float(b1u.x); v[5] += __uint_as_float(b1u.y);
+      v[6] += __uint_as_float(b1u.z); v[7] += __uint_as_float(b1u.w);
+    }
+    Vec16<__nv_bfloat16> rv;
+    rv.raw = pre[u];
+    float rf[8];
+    rv.to_float(rf);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += rf[i];
+    Vec16<__nv_bfloat16> w;
+    w.from_float(v);
+    r[4 * u] = w.raw.x;
+    r[4 * u + 1] = w.raw.y;
+    r[4 * u + 2] = w.raw.z;
+    r[4 * u + 3] = w.raw.w;
+  }
+}
+
 // fp32 wgrad partial: 32 columns of one output row
 __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32_t (&r)[32],
                                                    bool row_ok, bool zero, long long row_off,
@@ -732,6 +766,9 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
     // GELU backward with the pre-activation staged through the load buffer
     const bool fast_bwd = !WGRAD && p.epi == EPI_GELU_BWD && p.ld_buf && !p.bias && !p.residual &&
                           !p.aux_out && !p.c_k;
+    // residual (+ bias) with the residual staged through the load buffer
+    const bool fast_res = !WGRAD && p.epi == EPI_BIAS && p.residual && p.ld_buf && !p.aux_out &&
+                          !p.aux_in && !p.c_k && !p.zero_tail && !(p.dbg & 4);
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
       const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
@@ -836,7 +873,7 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         __syncwarp();
         if (c + NLB < NCH) issue_load(c + NLB);
       };
-      if (lsrc && p.ld_buf) {
+      if (lsrc && p.ld_buf && !(p.dbg & 2)) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");   // nothing left from the last tile
         __syncwarp();                  // the previous tile's reads of the buffers are done
         issue_load(0);
@@ -873,8 +910,9 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         const int n = tc.n0 + part * COLS_W + c * 32;
         if (WGRAD) {
           epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
-        } else if (fast && n + 32 <= p.N) {
-          // fast here means GELU (+ the pre-activation store in training)
+        } else if (fast && fast_gelu && n + 32 <= p.N) {
+          // bias + GELU (+ the pre-activation store in training); plain bias
+          // chunks of a partial tile take the general path below
           if (arow0) {
             __syncwarp();              // the previous flush's reads are done before z is staged
             epilogue_chunk_fast<true, true, true>(cur, sbw + c * 32, stg, lane);
@@ -888,9 +926,18 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
           take_load(c, pre);
           epilogue_chunk_gelu_bwd(cur, pre, row_ok);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
+        } else if (fast_res && n + 32 <= p.N) {
+          uint4 pre[4];
+          take_load(c, pre);
+          if (brow) epilogue_chunk_res<true>(cur, sbw + c * 32, pre);
+          else epilogue_chunk_res<false>(cur, nullptr, pre);
+          store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (n < p.N && wmask) {
           uint4 pre[4];
-          if (lsrc && p.ld_buf) {
+          if (p.dbg & 2) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pre[u] = make_uint4(0, 0, 0, 0);
+          } else if (lsrc && p.ld_buf) {
             take_load(c, pre);
           } else if (lsrc) {           // no load buffer (not expected): row-per-thread loads
 #pragma unroll
@@ -952,7 +999,7 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
 #pragma unroll 1
           for (int c = 0; c < NCH; c += 2) {
             chunk(std::true_type{}, c, ra, rb);
-            if (NCH > 1) chunk(std::true_type{}, c + 1, rb, ra);
+            if (c + 1 < NCH) chunk(std::true_type{}, c + 1, rb, ra);
           }
         } else {
 #pragma unroll 1
@@ -1087,14 +1134,23 @@ static int gemm_sms() {
 }
 // tile width: 0 auto, 128 or 256 forced (tests / tuning)
 static int g_gemm_bn = 0;
+// tuning / experiment flags: bit 0 = no staged (cp.async) epilogue operand
+// loads (row-per-thread loads instead)
+static int g_gemm_flags = 0;
 
-// Forward / dgrad tile width: 256 unless forced.  Measured on the configs[1]
-// shapes (scripts/ab_gemm_cublas.py train): BN = 128 loses even where it
-// removes a half-empty 256-column tile (n_out = 384: 729 vs 908 TFLOP/s) —
-// the narrower MMA re-reads A from shared memory per 128 columns.
-template <typename F>
-static int pick_bn(F&&, long long) {
-  return g_gemm_bn ? g_gemm_bn : 256;
+// Forward / dgrad tile width.  Measured on the configs[1] shapes
+// (scripts/ab_gemm_cublas.py train): BN = 128 loses even where it removes a
+// half-empty 256-column tile (n_out = 384: 729 vs 908 TFLOP/s) — the narrower
+// MMA re-reads A from shared memory per 128 columns.  BN = 192 (K-major
+// weights only) covers n_out = 384 / 1152 exactly where 256 leaves a half /
+// a fifth of the last column tile idle.
+static int pick_bn(int n_out, bool b_mn) {
+  if (g_gemm_bn) return (g_gemm_bn == 192 && b_mn) ? 256 : g_gemm_bn;
+  if (!b_mn) {
+    const int w256 = (n_out + 255) / 256 * 256 - n_out, w192 = (n_out + 191) / 192 * 192 - n_out;
+    if (w192 < w256) return 192;
+  }
+  return 256;
 }
 
 template <bool TWO_SM, bool B_MN, bool WGRAD>
@@ -1102,6 +1158,9 @@ static int launch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const
                      int grid, cudaStream_t st, bool wide_epi = false) {
   if constexpr (!WGRAD) {
     if (wide_epi && bn == 256) return sm100::launch<TWO_SM, B_MN, WGRAD, 256, 16>(ma, mb, p, grid, st);
+    if constexpr (!B_MN) {
+      if (bn == 192) return sm100::launch<TWO_SM, B_MN, WGRAD, 192>(ma, mb, p, grid, st);
+    }
   }
   return bn == 128 ? sm100::launch<TWO_SM, B_MN, WGRAD, 128>(ma, mb, p, grid, st)
                    : sm100::launch<TWO_SM, B_MN, WGRAD, 256>(ma, mb, p, grid, st);
@@ -1147,7 +1206,8 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
   p.out_groups = (__nv_bfloat16* const*)out_groups;
-  p.ld_buf = (residual || (epi == EPI_GELU_BWD && aux_in)) ? 1 : 0;
+  p.ld_buf = (residual || (epi == EPI_GELU_BWD && aux_in)) && !(g_gemm_flags & 1) ? 1 : 0;
+  p.dbg = g_gemm_flags;
   if (cs) {
     SCMOE_CHECK_ARG(num_groups == 1 && epi == EPI_BIAS && cs->k >= 1 && cs->k <= 2 && cs->y &&
                         cs->indices && cs->slots && cs->weights && cs->capacity >= 1 &&
@@ -1167,7 +1227,7 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_of(256, 256) >= sms / 2);
   const int tile_m = two ? 256 : 128;
   const long long max_units = two ? sms / 2 : sms;
-  const int bn = pick_bn([&](int b) { return tiles_of(tile_m, b); }, max_units);
+  const int bn = pick_bn(N, b_mn != 0);
   const long long tiles = tiles_of(tile_m, bn);
   const long long units = tiles < max_units ? tiles : max_units;
   if (units <= 0) return SCMOE_OK;
@@ -1177,8 +1237,10 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   const int b_rows = two ? bn / 2 : bn;
   rc = b_mn ? make_map(&mb, wt, N, K, n_wgroups, BK) : make_map(&mb, wt, K, N, n_wgroups, b_rows);
   if (rc) return rc;
-  const bool wide = !cs && !out_groups && wide_epilogue(K, epi, aux_out != nullptr,
-                                                         residual != nullptr);
+  // 16 epilogue warps split a 256-column tile in 64-column parts; the
+  // 192-column tile stays on 8 (96 columns each)
+  const bool wide = !cs && !out_groups && bn == 256 &&
+                    wide_epilogue(K, epi, aux_out != nullptr, residual != nullptr);
   if (two)
     rc = b_mn ? launch_bn<true, true, false>(bn, ma, mb, p, (int)units * 2, st, wide)
               : launch_bn<true, false, false>(bn, ma, mb, p, (int)units * 2, st, wide);
@@ -1287,6 +1349,11 @@ int make_map_2d(CUtensorMap* map, const void* base, int inner, int outer,
 
 }  // namespace scmoe
 
+extern "C" int scmoe_set_gemm_flags(int flags) {
+  scmoe::g_gemm_flags = flags;
+  return SCMOE_OK;
+}
+
 extern "C" int scmoe_set_gemm_mode(int mode) {
   if (mode < 0 || mode > 2) {
     scmoe::set_error("gemm mode must be 0 (auto), 1 (1-SM) or 2 (2-SM)");
@@ -1315,8 +1382,8 @@ extern "C" int scmoe_set_gemm_epilogue_warps(int e) {
 }
 
 extern "C" int scmoe_set_gemm_tile_n(int bn) {
-  if (bn != 0 && bn != 128 && bn != 256) {
-    scmoe::set_error("gemm tile width must be 0 (auto), 128 or 256");
+  if (bn != 0 && bn != 128 && bn != 192 && bn != 256) {
+    scmoe::set_error("gemm tile width must be 0 (auto), 128, 192 or 256");
     return SCMOE_ERR_ARG;
   }
   scmoe::g_gemm_bn = bn;

@@ -137,17 +137,22 @@ def _ref_ffn_rows(a, wt, bias, gelu):
 
 @pytest.mark.parametrize("G,W,C,Kd,N", [
     (1, 1, 128, 64, 256), (1, 1, 300, 200, 136), (8, 8, 512, 256, 1024), (4, 2, 130, 72, 520),
-    (8, 8, 1024, 2048, 8192), (3, 3, 257, 1024, 264), (16, 16, 64, 384, 1536)])
+    (8, 8, 1024, 2048, 8192), (3, 3, 257, 1024, 264), (16, 16, 64, 384, 1536),
+    (1, 1, 256, 128, 128), (1, 1, 256, 128, 384), (1, 1, 1000, 384, 1152),
+    (2, 2, 300, 128, 200), (1, 1, 256, 64, 32)])
 @pytest.mark.parametrize("gelu", [False, True])
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("tile_n", [128, 256])
+@pytest.mark.parametrize("tile_n", [128, 192, 256])
 def test_grouped_gemm_bf16(G, W, C, Kd, N, gelu, mode, tile_n):
-    """Both tcgen05 variants (1-SM 128xBN, 2-SM cta_group::2 256xBN) at both
-    tile widths (BN = 256, and 128 with four accumulator stages)."""
+    """Both tcgen05 variants (1-SM 128xBN, 2-SM cta_group::2 256xBN) at every
+    tile width (BN = 256; 192, the exact cover of n_out = 384 / 1152; 128
+    with four accumulator stages), with and without the residual epilogue
+    (bias + residual runs the straight-line residual path)."""
     K.set_gemm_mode(mode)
     K.set_gemm_tile_n(tile_n)
     try:
-        _grouped_gemm_case(G, W, C, Kd, N, gelu, residual=(mode == 2 and gelu))
+        _grouped_gemm_case(G, W, C, Kd, N, gelu,
+                           residual=(mode == 2 and gelu) or (not gelu and tile_n != 128))
     finally:
         K.set_gemm_mode(0)
         K.set_gemm_tile_n(0)
