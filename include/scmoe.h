@@ -205,6 +205,13 @@ int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap
 int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_t* ids,
                       const int32_t* n_rows, int max_rows, void* dst, void* stream);
 
+/* In-place SGD over n tensors in one launch (grad.py:330-331): p[i] -= lr *
+ * g[i] in fp32, rounded to the parameter dtype (SCMOE_BF16 / SCMOE_F32,
+ * gradient in the same dtype).  Host arrays of device pointers; numels a
+ * multiple of the 16-byte vector width, storage 16-byte aligned. */
+int scmoe_sgd_update(void* const* params, const void* const* grads, const long long* numels,
+                     const int* dtypes, int n, float lr, void* stream);
+
 /* Expert migration on the COPY ENGINE (offload.py:109-182, the H2D transfer
  * of the activated experts): dst[j] = src[ids[j]] for j < n_rows, rows of
  * row_bytes, as cudaMemcpyAsync on `stream` (runs of consecutive ids merged

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("scmoe_set_gemm_sm_budget", _i, [_i]),
     ("scmoe_gather_rows", _i, [_vp, _sz, _vp, _vp, _i, _vp, _vp]),
     ("scmoe_copy_rows", _i, [_vp, _sz, _vp, _i, _vp, _vp]),
+    ("scmoe_sgd_update", _i, [_vp, _vp, _vp, _vp, _i, ctypes.c_float, _vp]),
     ("scmoe_grouped_gemm_ex", _i, [_vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                    _i, _i, _i, _i, _i, _vp]),
     ("scmoe_grouped_wgrad_workspace_bytes", _sz, [_i, _i, _i, _i]),

@@ -745,7 +745,7 @@ class ScMoEBlockPair(nn.Module):
             p.grad = None
         out, dec, aux = self(h_in)
         if target is None:
-            loss = out.mean(dtype=torch.float32)      # fp32 accumulation, no fp32 copy of out
+            loss = TR.mean_loss(out)      # fp32 accumulation, no fp32 copy of out
         else:
             loss = (out.float() - target.float()).pow(2).sum() / out.shape[0]
         loss = loss + aux_coeff * aux
@@ -907,7 +907,7 @@ class ScMoEModel(nn.Module):
         for p in self.parameters():
             p.grad = None
         out, _, auxes = self(tokens)
-        loss = out.mean(dtype=torch.float32) if target is None else \
+        loss = TR.mean_loss(out) if target is None else \
             (out.float() - target.float()).pow(2).sum() / out.shape[0]
         for a in auxes:
             loss = loss + aux_coeff * a

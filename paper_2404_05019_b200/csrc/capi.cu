@@ -409,6 +409,89 @@ extern "C" int scmoe_gather_rows(const void* src, size_t row_bytes, const int32_
   return SCMOE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// In-place SGD over a list of tensors in ONE launch (grad.py:330-331,
+// p -= lr * g, fp32 arithmetic, rounded to the parameter dtype — the same
+// values as torch._foreach_add_(p, g, alpha=-lr)).  The tensor table travels
+// as a kernel parameter (no host->device copy, CUDA-graph capturable); 16-byte
+// vectors over the concatenated vector index space, grid-stride.
+namespace scmoe {
+namespace sgd_detail {
+constexpr int MAXT = 64;
+struct Table {
+  void* p[MAXT];
+  const void* g[MAXT];
+  long long vec_end[MAXT];      // inclusive prefix of 16-byte vectors
+  int bf16[MAXT];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ Table t, float lr,
+                                                  long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (t.vec_end[k] <= i) ++k;            // <= 64 tensors, warp-uniform mostly
+    const long long v = i - (k ? t.vec_end[k - 1] : 0);
+    uint4* pp = reinterpret_cast<uint4*>(t.p[k]) + v;
+    const uint4 gv = ld_nc_v4(reinterpret_cast<const uint4*>(t.g[k]) + v);
+    uint4 pv = *pp;
+    if (t.bf16[k]) {
+      Vec16<__nv_bfloat16> a, b;
+      a.raw = pv;
+      b.raw = gv;
+      float fa[8], fb[8];
+      a.to_float(fa);
+      b.to_float(fb);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) fa[e] = fmaf(-lr, fb[e], fa[e]);
+      a.from_float(fa);
+      pv = a.raw;
+    } else {
+      float* fa = reinterpret_cast<float*>(&pv);
+      const float* fb = reinterpret_cast<const float*>(&gv);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) fa[e] = fmaf(-lr, fb[e], fa[e]);
+    }
+    *pp = pv;
+  }
+}
+}  // namespace sgd_detail
+}  // namespace scmoe
+
+extern "C" int scmoe_sgd_update(void* const* params, const void* const* grads,
+                                const long long* numels, const int* dtypes, int n, float lr,
+                                void* stream) {
+  using namespace scmoe::sgd_detail;
+  SCMOE_CHECK_ARG(n >= 0 && (n == 0 || (params && grads && numels && dtypes)),
+                  "sgd_update: bad arguments");
+  for (int base = 0; base < n; base += MAXT) {
+    Table t = {};
+    long long tot = 0;
+    t.n = n - base < MAXT ? n - base : MAXT;
+    for (int j = 0; j < t.n; ++j) {
+      const int i = base + j;
+      SCMOE_CHECK_ARG(dtypes[i] == SCMOE_BF16 || dtypes[i] == SCMOE_F32, "sgd_update: dtype");
+      const int vec = dtypes[i] == SCMOE_BF16 ? 8 : 4;
+      SCMOE_CHECK_ARG(numels[i] % vec == 0 && ((uintptr_t)params[i] & 15) == 0 &&
+                          ((uintptr_t)grads[i] & 15) == 0,
+                      "sgd_update: tensor %d needs 16-byte aligned storage of whole vectors", i);
+      t.p[j] = params[i];
+      t.g[j] = grads[i];
+      t.bf16[j] = dtypes[i] == SCMOE_BF16;
+      tot += numels[i] / vec;
+      t.vec_end[j] = tot;
+    }
+    if (tot == 0) continue;
+    long long blocks = (tot + 255) / 256;
+    const long long cap = 4ll * scmoe::num_sms();
+    if (blocks > cap) blocks = cap;
+    sgd_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(t, lr, tot);
+    SCMOE_LAUNCH_CHECK();
+  }
+  return SCMOE_OK;
+}
+
 extern "C" int scmoe_copy_rows(const void* src, size_t row_bytes, const int32_t* ids,
                                int n_rows, void* dst, void* stream) {
   SCMOE_CHECK_ARG(src && dst && (ids || n_rows == 0) && n_rows >= 0, "bad copy_rows arguments");

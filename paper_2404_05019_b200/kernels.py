@@ -7,6 +7,7 @@ include/scmoe.h.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 from typing import Optional
@@ -301,6 +302,19 @@ def gather_rows(src: torch.Tensor, ids: torch.Tensor, n_rows: torch.Tensor, max_
     check(lib().scmoe_gather_rows(ptr(_c(src, "src")), row_bytes, ptr(_c(ids, "ids")),
                                   ptr(n_rows), max_rows, ptr(_c(out, "out")), stream_ptr(stream)))
     return out
+
+
+def sgd_update(params, grads, lr: float, stream=None) -> None:
+    """p -= lr * g for every (p, g) pair in one launch (bf16 / fp32 pairs of the
+    same dtype, 16-byte aligned whole vectors)."""
+    n = len(params)
+    if n == 0:
+        return
+    P = (ctypes.c_void_p * n)(*[p.data_ptr() for p in params])
+    G = (ctypes.c_void_p * n)(*[g.data_ptr() for g in grads])
+    N = (ctypes.c_longlong * n)(*[p.numel() for p in params])
+    D = (ctypes.c_int * n)(*[dtype_code(p.dtype) for p in params])
+    check(lib().scmoe_sgd_update(P, G, N, D, n, float(lr), stream_ptr(stream)))
 
 
 def copy_rows(src: torch.Tensor, ids_host: torch.Tensor, n_rows: int, out: torch.Tensor,

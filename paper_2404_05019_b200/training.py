@@ -331,17 +331,54 @@ class ExchangeFn(torch.autograd.Function):
         return ep.exchange_rows(d.contiguous(), ctx.group), None
 
 
+def _sgd_fusable(p: torch.Tensor) -> bool:
+    g = p.grad
+    vec = 8 if p.dtype == torch.bfloat16 else 4
+    return (p.is_cuda and p.dtype in (torch.bfloat16, torch.float32) and g.dtype == p.dtype
+            and p.is_contiguous() and g.is_contiguous() and p.numel() % vec == 0
+            and p.data_ptr() % 16 == 0 and g.data_ptr() % 16 == 0)
+
+
 def sgd_step(params, lr: float) -> None:
-    """In-place SGD (the reference's toy trainer, grad.py:330-331)."""
+    """In-place SGD (the reference's toy trainer, grad.py:330-331): every
+    parameter in ONE launch of scmoe_sgd_update (bf16 weights and fp32
+    biases alike; torch's multi-tensor apply ran it as ~70 CTAs, 22 us at
+    configs[1]).  Parameters the kernel cannot take (odd sizes / alignment)
+    go through torch's foreach add, same values."""
     with torch.no_grad():
-        # one multi-tensor launch per (dtype, grad dtype): a mixed list (bf16
-        # weights, fp32 biases) drops torch's foreach to one kernel per tensor
-        groups = {}
+        fused, rest = [], {}
         for p in params:
-            if p.grad is not None:
-                groups.setdefault((p.dtype, p.grad.dtype, p.device), []).append(p)
-        for ps in groups.values():
+            if p.grad is None:
+                continue
+            if _sgd_fusable(p):
+                fused.append(p)
+            else:
+                rest.setdefault((p.dtype, p.grad.dtype, p.device), []).append(p)
+        if fused:
+            K.sgd_update(fused, [p.grad for p in fused], lr)
+        for ps in rest.values():
             torch._foreach_add_(ps, [p.grad for p in ps], alpha=-lr)
+
+
+class MeanLossFn(torch.autograd.Function):
+    """mean(out) accumulated in fp32 (LossSpec "mean", grad.py:52-67); the
+    backward fills the constant gradient in one vectorised pass from the
+    device scalar (autograd's MeanBackward expanded it through a
+    non-vectorised broadcast kernel plus a dtype cast, ~22 us at configs[1])."""
+
+    @staticmethod
+    def forward(ctx, out):
+        ctx.shape, ctx.dtype, ctx.n = out.shape, out.dtype, out.numel()
+        return out.mean(dtype=torch.float32)
+
+    @staticmethod
+    def backward(ctx, g):
+        v = (g / ctx.n).to(ctx.dtype)
+        return torch.empty(ctx.shape, device=g.device, dtype=ctx.dtype).fill_(v)
+
+
+def mean_loss(out: torch.Tensor) -> torch.Tensor:
+    return MeanLossFn.apply(out)
 
 
 def allreduce_replicated_grads(module, group=None, experts_sharded: bool = True) -> None:

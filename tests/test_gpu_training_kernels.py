@@ -160,3 +160,33 @@ def test_bias_grad_tensor_core(G, W, C, N):
     for w in range(W):
         ref = sum(dy[gi, :int(rows[gi])].double().sum(0) for gi in range(w, G, W))
         _close(out[w], ref, rtol=1e-3)
+
+
+def test_sgd_update_matches_foreach():
+    """scmoe_sgd_update (one launch over every parameter) gives the values of
+    torch._foreach_add_(p, g, alpha=-lr): fp32 arithmetic, rounded once."""
+    from paper_2404_05019_b200 import training as TR
+    g = torch.Generator(device="cuda").manual_seed(3)
+    shapes = [((384, 1536), torch.bfloat16), ((1536,), torch.float32), ((8, 384), torch.float32),
+              ((3, 384, 384), torch.bfloat16), ((7,), torch.bfloat16)]     # 7: torch path
+    ps = [torch.randn(s, device="cuda", generator=g).to(dt) for s, dt in shapes]
+    gs = [torch.randn(s, device="cuda", generator=g).to(dt) for s, dt in shapes]
+    ref = [p.clone() for p in ps]
+    torch._foreach_add_(ref, gs, alpha=-0.03)
+    params = [torch.nn.Parameter(p) for p in ps]
+    for p, gr in zip(params, gs):
+        p.grad = gr
+    TR.sgd_step(params, 0.03)
+    for p, r in zip(params, ref):
+        assert torch.equal(p.data, r)
+
+
+def test_mean_loss_gradient():
+    from paper_2404_05019_b200 import training as TR
+    x = torch.randn(300, 64, device="cuda").bfloat16().requires_grad_(True)
+    l = TR.mean_loss(x)
+    l.backward()
+    x2 = x.detach().clone().requires_grad_(True)
+    l2 = x2.mean(dtype=torch.float32)
+    l2.backward()
+    assert torch.equal(l, l2) and torch.equal(x.grad, x2.grad)
