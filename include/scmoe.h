@@ -44,6 +44,7 @@ extern "C" {
 #define SCMOE_EPI_BIAS 0
 #define SCMOE_EPI_BIAS_GELU 1
 #define SCMOE_EPI_GELU_BWD 2     /* out = acc * gelu'(aux_in)  (tape.py:137-142) */
+#define SCMOE_EPI_MUL_AUX 3      /* out = acc * aux_in (aux_in = gelu'(z) saved by the forward) */
 
 /* weight operand layouts of scmoe_grouped_gemm_ex */
 #define SCMOE_W_NK 0             /* (W, n_out, k_in): the stored K-major weights */
@@ -403,6 +404,14 @@ int scmoe_window_attention_bwd(const void* qkv, const void* out, const void* dou
  *     the valid rows, fixed-order (deterministic) through the workspace. */
 int scmoe_gelu_fwd(const void* z, void* h, int num_groups, int group_cap, int cols,
                    const int32_t* group_rows, int rows_clip, void* stream);
+
+/* Training forward GELU that also saves the derivative: h = gelu(z) and
+ * dgelu = gelu'(z) (tape.py:137-142), both bf16, rows past rows(g) zero up to
+ * the 64-row block.  The backward then forms dz = (dy W2) * dgelu in the
+ * data-gradient GEMM's epilogue (SCMOE_EPI_MUL_AUX): no erf in the backward,
+ * no separate elementwise pass. */
+int scmoe_gelu_fwd_grad(const void* z, void* h, void* dgelu, int num_groups, int group_cap,
+                        int cols, const int32_t* group_rows, int rows_clip, void* stream);
 size_t scmoe_gelu_bwd_workspace_bytes(int num_groups, int group_cap, int cols);
 int scmoe_gelu_bwd(const void* dh, const void* z, void* dz, float* bias_grad, int num_groups,
                    int group_cap, int cols, const int32_t* group_rows, int rows_clip,

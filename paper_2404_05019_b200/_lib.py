@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("SCMOE_LIB") or os.path.join(_HERE, "libscmoe.so")
 SCMOE_OK, SCMOE_ERR_ARG, SCMOE_ERR_CUDA, SCMOE_ERR_UNSUPPORTED = 0, 1, 2, 3
 SCMOE_F32, SCMOE_BF16 = 0, 1
 COMBINE_MODES = {"direct_add": 0, "cg1": 1, "cg2": 2}
-EPI_BIAS, EPI_BIAS_GELU, EPI_GELU_BWD = 0, 1, 2
+EPI_BIAS, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_MUL_AUX = 0, 1, 2, 3
 W_NK, W_KN = 0, 1
 MAX_EXPERTS, MAX_K = 64, 8
 
@@ -81,6 +81,7 @@ SIGNATURES = [
     ("scmoe_window_attention_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, ctypes.c_float, _i,
                                         _vp, _vp]),
     ("scmoe_gelu_fwd", _i, [_vp, _vp, _i, _i, _i, _vp, _i, _vp]),
+    ("scmoe_gelu_fwd_grad", _i, [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp]),
     ("scmoe_gelu_bwd_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_gelu_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _sz, _vp]),
     ("scmoe_gate_backward_workspace_bytes", _sz, [_i, _i, _i, _i]),

@@ -66,11 +66,14 @@ __global__ void zero_tails_kernel(uint4* __restrict__ buf, int cap, int row_vecs
 //         are sized for ~6 blocks per SM: short, latency-bound row loops.
 // pass 2: block (32 columns x 32 stripe lanes), fixed-order sum of the
 //         stripes' partials.
-constexpr int COLSUM_THREADS = 256;
+constexpr int COLSUM_THREADS = 256;      // column vectors per block (max)
+constexpr int COLSUM_BLOCK = 256;        // threads per block: vectors x row lanes
 
 int colsum_vec(int dtype) { return dtype == SCMOE_BF16 ? 8 : 4; }
 
-// stripes per group: ~6 blocks per SM over (column tiles x groups)
+// stripes per group: ~6 blocks per SM over (column tiles x groups): short,
+// latency-bound row loops with many blocks in flight (fewer, longer stripes
+// measured slower); the final pass reads the partials four loads at a time
 int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
   const int vecs = (cols + vec - 1) / vec;
   const int col_tiles = (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
@@ -79,16 +82,16 @@ int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(COLSUM_THREADS)
+__global__ void __launch_bounds__(COLSUM_BLOCK)
 colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
                       const int32_t* __restrict__ group_rows, int rows_clip, int stripe_rows,
                       int n_stripes, float* __restrict__ part) {
   constexpr int VEC = Vec16<T>::N;
   constexpr int U = 8;
-  __shared__ float red[COLSUM_THREADS][VEC + 1];
+  __shared__ float red[COLSUM_BLOCK][VEC + 1];
   const int vecs = cols / VEC;
   const int vpb = min(vecs, COLSUM_THREADS);              // vectors per column tile
-  const int lanes = COLSUM_THREADS / vpb;
+  const int lanes = blockDim.x / vpb;
   const int v = threadIdx.x % vpb, lane = threadIdx.x / vpb;
   const int g = blockIdx.z, stripe = blockIdx.y;
   const int cv = blockIdx.x * vpb + v;                     // my column vector
@@ -143,17 +146,17 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int n_stripe
   __shared__ float red[32][33];
   const int g = blockIdx.y;
   const int c = blockIdx.x * 32 + threadIdx.x;
-  float a0 = 0.f, a1 = 0.f;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
   if (c < cols) {
     const float* p = part + (long long)g * n_stripes * cols + c;
     int k = threadIdx.y;
-    for (; k + 32 < n_stripes; k += 64) {
-      a0 += p[(long long)k * cols];
-      a1 += p[(long long)(k + 32) * cols];
+    for (; k + 96 < n_stripes; k += 128) {     // four independent loads in flight
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += p[(long long)(k + 32 * u) * cols];
     }
-    for (; k < n_stripes; k += 32) a0 += p[(long long)k * cols];
+    for (; k < n_stripes; k += 32) a[0] += p[(long long)k * cols];
   }
-  red[threadIdx.y][threadIdx.x] = a0 + a1;
+  red[threadIdx.y][threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
   __syncthreads();
   if (threadIdx.y == 0 && c < cols) {
     float t = 0.f;
@@ -219,7 +222,7 @@ extern "C" int scmoe_grouped_gemm_ex(const void* a, int dtype, const void* w, in
   SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
   SCMOE_CHECK_ARG(num_groups >= 1 && n_wgroups >= 1, "num_groups/n_wgroups must be >= 1");
   SCMOE_CHECK_ARG(group_cap >= 0 && n_out >= 1 && k_in >= 1, "bad GEMM shape");
-  SCMOE_CHECK_ARG(epilogue >= SCMOE_EPI_BIAS && epilogue <= SCMOE_EPI_GELU_BWD, "bad epilogue %d",
+  SCMOE_CHECK_ARG(epilogue >= SCMOE_EPI_BIAS && epilogue <= SCMOE_EPI_MUL_AUX, "bad epilogue %d",
                   epilogue);
   SCMOE_CHECK_ARG(w_layout == SCMOE_W_NK || w_layout == SCMOE_W_KN, "bad weight layout %d",
                   w_layout);
@@ -230,7 +233,7 @@ extern "C" int scmoe_grouped_gemm_ex(const void* a, int dtype, const void* w, in
     return grouped_gemm_bf16(a, w, w_layout == SCMOE_W_KN, bias, residual, aux_in, aux_out, out,
                              num_groups, n_wgroups, group_cap, group_rows, rows_clip, n_out, k_in,
                              epilogue, zero_tail, st);
-  SCMOE_CHECK_ARG(w_layout == SCMOE_W_NK && epilogue != SCMOE_EPI_GELU_BWD && !aux_out &&
+  SCMOE_CHECK_ARG(w_layout == SCMOE_W_NK && epilogue <= SCMOE_EPI_BIAS_GELU && !aux_out &&
                       !zero_tail,
                   "the fp32 parity GEMM supports the forward epilogues only");
   return grouped_gemm_f32((const float*)a, (const float*)w, bias, (const float*)residual,
@@ -377,14 +380,15 @@ extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, in
   const int col_tiles = (vecs + vpb - 1) / vpb;
   const int n_stripes = colsum_stripes(num_groups, group_cap, cols, vec);
   const int stripe_rows = (group_cap + n_stripes - 1) / n_stripes;
+  const int threads = (COLSUM_BLOCK / vpb) * vpb;          // whole row lanes of vpb vectors
   dim3 grid(col_tiles, n_stripes, num_groups);
   float* part = (float*)workspace;
   if (dtype == SCMOE_BF16)
-    colsum_partial_kernel<__nv_bfloat16><<<grid, COLSUM_THREADS, 0, st>>>(
+    colsum_partial_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
         (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes,
         part);
   else
-    colsum_partial_kernel<float><<<grid, COLSUM_THREADS, 0, st>>>(
+    colsum_partial_kernel<float><<<grid, threads, 0, st>>>(
         (const float*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes, part);
   SCMOE_LAUNCH_CHECK();
   colsum_final_kernel<<<dim3((cols + 31) / 32, num_groups), dim3(32, 32), 0, st>>>(

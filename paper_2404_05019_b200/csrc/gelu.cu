@@ -45,9 +45,43 @@ __device__ __forceinline__ uint4 gelu_vec(uint4 raw) {
   return a.raw;
 }
 
+// gelu(x) and gelu'(x) sharing the reciprocal and the exponential: the same
+// operation sequences as gelu_erf_fast / gelu_grad_fast, so both values are
+// bit-identical to the separate evaluations
+__device__ __forceinline__ void gelu_both(float x, float& g, float& dg) {
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752440f, fabsf(x), 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float e = ex2_approx((x * x) * -0.72134752044448170368f);   // exp(-x^2/2)
+  const float erf_abs = fmaf(-p, e, 1.0f);
+  const float hx = 0.5f * x;
+  g = fmaf(fabsf(hx), erf_abs, hx);
+  const float erf_v = copysignf(erf_abs, x);
+  dg = fmaf(0.5f, erf_v, 0.5f) + x * e * 0.39894228040143267794f;
+}
+
+__device__ __forceinline__ void gelu_vec2(uint4 raw, uint4& h, uint4& dh) {
+  Vec16<__nv_bfloat16> a;
+  a.raw = raw;
+  float f[8], g[8], d[8];
+  a.to_float(f);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) gelu_both(f[e], g[e], d[e]);
+  a.from_float(g);
+  h = a.raw;
+  a.from_float(d);
+  dh = a.raw;
+}
+
+// h = gelu(z) and, with GRAD, dg = gelu'(z) (the backward then multiplies
+// in the data-gradient GEMM's epilogue instead of re-evaluating erf)
+template <bool GRAD>
 __global__ void __launch_bounds__(GT)
-gelu_fwd_kernel(const uint4* __restrict__ z, uint4* __restrict__ h, int cap, int vecs_per_row,
-                const int32_t* __restrict__ gr, int clip) {
+gelu_fwd_kernel(const uint4* __restrict__ z, uint4* __restrict__ h, uint4* __restrict__ dg,
+                int cap, int vecs_per_row, const int32_t* __restrict__ gr, int clip) {
   const int g = blockIdx.y;
   const int rows = rows_valid(gr, g, clip, cap);
   const int rows_pad = gr ? rows_padded(rows, cap) : cap;
@@ -61,10 +95,21 @@ gelu_fwd_kernel(const uint4* __restrict__ z, uint4* __restrict__ h, int cap, int
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(z + base + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) h[base + i + u * stride] = gelu_vec(v[u]);
+    for (int u = 0; u < 4; ++u) {
+      if (GRAD) gelu_vec2(v[u], h[base + i + u * stride], dg[base + i + u * stride]);
+      else h[base + i + u * stride] = gelu_vec(v[u]);
+    }
   }
-  for (; i < n_pad; i += stride)
-    h[base + i] = i < n ? gelu_vec(ld_nc_v4(z + base + i)) : make_uint4(0, 0, 0, 0);
+  for (; i < n_pad; i += stride) {
+    if (GRAD) {
+      uint4 a = make_uint4(0, 0, 0, 0), b = a;
+      if (i < n) gelu_vec2(ld_nc_v4(z + base + i), a, b);
+      h[base + i] = a;
+      dg[base + i] = b;
+    } else {
+      h[base + i] = i < n ? gelu_vec(ld_nc_v4(z + base + i)) : make_uint4(0, 0, 0, 0);
+    }
+  }
 }
 
 // block (column tile of up to GT vectors, row stripe, group); thread (v, lane)
@@ -201,8 +246,30 @@ extern "C" int scmoe_gelu_fwd(const void* z, void* h, int num_groups, int group_
   long long bx = (per_group + GT * 4 - 1) / (GT * 4);
   const long long cap_bx = 8ll * num_sms() / num_groups;
   if (bx > cap_bx) bx = cap_bx;
-  gelu_fwd_kernel<<<dim3((unsigned)(bx < 1 ? 1 : bx), num_groups), GT, 0, (cudaStream_t)stream>>>(
-      (const uint4*)z, (uint4*)h, group_cap, cols / 8, group_rows, rows_clip);
+  gelu_fwd_kernel<false><<<dim3((unsigned)(bx < 1 ? 1 : bx), num_groups), GT, 0,
+                           (cudaStream_t)stream>>>((const uint4*)z, (uint4*)h, nullptr, group_cap,
+                                                   cols / 8, group_rows, rows_clip);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_gelu_fwd_grad(const void* z, void* h, void* dgelu, int num_groups,
+                                   int group_cap, int cols, const int32_t* group_rows,
+                                   int rows_clip, void* stream) {
+  SCMOE_CHECK_ARG(z && h && dgelu && num_groups >= 1 && group_cap >= 1 && cols >= 8 &&
+                      cols % 8 == 0,
+                  "gelu_fwd_grad: bad arguments");
+  SCMOE_CHECK_ARG(((uintptr_t)z & 15) == 0 && ((uintptr_t)h & 15) == 0 &&
+                      ((uintptr_t)dgelu & 15) == 0,
+                  "gelu_fwd_grad: 16-byte aligned bf16 rows needed");
+  if (rows_clip <= 0) rows_clip = group_cap;
+  const long long per_group = (long long)group_cap * cols / 8;
+  long long bx = (per_group + GT * 4 - 1) / (GT * 4);
+  const long long cap_bx = 8ll * num_sms() / num_groups;
+  if (bx > cap_bx) bx = cap_bx;
+  gelu_fwd_kernel<true><<<dim3((unsigned)(bx < 1 ? 1 : bx), num_groups), GT, 0,
+                          (cudaStream_t)stream>>>((const uint4*)z, (uint4*)h, (uint4*)dgelu,
+                                                  group_cap, cols / 8, group_rows, rows_clip);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

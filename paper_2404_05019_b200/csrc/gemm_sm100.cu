@@ -84,7 +84,7 @@ struct Idesc {
                                     ((uint32_t)(Cfg<TWO_SM, BN>::TILE_M >> 4) << 24);
 };
 
-enum Epi { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GELU_BWD = 2 };
+enum Epi { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GELU_BWD = 2, EPI_MUL_AUX = 3 };
 
 struct Params {
   int num_groups, n_wgroups, cap, rows_clip, N, K, epi, zero_tail;
@@ -418,6 +418,13 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, uint32_t (&r)[32
         zv.to_float(z);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(z[i]);
+      } else if (p.epi == EPI_MUL_AUX) {
+        Vec16<__nv_bfloat16> zv;
+        zv.raw = pre[u];                       // gelu'(z) saved by the forward
+        float z[8];
+        zv.to_float(z);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= z[i];
       }
       if (!LEAN && p.c_k) {
         // the ScMoE combine, same fp32 sequence as combine_kernel: shared
@@ -508,7 +515,9 @@ __device__ __forceinline__ void epilogue_chunk_fast(uint32_t (&r)[32],
 }
 
 // GELU backward, every column in range, no bias / residual: dZ = acc *
-// gelu'(z) with z from the staged load; padding rows (zero tails) get zeros
+// gelu'(z) with z from the staged load (MUL: the staged operand already is
+// gelu'(z), saved by the forward); padding rows (zero tails) get zeros
+template <bool MUL>
 __device__ __forceinline__ void epilogue_chunk_gelu_bwd(uint32_t (&r)[32], const uint4 (&pre)[4],
                                                         bool row_ok) {
 #pragma unroll
@@ -518,7 +527,8 @@ __device__ __forceinline__ void epilogue_chunk_gelu_bwd(uint32_t (&r)[32], const
     float z[8], v[8];
     zv.to_float(z);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = row_ok ? __uint_as_float(r[u * 8 + i]) * gelu_grad_fast(z[i]) : 0.f;
+    for (int i = 0; i < 8; ++i)
+      v[i] = row_ok ? __uint_as_float(r[u * 8 + i]) * (MUL ? z[i] : gelu_grad_fast(z[i])) : 0.f;
     Vec16<__nv_bfloat16> w;
     w.from_float(v);
     r[4 * u] = w.raw.x;
@@ -607,13 +617,14 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
   uint4* s_stage = reinterpret_cast<uint4*>(s_bias + E * 128);   // 2 KB per epilogue warp
   const int ring = C::STAGES - p.ld_buf;                                   // mainloop stages
-  // if ld_buf: the lent stage's A slot (and its B slot when >= 16 KB) hold the
-  // per-warp load buffers, NLB chunks in flight (16 warps: one chunk each,
-  // warps 0-7 in the A slot, 8-15 in the B slot)
-  constexpr int NLB = E == 16 ? 1 : (C::B_BYTES >= 16384 ? 2 : 1);
-  static_assert(E == 8 || C::B_BYTES >= 16384, "16 epilogue warps need a 16 KB B slot");
-  uint4* s_load0 = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 1) * C::A_BYTES);
-  uint4* s_load1 = reinterpret_cast<uint4*>(smem_b + (C::STAGES - 1) * C::B_BYTES);
+  // if ld_buf (= 2): the last two ring stages are lent to the epilogue: their
+  // A slots (32 KB) and B slots hold one 2 KB load buffer per (epilogue warp,
+  // chunk), so a tile's whole row-major operand (residual / saved gelu') is
+  // requested at the tile start, before the accumulator wait
+  constexpr int LB_A = 2 * C::A_BYTES / 2048;              // buffers in the A slots
+  static_assert(E * NCH <= LB_A + 2 * C::B_BYTES / 2048, "epilogue load buffers do not fit");
+  uint4* s_load0 = reinterpret_cast<uint4*>(smem_a + (C::STAGES - 2) * C::A_BYTES);
+  uint4* s_load1 = reinterpret_cast<uint4*>(smem_b + (C::STAGES - 2) * C::B_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -764,8 +775,9 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
     const bool fast_gelu = p.epi == EPI_BIAS_GELU;
     const bool lean = !p.c_k && !p.residual;   // epilogue_chunk<true>: combine / residual out
     // GELU backward with the pre-activation staged through the load buffer
-    const bool fast_bwd = !WGRAD && p.epi == EPI_GELU_BWD && p.ld_buf && !p.bias && !p.residual &&
-                          !p.aux_out && !p.c_k;
+    const bool fast_bwd = !WGRAD && (p.epi == EPI_GELU_BWD || p.epi == EPI_MUL_AUX) && p.ld_buf &&
+                          !p.bias && !p.residual && !p.aux_out && !p.c_k;
+    const bool mul_aux = p.epi == EPI_MUL_AUX;
     // residual (+ bias) with the residual staged through the load buffer
     const bool fast_res = !WGRAD && p.epi == EPI_BIAS && p.residual && p.ld_buf && !p.aux_out &&
                           !p.aux_in && !p.c_k && !p.zero_tail && !(p.dbg & 4);
@@ -833,17 +845,19 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
       }
       const uint32_t wmask = __ballot_sync(0xffffffffu, row_ok || pad_row);
       uint4* stg = s_stage + ew * 128;
-      // the row-major epilogue operand (residual / pre-activation), 32 rows x
-      // 64 B per chunk: coalesced cp.async into this warp's load buffers
-      // (same swizzle as the store staging), chunks c+1 .. c+NLB-1 in flight
-      // while chunk c is processed, the first NLB issued before the
-      // accumulator wait
+      // the row-major epilogue operand (residual / pre-activation / gelu'),
+      // 32 rows x 64 B per chunk: coalesced cp.async into this warp's load
+      // buffers (same swizzle as the store staging), every chunk of the tile
+      // issued (one commit group each) before the accumulator wait, so the
+      // epilogue never waits on a load issued while it was running
       const __nv_bfloat16* lsrc =
-          WGRAD ? nullptr : (p.residual ? p.residual : (p.epi == EPI_GELU_BWD ? p.aux_in : nullptr));
+          WGRAD ? nullptr
+                : (p.residual ? p.residual
+                              : ((p.epi == EPI_GELU_BWD || p.epi == EPI_MUL_AUX) ? p.aux_in : nullptr));
       const uint32_t lmask = __ballot_sync(0xffffffffu, row_ok);
       auto lbuf = [&](int c) {
-        if (E == 16) return (ew < 8 ? s_load0 + ew * 128 : s_load1 + (ew - 8) * 128);
-        return ((NLB == 2 && (c & 1)) ? s_load1 : s_load0) + ew * 128;
+        const int q = ew * NCH + c;
+        return q < LB_A ? s_load0 + q * 128 : s_load1 + (q - LB_A) * 128;
       };
       const long long lrow0 = ((long long)tc.g * p.cap + row_w0) * p.N;
       auto issue_load = [&](int c) __attribute__((always_inline)) {
@@ -861,23 +875,25 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       };
-      // chunk c's operand row for this lane: wait for its group, read the
-      // row, refill the buffer with chunk c + NLB
+      // chunk c's operand row for this lane: wait until groups 0..c landed
+      // (NCH - 1 - c newer groups may still be in flight)
       auto take_load = [&](int c, uint4(&pre)[4]) __attribute__((always_inline)) {
-        if (NLB == 2 && c + 1 < NCH) asm volatile("cp.async.wait_group 1;" ::: "memory");
-        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        switch (NCH - 1 - c) {
+          case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+          case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+          case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+          default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        }
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           pre[u] = lds128(smem_u32(lbuf(c) + lane * 4 + (u ^ ((lane >> 1) & 3))));
-        __syncwarp();
-        if (c + NLB < NCH) issue_load(c + NLB);
       };
       if (lsrc && p.ld_buf && !(p.dbg & 2)) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");   // nothing left from the last tile
         __syncwarp();                  // the previous tile's reads of the buffers are done
-        issue_load(0);
-        if (NLB == 2 && NCH > 1) issue_load(1);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) issue_load(c);
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -924,7 +940,8 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         } else if (fast_bwd && n + 32 <= p.N) {
           uint4 pre[4];
           take_load(c, pre);
-          epilogue_chunk_gelu_bwd(cur, pre, row_ok);
+          if (mul_aux) epilogue_chunk_gelu_bwd<true>(cur, pre, row_ok);
+          else epilogue_chunk_gelu_bwd<false>(cur, pre, row_ok);
           store_rows_staged(cur, stg, lane, orow0 + n, p.N, wmask, 32);
         } else if (fast_res && n + 32 <= p.N) {
           uint4 pre[4];
@@ -1189,7 +1206,8 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   SCMOE_CHECK_ARG(aligned16(a) && aligned16(wt) && aligned16(out) && aligned16(bias) &&
                       aligned16(residual) && aligned16(aux_in) && aligned16(aux_out),
                   "GEMM operands must be 16-byte aligned");
-  SCMOE_CHECK_ARG(epi != EPI_GELU_BWD || aux_in, "GELU backward needs the pre-activation");
+  SCMOE_CHECK_ARG((epi != EPI_GELU_BWD && epi != EPI_MUL_AUX) || aux_in,
+                  "GELU backward needs the pre-activation / the saved gelu'");
   Params p = {};
   p.num_groups = num_groups;
   p.n_wgroups = n_wgroups;
@@ -1206,7 +1224,8 @@ int grouped_gemm_bf16(const void* a, const void* wt, int b_mn, const float* bias
   p.aux_out = (__nv_bfloat16*)aux_out;
   p.out = (__nv_bfloat16*)out;
   p.out_groups = (__nv_bfloat16* const*)out_groups;
-  p.ld_buf = (residual || (epi == EPI_GELU_BWD && aux_in)) && !(g_gemm_flags & 1) ? 1 : 0;
+  p.ld_buf = (residual || ((epi == EPI_GELU_BWD || epi == EPI_MUL_AUX) && aux_in)) &&
+                     !(g_gemm_flags & 1) ? 2 : 0;
   p.dbg = g_gemm_flags;
   if (cs) {
     SCMOE_CHECK_ARG(num_groups == 1 && epi == EPI_BIAS && cs->k >= 1 && cs->k <= 2 && cs->y &&

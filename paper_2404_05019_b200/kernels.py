@@ -381,6 +381,22 @@ def gelu_fwd(z: torch.Tensor, group_rows: Optional[torch.Tensor] = None, rows_cl
     return out if z.dim() == 3 else out.view(C, H)
 
 
+def gelu_fwd_grad(z: torch.Tensor, group_rows: Optional[torch.Tensor] = None,
+                  rows_clip: int = 0, stream=None):
+    """(gelu(z), gelu'(z)) on each group's valid rows, zero-padded tails."""
+    ensure_device(z)
+    z3 = z if z.dim() == 3 else z.unsqueeze(0)
+    G, C, H = z3.shape
+    if z.dtype != torch.bfloat16:
+        raise ValueError("gelu_fwd_grad is bf16")
+    h, dg = torch.empty_like(z3), torch.empty_like(z3)
+    check(lib().scmoe_gelu_fwd_grad(ptr(_c(z3, "z")), ptr(h), ptr(dg), G, C, H, ptr(group_rows),
+                                    rows_clip, stream_ptr(stream)))
+    if z.dim() == 3:
+        return h, dg
+    return h.view(C, H), dg.view(C, H)
+
+
 def gelu_bwd(dh: torch.Tensor, z: torch.Tensor, group_rows: Optional[torch.Tensor] = None,
              rows_clip: int = 0, bias_grad: bool = True, stream=None):
     """(dz = dh * gelu'(z) with zero-padded tails, per-group bias gradient

@@ -95,9 +95,11 @@ class LinearFn(torch.autograd.Function):
         return dx, dwt, res_grad, None
 
 
-# training FFN GELU: separate full-occupancy elementwise passes (True) or the
-# GEMM epilogues (False); at d = 384 the K = 384 tiles make the GEMMs'
-# elementwise epilogues the bottleneck (csrc/gelu.cu)
+# training FFN GELU: a separate full-occupancy forward pass that writes
+# gelu(z) and gelu'(z) (True; the backward's data-gradient GEMM multiplies by
+# gelu'(z) in its epilogue), or the GEMM epilogues evaluating erf (False); at
+# d = 384 the K = 384 tiles make erf in the GEMM epilogues the bottleneck
+# (csrc/gelu.cu)
 SPLIT_GELU = True
 
 
@@ -125,11 +127,14 @@ class FFNFn(torch.autograd.Function):
         G, C, d = x3.shape
         h = w13.shape[1]
         if SPLIT_GELU:
-            # plain bias GEMM -> z, then h = gelu(z) as a full-occupancy pass
-            # (zero-padded tails for the weight gradients)
+            # plain bias GEMM -> z, then h = gelu(z) and gelu'(z) in one
+            # full-occupancy pass (zero-padded tails for the weight
+            # gradients); the backward multiplies by the saved gelu'(z) in
+            # its data-gradient GEMM's epilogue
             z = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), epilogue=_lib.EPI_BIAS,
                                   group_rows=group_rows, rows_clip=rows_clip)
-            hid = K.gelu_fwd(z, group_rows, rows_clip)
+            hid, dgelu = K.gelu_fwd_grad(z, group_rows, rows_clip)
+            z = dgelu
         else:
             z = torch.empty(G, C, h, device=x.device, dtype=x.dtype)
             hid = K.grouped_gemm_ex(x3, w13, _NK, h, bias=b1.view(-1, h), aux_out=z,
@@ -138,7 +143,7 @@ class FFNFn(torch.autograd.Function):
         res3 = None if residual is None else residual.view(G, C, d)
         y = K.grouped_gemm_ex(hid, w23, _NK, d, bias=b2.view(-1, d), residual=res3,
                               group_rows=group_rows, rows_clip=rows_clip)
-        ctx.save_for_backward(x3, z, hid, w13, w23, group_rows)
+        ctx.save_for_backward(x3, z, hid, w13, w23, group_rows)   # z: gelu'(z) when split
         ctx.meta = (two_d, rows_clip, residual is not None, b1.shape, b2.shape, w1t.shape,
                     w2t.shape)
         # y = FFN(x) + x (the Block-MLP): the data gradient adds dy in its
@@ -160,10 +165,11 @@ class FFNFn(torch.autograd.Function):
         if grouped:
             K.zero_tails(dy3, group_rows, rows_clip)
         if SPLIT_GELU:
-            # plain data-gradient GEMM -> dh, then dz = dh * gelu'(z) with the
-            # bias gradient (column sums of dz) in the same pass
-            dh = K.grouped_gemm_ex(dy3, w23, _KN, h, group_rows=group_rows, rows_clip=rows_clip)
-            dz, db1_g = K.gelu_bwd(dh, z, group_rows, rows_clip)
+            # z holds gelu'(z) here (saved by the forward): dz = (dy W2) *
+            # gelu'(z) in the data-gradient GEMM's epilogue, zero tails
+            dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_MUL_AUX,
+                                   group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+            db1_g = None
         else:
             dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                    group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)

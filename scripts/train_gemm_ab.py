@@ -52,6 +52,9 @@ shapes = [  # name, K, N, layout, bias, residual
     ("ffn1_fwd", 384, 1536, L.W_NK, True, False),
     ("qkv_fwd", 384, 1152, L.W_NK, False, False),
     ("ffn2_dh", 384, 1536, L.W_KN, False, False),
+    ("ffn2_dz_mul", 384, 1536, L.W_KN, False, "mul"),
+    ("ffn2_dz_gbwd", 384, 1536, L.W_KN, False, "gbwd"),
+    ("ffn1_fwd_gelu_aux", 384, 1536, L.W_NK, True, "gelu_aux"),
 ]
 variants = [(0, 0, 0), (8, 0, 0), (16, 0, 0), (8, 128, 0)]
 if len(sys.argv) > 1:     # epi:bn:flags
@@ -66,13 +69,20 @@ for name, Kd, N, lay, bias, res in shapes:
         w = w.t().contiguous()
     b = torch.zeros(N, device="cuda") if bias else None
     r = torch.randn(M, N, device="cuda").bfloat16() if res else None
+    kw = dict(bias=b, residual=r)
+    if res == "mul":
+        kw = dict(aux_in=r, epilogue=L.EPI_MUL_AUX)
+    elif res == "gbwd":
+        kw = dict(aux_in=r, epilogue=L.EPI_GELU_BWD)
+    elif res == "gelu_aux":
+        kw = dict(bias=b, aux_out=r, epilogue=L.EPI_BIAS_GELU)
     row = []
     for e, bn, fl in variants:
         K.set_gemm_epilogue_warps(e)
         L.lib().scmoe_set_gemm_tile_n(bn)
         L.lib().scmoe_set_gemm_flags(fl)
         try:
-            t = timeit(lambda: K.grouped_gemm_ex(a, w, lay, N, bias=b, residual=r))
+            t = timeit(lambda: K.grouped_gemm_ex(a, w, lay, N, **kw))
         except Exception as ex:  # noqa: BLE001
             t = float("nan")
         row.append(t)
