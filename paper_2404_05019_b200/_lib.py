@@ -105,7 +105,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                           " or `make -C paper_2404_05019_b200/csrc`")
     so = ctypes.CDLL(path)
     for name, res, args in SIGNATURES:
-        fn = getattr(so, name)
+        # an A/B against an older build (SCMOE_LIB) may lack newer entries
+        fn = getattr(so, name, None) if os.environ.get("SCMOE_LIB") else getattr(so, name)
+        if fn is None:
+            continue
         fn.restype = res
         fn.argtypes = args
     return so

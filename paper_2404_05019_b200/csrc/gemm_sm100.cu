@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, tensor-map prefetch) overlapped the previous kernel's tail;
+  // no global memory is touched before the previous grid completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 3) {
     if (WGRAD) {
       // k-blocks feeding each weight group
@@ -783,6 +787,11 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
                           !p.aux_in && !p.c_k && !p.zero_tail && !(p.dbg & 4);
     int it = 0;
     for (int t = unit; t < total_tiles; t += n_units, ++it) {
+      // this CTA's last tile: let the next kernel start launching (it waits in
+      // griddepcontrol.wait for this grid's completion; triggering only here
+      // keeps every CTA of this grid resident before any dependent CTA can be)
+      if (t + n_units >= total_tiles && ew == 0 && lane == 0)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
       const int acc = it % ACC_STAGES;
       const uint32_t acc_phase = (it / ACC_STAGES) & 1;
@@ -1108,6 +1117,9 @@ int make_map(CUtensorMap* map, const void* base, int inner, int outer, int group
   return SCMOE_OK;
 }
 
+// programmatic dependent launch of the GEMMs (1 = on; scmoe_set_gemm_flags bit 3 turns it off)
+static int g_gemm_pdl = 1;
+
 template <bool TWO_SM, bool B_MN, bool WGRAD, int BN, int E = EPI_WARPS>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
            cudaStream_t st) {
@@ -1124,13 +1136,17 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int gr
   cfg.blockDim = dim3(Threads<E>::value);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = TWO_SM ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch (the kernel waits in griddepcontrol.wait
+  // before its first global access)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = g_gemm_pdl;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   SCMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, p));
   return SCMOE_OK;
 }
@@ -1370,6 +1386,7 @@ int make_map_2d(CUtensorMap* map, const void* base, int inner, int outer,
 
 extern "C" int scmoe_set_gemm_flags(int flags) {
   scmoe::g_gemm_flags = flags;
+  scmoe::sm100::g_gemm_pdl = (flags & 8) ? 0 : 1;
   return SCMOE_OK;
 }
 
