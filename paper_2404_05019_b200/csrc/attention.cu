@@ -80,6 +80,22 @@ __device__ __forceinline__ void load_tile(Tile<HD> t, const bf16* g, long long l
     cp_async16(t.at(r, c), g + (row0 + r) * ld + col0 + c);
   }
 }
+// the same with the window length and the block size (2 SF threads) known at
+// compile time: a fixed, fully unrolled trip count
+template <int HD, int SF>
+__device__ __forceinline__ void load_tile_c(Tile<HD> t, const bf16* g, long long ld,
+                                            long long row0, int col0) {
+  constexpr int CH = HD / 8, NT = 2 * SF, N = SF * CH;
+  const bf16* base = g + row0 * ld + col0;
+#pragma unroll
+  for (int k = 0; k < (N + NT - 1) / NT; ++k) {
+    const int i = threadIdx.x + k * NT;
+    if (N % NT == 0 || i < N) {
+      const int r = i / CH, c = (i % CH) * 8;
+      cp_async16(t.at(r, c), base + r * ld + c);
+    }
+  }
+}
 
 // A fragment (16 x 16 at rows r0, cols c0) of a row-major shared tile
 template <int HD>
@@ -289,9 +305,9 @@ win_attn_fwd_persistent(const bf16* __restrict__ qkv, int H, int n_items, float 
     const int w = item / H, h = item - w * H;
     const long long row0 = (long long)w * SF;
     bf16* p = base + b * 3 * TILE;
-    load_tile<HD>(Tile<HD>{p}, qkv, ld, row0, h * HD, SF);
-    load_tile<HD>(Tile<HD>{p + TILE}, qkv, ld, row0, d + h * HD, SF);
-    load_tile<HD>(Tile<HD>{p + 2 * TILE}, qkv, ld, row0, 2 * d + h * HD, SF);
+    load_tile_c<HD, SF>(Tile<HD>{p}, qkv, ld, row0, h * HD);
+    load_tile_c<HD, SF>(Tile<HD>{p + TILE}, qkv, ld, row0, d + h * HD);
+    load_tile_c<HD, SF>(Tile<HD>{p + 2 * TILE}, qkv, ld, row0, 2 * d + h * HD);
   };
   int item = blockIdx.x;
   if (item < n_items) issue(item, 0);
@@ -330,30 +346,40 @@ win_attn_bwd_kernel(const bf16* __restrict__ qkv, const bf16* __restrict__ o,
   bf16* dst = Os.p + S * P;                   // dS^T [key][query]
   float* Dq = (float*)(dst + S * DSP);        // D = rowsum(dO o O) per query
   float* Lq = Dq + S;                         // base-2 lse per query
-  load_tile<HD>(Gs, dout, d, row0, h * HD, S);
-  load_tile<HD>(Os, o, d, row0, h * HD, S);
+  auto load = [&](Tile<HD> t, const bf16* g, long long ldg, int col0) {
+    if (SF) load_tile_c<HD, SF ? SF : 16>(t, g, ldg, row0, col0);
+    else load_tile<HD>(t, g, ldg, row0, col0, S);
+  };
+  load(Gs, dout, d, h * HD);
+  load(Os, o, d, h * HD);
   asm volatile("cp.async.commit_group;" ::: "memory");
-  load_tile<HD>(Qs, qkv, ld, row0, h * HD, S);
-  load_tile<HD>(Ks, qkv, ld, row0, d + h * HD, S);
-  load_tile<HD>(Vs, qkv, ld, row0, 2 * d + h * HD, S);
+  load(Qs, qkv, ld, h * HD);
+  load(Ks, qkv, ld, d + h * HD);
+  load(Vs, qkv, ld, 2 * d + h * HD);
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int i = threadIdx.x; i < S; i += blockDim.x) Lq[i] = lse[(row0 + i) * H + h];
   asm volatile("cp.async.wait_group 1;" ::: "memory");
   __syncthreads();                            // dO and O landed: D while Q / K / V load
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+  // D = rowsum(dO o O): two threads per row (blockDim = 2 S), HD / 2 columns
+  // each, partner sum by shuffle
+  {
+    const int i = threadIdx.x >> 1, half = threadIdx.x & 1;
     float acc = 0.f;
+    if (i < S) {
 #pragma unroll
-    for (int c = 0; c < HD; c += 8) {
-      Vec16<bf16> a, b;
-      a.raw = *reinterpret_cast<const uint4*>(Os.at(i, c));
-      b.raw = *reinterpret_cast<const uint4*>(Gs.at(i, c));
-      float fa[8], fb[8];
-      a.to_float(fa);
-      b.to_float(fb);
+      for (int c = half * (HD / 2); c < (half + 1) * (HD / 2); c += 8) {
+        Vec16<bf16> a, b;
+        a.raw = *reinterpret_cast<const uint4*>(Os.at(i, c));
+        b.raw = *reinterpret_cast<const uint4*>(Gs.at(i, c));
+        float fa[8], fb[8];
+        a.to_float(fa);
+        b.to_float(fb);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(fa[e], fb[e], acc);
+        for (int e = 0; e < 8; ++e) acc = fmaf(fa[e], fb[e], acc);
+      }
     }
-    Dq[i] = acc;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (i < S && half == 0) Dq[i] = acc;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -474,22 +500,38 @@ win_attn_bwd_kernel(const bf16* __restrict__ qkv, const bf16* __restrict__ o,
   // ---- phase B: warp owns queries [m0, m0 + 16): dQ = dS K * scale
   float dq[HD / 8][4];
   if (active) {
+    // two accumulator sets (even / odd key blocks): the chained MMAs of one
+    // set alternate with the other's instead of waiting on each other
+    float dq2[HD / 8][4];
 #pragma unroll
-    for (int n = 0; n < HD / 8; ++n) dq[n][0] = dq[n][1] = dq[n][2] = dq[n][3] = 0.f;
-#pragma unroll 3
-    for (int kb = 0; kb < nq; ++kb) {
+    for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dq[n][e] = dq2[n][e] = 0.f;
+    auto kblock = [&](int kb, float (&acc)[HD / 8][4]) __attribute__((always_inline)) {
       const int k0 = kb * 16;
-      if (causal && k0 > m0 + 15) break;       // keys after every query of mine
       uint32_t a[4];                            // dS (16 queries x 16 keys) from dS^T
       ldsm_x4_t(a, dst + (k0 + (lane & 7) + (lane >> 4) * 8) * DSP + m0 + ((lane >> 3) & 1) * 8);
 #pragma unroll
       for (int n = 0; n < HD / 8; n += 2) {
         uint32_t b[4];
         frag_b_cols<HD>(b, Ks, k0, n * 8, lane);
-        mma16816(dq[n], a, b[0], b[1]);
-        mma16816(dq[n + 1], a, b[2], b[3]);
+        mma16816(acc[n], a, b[0], b[1]);
+        mma16816(acc[n + 1], a, b[2], b[3]);
       }
+    };
+    // keys after every query of mine contribute nothing (causal)
+    const int kb_end = causal ? min(nq, (m0 + 15) / 16 + 1) : nq;
+    int kb = 0;
+#pragma unroll 2
+    for (; kb + 1 < kb_end; kb += 2) {
+      kblock(kb, dq);
+      kblock(kb + 1, dq2);
     }
+    if (kb < kb_end) kblock(kb, dq);
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dq[n][e] += dq2[n][e];
   }
   __syncthreads();                             // every read of Q / K / V / dS^T is done
   if (!active) return;
