@@ -49,6 +49,9 @@ template <int E> struct Threads { static constexpr int value = 128 + E * 32; };
 constexpr int THREADS = Threads<EPI_WARPS>::value;
 constexpr int TMEM_COLS = 512;                   // 512 / BN accumulator stages
 constexpr int MAX_GROUPS = 1024;
+// groups up to which the forward / dgrad schedule packs whole groups into
+// waves (see the virtual tile starts in gemm_kernel)
+constexpr int MAX_PACK = 64;
 constexpr int MN_BOX = 64;                       // MN-major TMA box: 64 (mn) x 64 (k)
 constexpr int MN_BOX_BYTES = MN_BOX * BK * 2;    // 8 KB
 
@@ -69,7 +72,8 @@ struct Cfg {
   static constexpr int RING_BYTES = E_ == 8 ? 192 * 1024 : 176 * 1024;
   static constexpr int STAGES = (RING_BYTES / STAGE_BYTES) < 8 ? (RING_BYTES / STAGE_BYTES) : 8;
   // + per-epilogue-warp bias slice (E warps x 128 fp32), staged once per tile
-  static constexpr size_t MISC = 256 + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t MISC =
+      256 + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 16 + ((MAX_PACK + 1) * 4 + 15) / 16 * 16;
   // + per-epilogue-warp 2 KB store-transpose staging
   static constexpr size_t SMEM =
       1024 + (size_t)STAGES * STAGE_BYTES + MISC + E_ * 128 * 4 + E_ * 2048;
@@ -270,12 +274,33 @@ __device__ __forceinline__ int group_rows_of(const Params& p, int g) {
 // in wgrad mode, the split's k-block range.
 struct Tile {
   int g, m0, n0, s, kb_lo, kb_hi;
+  bool idle;   // a packing gap of the virtual schedule: no work
 };
 
 template <int TILE_M, int BN, bool WGRAD>
 __device__ __forceinline__ Tile decode_tile(const Params& p, int t, int n_tiles_n,
-                                            const int* prefix) {
+                                            const int* prefix, const int* vstart) {
   Tile c;
+  c.idle = false;
+  if (!WGRAD && p.num_groups <= MAX_PACK) {
+    // packed schedule: group g owns virtual slots [vstart[g], vstart[g] +
+    // tiles(g)); slots past a group's tiles are gaps
+    int lo = 0, hi = p.num_groups - 1;         // largest g with vstart[g] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (vstart[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const int local = t - vstart[lo];
+    c.g = lo;
+    c.idle = local >= (prefix[lo + 1] - prefix[lo]) * n_tiles_n;
+    c.m0 = (local / n_tiles_n) * TILE_M;
+    c.n0 = (local % n_tiles_n) * BN;
+    c.s = 0;
+    c.kb_lo = 0;
+    c.kb_hi = c.idle ? 0 : (p.K + BK - 1) / BK;
+    return c;
+  }
   const int nt = t % n_tiles_n;
   int r = t / n_tiles_n;
   c.n0 = nt * BN;
@@ -614,6 +639,7 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
   uint64_t* tempty_bar = bars + 2 * C::STAGES + ACC_STAGES;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 2 * ACC_STAGES);
   int* s_prefix = reinterpret_cast<int*>(smem_b + C::STAGES * C::B_BYTES + 256);
+  int* s_vstart = s_prefix + ((MAX_GROUPS + 1) * 4 + 15) / 16 * 4;
   float* s_bias = reinterpret_cast<float*>(smem_b + C::STAGES * C::B_BYTES + C::MISC);
   uint4* s_stage = reinterpret_cast<uint4*>(s_bias + E * 128);   // 2 KB per epilogue warp
   const int ring = C::STAGES - p.ld_buf;                                   // mainloop stages
@@ -687,6 +713,33 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         if (g < p.num_groups) s_prefix[g + 1] = carry + v;
         carry += __shfl_sync(0xffffffffu, v, 31);
       }
+      // Group-aligned waves.  The persistent units take virtual slots t =
+      // unit, unit + n_units, ..., so slots [w * n_units, (w+1) * n_units)
+      // run together ("wave" w).  A group that fits in one wave but would
+      // straddle two is moved to the next wave's start while the gaps fit in
+      // the slack of the minimal wave count: its weights are then streamed
+      // by one wave instead of two (the K = 8192 routed GEMM2 re-read each
+      // expert's W2 in both waves it straddled: 1.42x DRAM traffic).  The
+      // tile -> unit assignment never changes a tile's result.
+      __syncwarp();
+      if (p.num_groups <= MAX_PACK && lane == 0) {
+        const int ntn = (p.N + BN - 1) / BN;
+        const int units = TWO_SM ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+        const int total = s_prefix[p.num_groups] * ntn;
+        int slack = (total + units - 1) / units * units - total;
+        int v = 0;
+        for (int g = 0; g < p.num_groups; ++g) {
+          const int c = (s_prefix[g + 1] - s_prefix[g]) * ntn;
+          const int f = v % units, gap = units - f;
+          if (c > 0 && c <= units && f > 0 && c > gap && gap <= slack) {
+            slack -= gap;
+            v += gap;
+          }
+          s_vstart[g] = v;
+          v += c;
+        }
+        s_vstart[p.num_groups] = v;
+      }
     }
   }
   tc_fence_before();
@@ -698,14 +751,15 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
   const int n_tiles_n = (p.N + BN - 1) / BN;
   const int total_tiles =
       WGRAD ? p.splits * p.n_wgroups * ((p.m_out + C::TILE_M - 1) / C::TILE_M) * n_tiles_n
-            : s_prefix[p.num_groups] * n_tiles_n;
+            : (p.num_groups <= MAX_PACK ? s_vstart[p.num_groups] : s_prefix[p.num_groups] * n_tiles_n);
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs load their own halves) =====
     int stage = 0;
     uint32_t phase = 0;
     for (int t = unit; t < total_tiles; t += n_units) {
-      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
+      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix, s_vstart);
+      if (tc.idle) continue;
       const int am = tc.m0 + (int)rank * C::CTA_M;
       const int bn = tc.n0 + (int)rank * C::B_ROWS;
       for_each_kblock<WGRAD>(p, tc, [&](int g, int kb) {
@@ -731,8 +785,9 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = unit; t < total_tiles; t += n_units, ++it) {
-        const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
+      for (int t = unit; t < total_tiles; t += n_units) {
+        const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix, s_vstart);
+        if (tc.idle) continue;
         const int acc = it % ACC_STAGES;
         const uint32_t acc_phase = (it / ACC_STAGES) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -764,6 +819,7 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         });
         if (lane == 0) tc_commit<TWO_SM>(&tfull_bar[acc]);
         __syncwarp();
+        ++it;
       }
     }
   } else if (warp >= 4) {
@@ -786,15 +842,17 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
     const bool fast_res = !WGRAD && p.epi == EPI_BIAS && p.residual && p.ld_buf && !p.aux_out &&
                           !p.aux_in && !p.c_k && !p.zero_tail && !(p.dbg & 4);
     int it = 0;
-    for (int t = unit; t < total_tiles; t += n_units, ++it) {
+    for (int t = unit; t < total_tiles; t += n_units) {
       // this CTA's last tile: let the next kernel start launching (it waits in
       // griddepcontrol.wait for this grid's completion; triggering only here
       // keeps every CTA of this grid resident before any dependent CTA can be)
       if (t + n_units >= total_tiles && ew == 0 && lane == 0)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix);
+      const Tile tc = decode_tile<C::TILE_M, BN, WGRAD>(p, t, n_tiles_n, s_prefix, s_vstart);
+      if (tc.idle) continue;
       const int acc = it % ACC_STAGES;
       const uint32_t acc_phase = (it / ACC_STAGES) & 1;
+      ++it;
       const int row_w0 = tc.m0 + (int)rank * C::CTA_M + quad * 32;   // this warp's first row
       const int row = row_w0 + lane;
       bool row_ok, pad_row = false;
