@@ -38,8 +38,11 @@ constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 constexpr size_t CTR_BYTES = 256;
 
 // workspace = [counters | per-tile status (or tile counts) | per-tile prob partials]
+// (per-tile rows for the FMA kernel's 64-token tiles; per-CTA rows for the
+// tensor-core kernel, at most one per 16 tokens and at most 1024 CTAs)
 __host__ __device__ inline size_t gate_ws_bytes(int n_tok, int n_exp) {
-  const size_t tiles = (size_t)((n_tok + 63) / 64);
+  const size_t t64 = (size_t)((n_tok + 63) / 64), t16 = (size_t)((n_tok + 15) / 16);
+  const size_t tiles = t64 > (t16 < 1024 ? t16 : 1024) ? t64 : (t16 < 1024 ? t16 : 1024);
   return (CTR_BYTES + 2 * tiles * (size_t)n_exp * 4 + 15) & ~(size_t)15;
 }
 
@@ -105,16 +108,20 @@ struct RouteState {            // survives between publish and finish (shared me
   int32_t lr[TOK_][SCMOE_MAX_K];   // rank of the selection inside its tile
 };
 
-// LOCAL = true (tensor-core gate): no look-back at all — the in-tile rank of
-// every selection goes to `slots` and the tile's per-expert count to
-// status[tile][e]; the kernel's tail adds the prefix over earlier tiles.
+// LOCAL = true (tensor-core gate): a sub-tile of `nv` tokens from t0 inside
+// the CTA's contiguous token range, no look-back at all — every selection's
+// rank relative to the CTA's first token (the CTA's running per-expert count
+// `cta_run` + the rank inside the sub-tile) goes to lcache[(lc_off + i) * k
+// + j] (or to `slots` when lcache is null); the softmax partials accumulate
+// into cta_ps; the kernel's tail adds the prefix over earlier CTAs.
 template <int NMAX, int TOK_, int THREADS_, int BASE = 0, int BAR = 1, bool LOCAL = false>
 __device__ __forceinline__ void route_publish(
     const float (*s_logit)[NMAX + 1], RouteState<NMAX, TOK_>& rs, int tile,
     const int32_t* __restrict__ exclude, int n_tok, int N, int k, float* __restrict__ logits,
     int32_t* __restrict__ indices, float* __restrict__ weights, int32_t* __restrict__ counts,
     uint32_t* __restrict__ status, float* __restrict__ psum, int32_t* __restrict__ slots = nullptr,
-    uint32_t* lcache = nullptr) {
+    uint32_t* lcache = nullptr, long long t0 = 0, int nv = 0, uint32_t* cta_run = nullptr,
+    float* cta_ps = nullptr, int lc_off = 0) {
   constexpr int RW = TOK_ / 32;
   __shared__ int s_wcnt[RW][NMAX];
   __shared__ float s_wprob[RW][NMAX];
@@ -122,8 +129,8 @@ __device__ __forceinline__ void route_publish(
   const int warp = tid >> 5, lane = tid & 31;
   int sel[SCMOE_MAX_K];
   int rank[SCMOE_MAX_K];
-  const int t = tile * TOK_ + tid;
-  const bool valid = (tid < TOK_) && (t < n_tok);
+  const long long t = LOCAL ? t0 + tid : (long long)tile * TOK_ + tid;
+  const bool valid = (tid < TOK_) && (LOCAL ? tid < nv : t < n_tok);
   // SPLIT (tensor-core gate, <= 16 experts, >= 2 threads per token): a
   // second thread per token (tid - TOK_) writes the logits and computes the
   // full-softmax probability sums while the first runs top-k, ballots and
@@ -132,8 +139,8 @@ __device__ __forceinline__ void route_publish(
   constexpr bool SPLIT = LOCAL && NMAX <= 16 && THREADS_ >= 2 * TOK_;
   if (SPLIT && tid >= TOK_ && tid < 2 * TOK_) {
     const int tok = tid - TOK_;
-    const int tb = tile * TOK_ + tok;
-    const bool vb = tb < n_tok;
+    const long long tb = t0 + tok;
+    const bool vb = tok < nv;
     float h[NMAX];
 #pragma unroll
     for (int e = 0; e < NMAX; ++e) h[e] = (e < N) ? s_logit[tok][e] : 0.f;
@@ -306,7 +313,7 @@ __device__ __forceinline__ void route_publish(
   // aggregate at once so later tiles can make progress
   if (tid < N) {
     const int e = tid;
-    uint32_t run = 0;
+    uint32_t run = LOCAL ? cta_run[e] : 0u;
     float psum_tile = 0.f;
 #pragma unroll
     for (int w = 0; w < RW; ++w) {
@@ -315,10 +322,11 @@ __device__ __forceinline__ void route_publish(
       run += (uint32_t)c;
       psum_tile += s_wprob[w][e];
     }
-    psum[(size_t)tile * N + e] = psum_tile;
     if (LOCAL) {
-      status[(size_t)tile * N + e] = run;
+      cta_run[e] = run;
+      cta_ps[e] += psum_tile;
     } else {
+      psum[(size_t)tile * N + e] = psum_tile;
       rs.agg[e] = run;
       st_volatile_u32(status + (size_t)tile * N + e, (tile == 0 ? FLAG_INC : FLAG_AGG) | run);
       if (run) atomicAdd(&counts[e], (int)run);
@@ -335,8 +343,8 @@ __device__ __forceinline__ void route_publish(
       if (j < k) {
         const int lr = s_wcnt[warp][sel[j]] + rank[j];
         if (LOCAL) {
-          slots[(long long)t * k + j] = lr;
-          if (lcache && j < 2) lcache[tid * 2 + j] = ((uint32_t)sel[j] << 16) | (uint32_t)lr;
+          if (lcache) lcache[(lc_off + tid) * k + j] = ((uint32_t)sel[j] << 16) | (uint32_t)lr;
+          else slots[t * k + j] = lr;
         } else {
           rs.sel[tid][j] = (int8_t)sel[j];
           rs.lr[tid][j] = lr;
@@ -582,23 +590,33 @@ __global__ void __launch_bounds__(THREADS) gate_topk_kernel(
 // logits keep fp32-level accuracy while the FMA pipe no longer bounds the pass
 // over x.
 //
-// Persistent and warp-specialised, one CTA per SM, tiles of TOK tokens
-// assigned round-robin (no cross-tile dependency while streaming; the tail adds the
-// capacity-slot prefix over tiles afterwards).
-//   producer warp  — per stage, KC/64 TMA boxes of TOK rows x 64 columns
-//                    (cp.async.bulk.tensor.2d, 128B swizzle, OOB rows/columns
-//                    zero-filled) plus the matching slice of the split-weight
-//                    blob (gate_split_weights_kernel; one 1-D bulk copy),
-//                    completion on the stage's "full" mbarrier.  Per-row 1-D copies of x were measured
-//                    issue-bound (~1.8 TB/s at 512 B per copy); boxes are not;
+// Persistent and warp-specialised, one CTA per SM.  CTA c owns a contiguous,
+// balanced range of 16-token row tiles (ceil(T/16) split over the grid to
+// within one row tile; whole 64-token tiles left 40 of 148 SMs idle for the
+// second half of the stream at configs[2]), walked in sub-tiles of <= 4 row
+// tiles.  No cross-CTA dependency while streaming; the tail adds the
+// capacity-slot prefix over the earlier CTAs.
+//   producer warp  — per stage and sub-tile, (KC/64) x (row tiles) TMA boxes of
+//                    16 rows x 64 columns (cp.async.bulk.tensor.2d, 128B
+//                    swizzle, OOB rows/columns zero-filled; a 2 KB box is the
+//                    same swizzle image as a slice of a 64-row box), plus the
+//                    matching slice of the split-weight blob
+//                    (gate_split_weights_kernel; one 1-D bulk copy), completion
+//                    on the stage's "full" mbarrier.  Per-row 1-D copies of x
+//                    were measured issue-bound (~1.8 TB/s at 512 B per copy);
+//                    boxes are not.  (A shared-memory-resident blob with one
+//                    stage fewer was measured slower: the stream is bound by
+//                    bytes in flight, not by the blob's L2 reads);
 //   8 MMA warps    — warp w takes m16 tile w%4 and half w/4 of the stage's k16
 //                    steps: ldmatrix.x4 A fragments, B fragments as 8-byte
 //                    shared loads, one accumulator chain per weight part; the two
 //                    halves' partial logits are summed in a fixed order into a
 //                    double-buffered logits tile;
-//   4 routing warps — route_publish(LOCAL) per tile (top-k, weights, in-tile
-//                    ranks, per-expert tile counts, softmax partials), off the
-//                    MMA warps' critical path.
+//   4 routing warps — route_publish(LOCAL) per sub-tile (top-k, weights,
+//                    CTA-local ranks, CTA per-expert counts, softmax partials),
+//                    off the MMA warps' critical path; after the last sub-tile
+//                    one (N-word) table row per CTA, a grid-wide count of
+//                    published rows, and the prefix over earlier CTAs' rows.
 constexpr int GT_KC = 256;                       // columns per stage (4 TMA boxes)
 constexpr int GT_BOXB = TOK * 128;               // one 64-col x TOK-row box, 128B swizzle
 constexpr int GT_XB = (GT_KC / 64) * GT_BOXB;    // x part of a stage
@@ -713,8 +731,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
     const int32_t* __restrict__ exclude, int n_tok, int d, int N, int k, int quota,
     float* __restrict__ logits, int32_t* __restrict__ indices, float* __restrict__ weights,
     int32_t* __restrict__ slots, uint8_t* __restrict__ dropped, int32_t* __restrict__ counts,
-    float* __restrict__ prob_sum, uint32_t* __restrict__ ctrs, uint32_t* __restrict__ status,
-    float* __restrict__ psum, int num_tiles) {
+    float* __restrict__ prob_sum, uint32_t* __restrict__ ctrs, uint32_t* __restrict__ cta_cnt,
+    float* __restrict__ cta_psum, int n16) {
   using C = GateTC<NT>;
   constexpr int NMAX = NT * 8;
   constexpr int S = C::STAGES;
@@ -723,9 +741,15 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
   __shared__ float s_logit[2][TOK][NMAX + 1];     // MMA warps -> routing warps
   __shared__ float s_part[2][TOK][NMAX + 1];
   __shared__ __align__(8) uint64_t full_bar[S], empty_bar[S], lfull_bar[2], lempty_bar[2];
-  __shared__ int s_stage_tile[S], s_logit_tile[2];
+  __shared__ int s_stage_row[S], s_stage_m16[S], s_logit_row[2], s_logit_nv[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkc = (d + GT_KC - 1) / GT_KC;
+  // this CTA's contiguous range of 16-token row tiles (balanced to within one
+  // tile: whole 64-token tiles left 40 of 148 SMs idle for the second half of
+  // the stream at configs[2])
+  const int m16_lo = (int)((long long)blockIdx.x * n16 / gridDim.x);
+  const int m16_hi = (int)((long long)(blockIdx.x + 1) * n16 / gridDim.x);
+  const int cta_t0 = m16_lo * 16;
   if (tid == 0) {
     gate_trace(0);
     for (int i = 0; i < S; ++i) {
@@ -742,117 +766,110 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
 
   if (warp > GT_PRODUCER) {
     // ---------------- routing warps ----------------
-    // per tile: top-k, weights, in-tile ranks and per-expert tile counts (no
-    // cross-tile dependency); after the CTA's last tile, a grid-wide wait for
-    // every tile's counts (safe: the grid is persistent and resident, and no
-    // CTA waits on the one waiting), then the tile prefixes turn this CTA's
-    // in-tile ranks into capacity slots — no second launch.
+    // per sub-tile: top-k, weights, ranks relative to the CTA's first token
+    // (CTA running counts, no cross-CTA dependency); after the CTA's last
+    // sub-tile it publishes its per-expert totals, waits for every CTA's
+    // (safe: the grid is persistent and resident, and no CTA waits on the
+    // one waiting), and adds the prefix over the earlier CTAs — no second
+    // launch, one (N-word) table row per CTA
     __shared__ RouteState<NMAX, TOK> rs;
     constexpr int RT = GT_ROUTERS * 32;
-    constexpr int LCACHE_TILES = 4;        // (expert, in-tile rank) of this CTA's first tiles
-    __shared__ uint32_t s_lcache[LCACHE_TILES][TOK * 2];
+    constexpr int LCACHE = 2048;           // (expert, CTA-local rank) words
+    __shared__ uint32_t s_lcache[LCACHE];
+    __shared__ uint32_t s_run[NMAX];
+    __shared__ float s_ps[NMAX];
     const int rtid = tid - GT_ROUTE_BASE;
+    const int cta_tok = min(m16_hi * 16, n_tok) - cta_t0;
+    const bool cached = (long long)cta_tok * k <= LCACHE;
+    if (rtid < NMAX) {
+      s_run[rtid] = 0;
+      s_ps[rtid] = 0.f;
+    }
+    consumer_sync<RT, 2>();
     for (uint32_t n = 0;; ++n) {
       const int b = n & 1;
       mbar_wait(&lfull_bar[b], (n >> 1) & 1);
-      const int tile = s_logit_tile[b];
-      if (tile < 0) break;
+      const int row0 = s_logit_row[b];
+      if (row0 < 0) break;
+      const int nv = s_logit_nv[b];
       if (rtid == 0) gate_trace(5);
       route_publish<NMAX, TOK, RT, GT_ROUTE_BASE, 2, true>(
-          s_logit[b], rs, tile, exclude, n_tok, N, k, logits, indices, weights, counts, status,
-          psum, slots, (n < LCACHE_TILES && k <= 2) ? s_lcache[n] : nullptr);
+          s_logit[b], rs, 0, exclude, n_tok, N, k, logits, indices, weights, counts, nullptr,
+          nullptr, slots, cached ? s_lcache : nullptr, row0, nv, s_run, s_ps, row0 - cta_t0);
       __syncwarp();
       if (rtid == 0) gate_trace(6);
       if (lane == 0) mbar_arrive(&lempty_bar[b]);   // publish read s_logit[b] before its barrier
-      // every router thread's writes -> CTA barrier -> one release add (cumulative):
-      // no per-thread fence (a __threadfence is a MEMBAR.SC.GPU per thread)
       consumer_sync<RT, 2>();
-      if (rtid == 0)
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctrs + 2) : "memory");
     }
+    // this CTA's totals -> its table row; every router thread's writes ->
+    // CTA barrier -> one release add (cumulative): no per-thread fence
+    if (rtid < N) {
+      cta_cnt[(size_t)blockIdx.x * N + rtid] = s_run[rtid];
+      cta_psum[(size_t)blockIdx.x * N + rtid] = s_ps[rtid];
+    }
+    consumer_sync<RT, 2>();
     if (rtid == 0) {
       gate_trace(2);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctrs + 2) : "memory");
       const long long t0 = clock64();
-      while (ld_acquire_gpu(ctrs + 2) < (uint32_t)num_tiles) {
-        __nanosleep(200);
+      while (ld_acquire_gpu(ctrs + 2) < gridDim.x) {
+        __nanosleep(64);
         if (clock64() - t0 > (40LL << 30)) __trap();   // ~20 s: never hang the GPU
       }
       gate_trace(3);
     }
     consumer_sync<RT, 2>();
-    // the stage ring is idle now: load the whole (tiles, N) count table (and
-    // on CTA 0 the probability partials) into it with every router thread
-    // (many loads in flight), transposed to [N][tiles + 1]
-    const int ld = num_tiles + 1;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(gsm);
-    float* ptab = reinterpret_cast<float*>(gsm) + (size_t)N * ld;
-    const int ent = num_tiles * N;
-    const bool first = blockIdx.x == 0;
-#pragma unroll 8
-    for (int m = rtid; m < ent; m += RT) {
-      tab[(m % N) * ld + m / N] = __ldcg(status + m);
-      if (first) ptab[(m % N) * ld + m / N] = __ldcg(psum + m);
-    }
-    consumer_sync<RT, 2>();
-    // this CTA's tiles only need their own prefixes: a parallel reduction over
-    // the shared-memory table per tile (thread (e, p) sums tiles p, p+P, ...)
+    // exclusive prefix over the earlier CTAs: thread (e, p) sums CTAs p, p+P,
+    // ... (independent loads in flight), the P partials added in order; the
+    // last CTA also forms the totals and the softmax mean (fixed order:
+    // deterministic)
     constexpr int P = RT / NMAX;
     __shared__ uint32_t s_red[P][NMAX];
+    __shared__ float s_fred[P][NMAX];
     __shared__ uint32_t s_base[NMAX];
+    const bool last = blockIdx.x == gridDim.x - 1;
     const int e = rtid % NMAX, p = rtid / NMAX;
-    for (int tile = blockIdx.x, n = 0; tile < num_tiles; tile += gridDim.x, ++n) {
+    {
       uint32_t acc = 0;
-      if (e < N)
-        for (int t = p; t < tile; t += P) acc += tab[e * ld + t];
-      s_red[p][e] = acc;
-      consumer_sync<RT, 2>();
-      if (rtid < NMAX) {
-        uint32_t base = 0;
-#pragma unroll
-        for (int q = 0; q < P; ++q) base += s_red[q][rtid];
-        s_base[rtid] = base;
-      }
-      consumer_sync<RT, 2>();
-      const bool cached = n < LCACHE_TILES && k <= 2;
-      for (int i = rtid; i < TOK * k; i += RT) {
-        const long long t = (long long)tile * TOK + i / k;
-        if (t >= n_tok) break;
-        const long long o = t * k + i % k;
-        int slot;
-        if (cached) {
-          const uint32_t v = s_lcache[n][(i / k) * 2 + i % k];
-          slot = (int)s_base[v >> 16] + (int)(v & 0xffffu);
-        } else {
-          slot = (int)s_base[indices[o]] + slots[o];
-        }
-        slots[o] = slot;
-        dropped[o] = slot >= quota ? 1 : 0;
-      }
-      consumer_sync<RT, 2>();
-    }
-    if (first) {
-      // totals and the softmax mean: fixed summation order (deterministic)
-      __shared__ float s_ps[P][NMAX];
-      uint32_t c = 0;
       float ps = 0.f;
-      if (e < N)
-        for (int t = p; t < num_tiles; t += P) {
-          c += tab[e * ld + t];
-          ps += ptab[e * ld + t];
+      if (e < N) {
+        const int lim = last ? (int)gridDim.x : (int)blockIdx.x;
+#pragma unroll 4
+        for (int c2 = p; c2 < lim; c2 += P) {
+          if (c2 < (int)blockIdx.x) acc += __ldcg(cta_cnt + (size_t)c2 * N + e);
+          if (last) ps += __ldcg(cta_psum + (size_t)c2 * N + e);
         }
-      s_red[p][e] = c;
-      s_ps[p][e] = ps;
-      consumer_sync<RT, 2>();
-      if (rtid < N) {
-        uint32_t cs = 0;
-        float fs = 0.f;
-        for (int q = 0; q < P; ++q) {
-          cs += s_red[q][rtid];
-          fs += s_ps[q][rtid];
-        }
-        counts[rtid] = (int)cs;
+      }
+      s_red[p][e] = acc;
+      s_fred[p][e] = ps;
+    }
+    consumer_sync<RT, 2>();
+    if (rtid < NMAX) {
+      uint32_t base = 0;
+      float fs = 0.f;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        base += s_red[q][rtid];
+        fs += s_fred[q][rtid];
+      }
+      s_base[rtid] = base;
+      if (last && rtid < N) {
+        counts[rtid] = (int)(base + s_run[rtid]);
         prob_sum[rtid] = fs;
       }
+    }
+    consumer_sync<RT, 2>();
+    for (int i = rtid; i < cta_tok * k; i += RT) {
+      const long long o = (long long)cta_t0 * k + i;
+      int slot;
+      if (cached) {
+        const uint32_t v = s_lcache[i];
+        slot = (int)s_base[v >> 16] + (int)(v & 0xffffu);
+      } else {
+        slot = (int)s_base[indices[o]] + slots[o];
+      }
+      slots[o] = slot;
+      dropped[o] = slot >= quota ? 1 : 0;
     }
     if (rtid == 0) gate_trace(4);
     return;
@@ -860,17 +877,19 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
 
   if (warp == GT_PRODUCER) {
     // ---------------- producer warp ----------------
-    // static round-robin tiles (no cross-tile dependency in this kernel)
+    // sub-tiles of up to 4 row tiles (64 tokens) of this CTA's range; per
+    // stage 16-row x 64-column boxes (2 KB, 1024-aligned: the same 128B-swizzle
+    // image as one 64-row box)
     uint32_t it = 0;
-    for (int tile = blockIdx.x;; tile += gridDim.x) {
-      const bool live = tile < num_tiles;
-      const int row0 = tile * TOK;
+    for (int m = m16_lo;; m += 4) {
+      const bool live = m < m16_hi;
+      const int m16 = live ? min(4, m16_hi - m) : 0;
       for (int kc = 0; kc < (live ? nkc : 1); ++kc, ++it) {
         const int s = it % S;
         mbar_wait(&empty_bar[s], ((it / S) & 1) ^ 1);
         if (!live) {
           if (lane == 0) {
-            s_stage_tile[s] = -1;
+            s_stage_row[s] = -1;
             mbar_arrive(&full_bar[s]);
           }
           break;
@@ -880,16 +899,21 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
         const uint32_t blobb = (uint32_t)nbox * GT_GROUP_B * NT;
         uint8_t* st = gsm + (size_t)s * C::STAGEB;
         if (lane == 0) {
-          s_stage_tile[s] = tile;
-          mbar_expect_tx(&full_bar[s], (uint32_t)nbox * GT_BOXB + blobb);
+          s_stage_row[s] = m * 16;
+          s_stage_m16[s] = m16;
+          mbar_expect_tx(&full_bar[s], (uint32_t)(nbox * m16) * 2048u + blobb);
           bulk_g2s(st + GT_XB, blob + (size_t)(c0 / 64) * GT_GROUP_B * NT, blobb, &full_bar[s]);
-          for (int b = 0; b < nbox; ++b)
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-                "[%0], [%1, {%2, %3}], [%4];"
-                ::"r"(smem_u32(st + b * GT_BOXB)), "l"(&xmap), "r"(c0 + 64 * b), "r"(row0),
-                  "r"(smem_u32(&full_bar[s]))
-                : "memory");
+        }
+        __syncwarp();
+        // one box per lane: lane = b * 4 + r (b < nbox, r < m16)
+        if (lane < nbox * 4 && (lane & 3) < m16) {
+          const int bx = lane >> 2, r = lane & 3;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+              "[%0], [%1, {%2, %3}], [%4];"
+              ::"r"(smem_u32(st + bx * GT_BOXB + r * 2048)), "l"(&xmap), "r"(c0 + 64 * bx),
+                "r"(m * 16 + 16 * r), "r"(smem_u32(&full_bar[s]))
+              : "memory");
         }
         __syncwarp();
       }
@@ -914,29 +938,32 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[p][nt][q] = 0.f;
-    int tile = -1;
+    int row0 = -1, m16 = 0;
     for (int kc = 0; kc < nkc; ++kc, ++it) {
       const int s = it % S;
       mbar_wait(&full_bar[s], (it / S) & 1);
       if (it == 0 && tid == 0) gate_trace(1);
       if (tid == 0) gate_trace_stage(it);
-      tile = s_stage_tile[s];
-      if (tile < 0) break;
-      const uint8_t* st = gsm + (size_t)s * C::STAGEB;
-      const int nsteps = (min(GT_KC, d - kc * GT_KC) + 63) / 64 * 4;
-      const int half = nsteps / 2;                       // whole boxes: a multiple of 4
-      const uint32_t abase = smem_u32(st) + lrow * 128;
-      const uint2* bl = reinterpret_cast<const uint2*>(st + GT_XB);
-      for (int j = kh * half; j < (kh + 1) * half; ++j) {
-        uint32_t a[4];
-        const int q = ((j & 3) * 2 + lhi) ^ (lrow & 7);
-        ldmatrix_x4(a, abase + (j >> 2) * GT_BOXB + q * 16);
+      row0 = s_stage_row[s];
+      if (row0 < 0) break;
+      m16 = s_stage_m16[s];
+      if (mt < m16) {
+        const uint8_t* st = gsm + (size_t)s * C::STAGEB;
+        const int nsteps = (min(GT_KC, d - kc * GT_KC) + 63) / 64 * 4;
+        const int half = nsteps / 2;                       // whole boxes: a multiple of 4
+        const uint32_t abase = smem_u32(st) + lrow * 128;
+        const uint2* bl = reinterpret_cast<const uint2*>(st + GT_XB);
+        for (int j = kh * half; j < (kh + 1) * half; ++j) {
+          uint32_t a[4];
+          const int q = ((j & 3) * 2 + lhi) ^ (lrow & 7);
+          ldmatrix_x4(a, abase + (j >> 2) * GT_BOXB + q * 16);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+          for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            const uint2 b = bl[((((j >> 2) * NT + nt) * 3 + p) * 4 + (j & 3)) * 32 + lane];
-            mma_bf16_16816(acc[p][nt], a[0], a[1], a[2], a[3], b.x, b.y);
+            for (int p = 0; p < 3; ++p) {
+              const uint2 b = bl[((((j >> 2) * NT + nt) * 3 + p) * 4 + (j & 3)) * 32 + lane];
+              mma_bf16_16816(acc[p][nt], a[0], a[1], a[2], a[3], b.x, b.y);
+            }
           }
         }
       }
@@ -944,10 +971,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
     const int b = n & 1;
-    if (tid == 0 && tile >= 0) gate_trace(7);
+    if (tid == 0 && row0 >= 0) gate_trace(7);
     mbar_wait(&lempty_bar[b], ((n >> 1) & 1) ^ 1);      // routing done with buffer b
-    if (tid == 0 && tile >= 0) gate_trace(8);
-    if (tile >= 0) {
+    if (tid == 0 && row0 >= 0) gate_trace(8);
+    if (row0 >= 0) {
       // partial logits, smallest weight part first; C fragment rows g / g+8,
       // experts nt*8 + 2c + {0,1}
 #pragma unroll
@@ -962,16 +989,19 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
         s_part[kh][mt * 16 + g + 8][e + 1] = v[3];
       }
       consumer_sync<GT_CONSUMERS * 32>();
-      for (int i = tid; i < TOK * NMAX; i += GT_CONSUMERS * 32) {
+      for (int i = tid; i < m16 * 16 * NMAX; i += GT_CONSUMERS * 32) {
         const int t = i / NMAX, e = i % NMAX;
         s_logit[b][t][e] = s_part[0][t][e] + s_part[1][t][e];
       }
     }
-    if (tid == 0) s_logit_tile[b] = tile;
+    if (tid == 0) {
+      s_logit_row[b] = row0;
+      s_logit_nv[b] = row0 >= 0 ? min(m16 * 16, n_tok - row0) : 0;
+    }
     consumer_sync<GT_CONSUMERS * 32>();   // s_part reads done before the next tile's writes
-    if (tid == 0 && tile >= 0) gate_trace(9);
+    if (tid == 0 && row0 >= 0) gate_trace(9);
     if (lane == 0) mbar_arrive(&lfull_bar[b]);
-    if (tile < 0) break;
+    if (row0 < 0) break;
   }
 }
 
@@ -983,17 +1013,14 @@ int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* p
                    int32_t* idx, float* w, int32_t* slots, uint8_t* drop, int32_t* counts,
                    float* prob_sum, uint8_t* ws, cudaStream_t st) {
   using C = GateTC<NT>;
-  const int tiles = (T_ + TOK - 1) / TOK;
+  const int n16 = (T_ + 15) / 16;
   const int ngrp = (d + 63) / 64;
+  // persistent and fully resident (one CTA per SM): the in-kernel wait for
+  // every CTA's counts cannot deadlock
+  const int grid = min(min(n16, num_sms()), 1024);
   uint32_t* ctrs = reinterpret_cast<uint32_t*>(ws);
-  uint32_t* tile_counts = reinterpret_cast<uint32_t*>(ws + CTR_BYTES);
-  float* psum = reinterpret_cast<float*>(ws + CTR_BYTES + (size_t)tiles * N * 4);
-  // the in-kernel slot pass scans the (tiles, N) count and probability tables
-  // inside the stage ring
-  if ((size_t)2 * (tiles + 1) * N * 4 > (size_t)C::STAGES * C::STAGEB) {
-    set_error("tensor-core gate: %d tokens x %d experts exceed the in-kernel slot table", T_, N);
-    return SCMOE_ERR_UNSUPPORTED;
-  }
+  uint32_t* cta_cnt = reinterpret_cast<uint32_t*>(ws + CTR_BYTES);
+  float* cta_psum = reinterpret_cast<float*>(ws + CTR_BYTES + (size_t)grid * N * 4);
   const uint8_t* blob = (const uint8_t*)presplit;
   if (!blob) {      // split the weights now (inference callers pass a cached blob)
     uint8_t* b = ws + gate_ws_bytes(T_, N);
@@ -1002,7 +1029,7 @@ int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* p
     SCMOE_LAUNCH_CHECK();
     blob = b;
   }
-  // publish counter of the in-kernel slot pass (a memset node in a graph)
+  // publish counter of the in-kernel prefix (a memset node in a graph)
   SCMOE_CUDA_TRY(cudaMemsetAsync(ctrs, 0, 16, st));
   static bool attr_set = false;   // once per instantiation, never inside a graph capture
   if (!attr_set) {
@@ -1011,14 +1038,11 @@ int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* p
     attr_set = true;
   }
   CUtensorMap xmap;
-  const int rc = make_map_2d(&xmap, x, d, T_, ld_x * 2, TOK);
+  const int rc = make_map_2d(&xmap, x, d, T_, ld_x * 2, 16);
   if (rc != SCMOE_OK) return rc;
-  // persistent and fully resident (one CTA per SM): the in-kernel wait for
-  // every tile's counts cannot deadlock
-  const int grid = min(tiles, num_sms());
   gate_topk_tc_kernel<NT><<<grid, GT_THREADS, C::SMEM, st>>>(
       xmap, blob, excl, T_, d, N, k, quota, logits, idx, w, slots, drop, counts, prob_sum, ctrs,
-      tile_counts, psum, tiles);
+      cta_cnt, cta_psum, n16);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

@@ -18,8 +18,9 @@ flush = torch.ones(128 * 1024 * 1024, device="cuda")
 lib = _lib.lib()
 fn = lib.scmoe_debug_gate_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-tiles = (T + 63) // 64
-ctas = min(tiles, torch.cuda.get_device_properties(0).multi_processor_count)
+n16 = (T + 15) // 16
+ctas = min(n16, torch.cuda.get_device_properties(0).multi_processor_count)
+tiles = ctas * ((n16 + ctas - 1) // ctas + 3) // 4     # sub-tiles of <= 4 row tiles per CTA
 for rep in range(4):
     flush.sum()
     torch.cuda.synchronize()

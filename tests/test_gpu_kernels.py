@@ -81,12 +81,14 @@ def test_gate_ties_and_zeros(dtype):
 @pytest.mark.parametrize("T,d,N,k,cf", [
     (1, 64, 1, 1, 1.0), (300, 384, 8, 1, 1.0), (129, 320, 5, 2, 1.0), (2000, 4096, 16, 2, 1.0),
     (5000, 3072, 12, 1, 1.25), (64, 64, 16, 4, 0.5), (40000, 256, 8, 2, 1.0),
-    (300, 200, 8, 1, 1.0), (129, 72, 5, 2, 1.0)])
+    (300, 200, 8, 1, 1.0), (129, 72, 5, 2, 1.0), (200000, 64, 8, 2, 1.0)])
 def test_gate_tensor_core_path(T, d, N, k, cf):
     """bf16 tokens, N <= 16, d % 64 == 0: the persistent tensor-core gate
     (mma.sync on a 3-part bf16 weight split, bulk-copied row stages): one and
     several stages per tile, partial last stage (d=384, 320), partial last
-    tile, more tiles than SMs (T=40000).  d % 64 != 0 takes the FMA kernel."""
+    tile, more tiles than SMs (T=40000), more CTA-local ranks than the
+    shared-memory rank cache holds (T=200000, k=2: re-read from `slots`).
+    d % 64 != 0 takes the FMA kernel."""
     _gate_case(T, d, N, k, cf, torch.bfloat16, seed=T + d + N)
 
 
