@@ -459,7 +459,52 @@ def hbm_kernel_times(moe, x, reps: int = 10):
         us = sum(getattr(e, "device_time_total", 0.0) or e.cuda_time_total for e in own) / reps
         res_d[name] = {"us": us, "bytes": nbytes, "gbps": nbytes / us / 1e3,
                        "kernels": sorted({e.name.split("(")[0][-60:] for e in own})}
-    del flush
+    # Sustained: R back-to-back ops on rotating input AND output buffers (one
+    # graph), so op i's dirty lines drain to DRAM while op i+1 runs and are
+    # charged to it — the single-op number above ends while up to ~2/3 of the
+    # output still sits in L2 (ncu: dispatch wrote 19.5 of 67 MB before its
+    # end).  Mean CUPTI kernel time per op over the last R-1 ops.
+    R = 6
+    xs = [x.clone() for _ in range(R)]
+    bufs = [torch.empty_like(buf) for _ in range(R)]
+    ses = [torch.randn_like(x) for _ in range(R)]
+    outs = [torch.empty_like(x) for _ in range(R)]
+    rot = {
+        "gate": lambda i: moe.route(xs[i]),
+        "dispatch": lambda i: K.dispatch(xs[i], dec.indices, dec.slots, N, dec.capacity,
+                                         out=bufs[i]),
+        "combine": lambda i: K.combine(bufs[i], dec.indices, dec.slots, dec.weights, dec.capacity,
+                                       se_out=ses[i], residual=xs[i], out=outs[i]),
+    }
+    for name, fn in rot.items():
+        for i in range(R):
+            fn(i)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(st)
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for i in range(R):
+                    fn(i)
+        st.wait_stream(cs)
+        torch.cuda.synchronize()
+        flush.sum()
+        g.replay()
+        torch.cuda.synchronize()
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            flush.sum()
+            g.replay()
+            torch.cuda.synchronize()
+        dev = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                      and "reduce_kernel" not in e.name], key=lambda e: e.time_range.start)
+        per_op = len(dev) // R
+        tail = dev[per_op:]                       # ops 2..R: each pays its predecessor's drain
+        us = sum(getattr(e, "device_time_total", 0.0) or e.cuda_time_total for e in tail) / (R - 1)
+        nbytes = res_d[name]["bytes"]
+        res_d[name].update({"sustained_us": us, "sustained_gbps": nbytes / us / 1e3})
+    del flush, xs, bufs, ses, outs
     return res_d
 
 
@@ -1130,11 +1175,16 @@ def run_ours(args):
                                 "the kept rows, gate"},
         "clocks": clocks,
         "hbm_kernels": None if hbm_ops is None else {
-            k: dict(v, peak=peaks.get("hbm_gbs"), frac=v["gbps"] / peaks["hbm_gbs"]
+            k: dict(v, peak=peaks.get("hbm_gbs"),
+                    frac=v["gbps"] / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
+                    sustained_frac=v["sustained_gbps"] / peaks["hbm_gbs"]
                     if peaks.get("hbm_gbs") else None) for k, v in hbm_ops.items()},
-        "hbm_kernels_note": "CUPTI durations of each op's kernels after a 512 MB read flush of "
-                            "L2; the op's writes can still be draining from L2 when its kernel "
-                            "ends, so frac may exceed 1 against the measured copy peak",
+        "hbm_kernels_note": "us / frac: CUPTI durations of one op's kernels after a 512 MB read "
+                            "flush of L2 (the op's writes can still be draining from L2 when its "
+                            "kernel ends, so frac may exceed 1 against the measured copy peak); "
+                            "sustained_*: 6 back-to-back ops on rotating input and output "
+                            "buffers in one graph, mean of ops 2..6, each paying the previous "
+                            "op's write-back",
         "gpu_launches": args.steps * own_per_step,
         "launches_per_step": {"scmoe": own_per_step, "library": lib_per_step,
                               "how": "torch.profiler (CUPTI) over one step; 'scmoe' = kernels of "

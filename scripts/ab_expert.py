@@ -22,6 +22,7 @@ w1 = (torch.randn(h, d, device="cuda", generator=gen) * 0.02).bfloat16()
 w2 = (torch.randn(d, h, device="cuda", generator=gen) * 0.02).bfloat16()
 b1 = torch.zeros(h, device="cuda"); b2 = torch.zeros(d, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+K.set_gemm_epilogue_warps(int(os.environ.get("SCMOE_EPI", "0")))
 with torch.no_grad():
     dec = layer.route(x)
     buf = K.dispatch(x, dec.indices, dec.slots, N, dec.capacity)
@@ -48,11 +49,13 @@ for i, e in enumerate(ks):
 print(json.dumps({k: sorted(v)[len(v) // 2] for k, v in res.items()}))
 '''
 libs = sys.argv[1:3]
+# "lib.so@16": the same build with 16 epilogue warps forced (SCMOE_EPI)
 rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 res = {l: [] for l in libs}
 for r in range(rounds):
     for lib in libs:
-        env = dict(os.environ, SCMOE_LIB=os.path.abspath(lib), ROOT=ROOT)
+        path, _, epi = lib.partition("@")
+        env = dict(os.environ, SCMOE_LIB=os.path.abspath(path), ROOT=ROOT, SCMOE_EPI=epi or "0")
         out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
         if not line:

@@ -42,7 +42,18 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size",
            "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
-           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_bytes.sum"]
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_bytes.sum",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_elapsed",
+           "smsp__average_warp_latency_issue_stalled_long_scoreboard",
+           "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
+           "smsp__pcsamp_warps_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_wait",
+           "smsp__pcsamp_warps_issue_stalled_lg_throttle",
+           "smsp__pcsamp_warps_issue_stalled_mio_throttle",
+           "smsp__pcsamp_warps_issue_stalled_membar",
+           "smsp__pcsamp_warps_issue_stalled_sleeping",
+           "smsp__pcsamp_warps_issue_stalled_selected"]
 
 
 def full(path):
