@@ -198,6 +198,23 @@ size_t scmoe_grouped_colsum_workspace_bytes(int num_groups, int group_cap, int c
 int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap, int cols,
                          const int32_t* group_rows, int rows_clip, float* out,
                          void* workspace, size_t workspace_bytes, void* stream);
+/* Two matrices with the same groups (x0: (G, cap, cols0), x1: (G, cap,
+ * cols1), e.g. an FFN's two bias gradients dy and dz) in one launch per
+ * pass: out0 (G, cols0), out1 (G, cols1), same arithmetic as two
+ * scmoe_grouped_colsum calls.  The passes are programmatic dependent
+ * launches. */
+size_t scmoe_grouped_colsum2_workspace_bytes(int num_groups, int group_cap, int cols0,
+                                             int cols1);
+int scmoe_grouped_colsum2(const void* x0, const void* x1, int dtype, int num_groups,
+                          int group_cap, int cols0, int cols1, const int32_t* group_rows,
+                          int rows_clip, float* out0, float* out1, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* Balance loss from the gate's statistics (arch.py:436-439, gating.py:
+ * 159-170): *aux = N * sum_e (counts[e] / (T k)) (prob_sum[e] / T), fp32,
+ * experts summed in order. */
+int scmoe_gate_aux_loss(const int32_t* counts, const float* prob_sum, int n_tokens,
+                        int n_experts, int k, float* aux, void* stream);
 
 /* Expert migration (offload.py:109-182 made real): dst[j] = src[ids[j]] for
  * j < min(*n_rows, max_rows), rows of row_bytes.  src may be pinned host

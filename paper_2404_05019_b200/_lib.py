@@ -59,6 +59,9 @@ SIGNATURES = [
     ("scmoe_zero_tails", _i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _vp]),
     ("scmoe_grouped_colsum_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_grouped_colsum", _i, [_vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),
+    ("scmoe_gate_aux_loss", _i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    ("scmoe_grouped_colsum2_workspace_bytes", _sz, [_i, _i, _i, _i]),
+    ("scmoe_grouped_colsum2", _i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
     ("scmoe_dispatch_scaled", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
     ("scmoe_expert_ffn", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i,
                               _i, _i, _vp]),

@@ -3,6 +3,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace scmoe {
@@ -71,30 +73,38 @@ constexpr int COLSUM_BLOCK = 256;        // threads per block: vectors x row lan
 
 int colsum_vec(int dtype) { return dtype == SCMOE_BF16 ? 8 : 4; }
 
-// stripes per group: ~6 blocks per SM over (column tiles x groups): short,
-// latency-bound row loops with many blocks in flight (fewer, longer stripes
-// measured slower); the final pass reads the partials four loads at a time
-int colsum_stripes(int num_groups, int group_cap, int cols, int vec) {
-  const int vecs = (cols + vec - 1) / vec;
-  const int col_tiles = (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
-  int st = (6 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
-  return max(1, min(st, (group_cap + 7) / 8));
-}
+// Up to two matrices with the same group structure (an FFN's two bias
+// gradients) in one launch per pass: tensor i covers column tiles
+// [tile0[i], tile0[i+1]) of blockIdx.x (pass 1) / column blocks (pass 2).
+struct ColsumSet {
+  const void* x[2];
+  int cols[2];
+  int vpb[2];          // column vectors per pass-1 tile
+  int tile0[3];        // pass-1 column-tile ranges
+  int blk0[3];         // pass-2 32-column block ranges
+  float* part[2];      // [G][n_stripes][cols]
+  float* out[2];       // [G][cols]
+};
 
 template <typename T>
 __global__ void __launch_bounds__(COLSUM_BLOCK)
-colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
-                      const int32_t* __restrict__ group_rows, int rows_clip, int stripe_rows,
-                      int n_stripes, float* __restrict__ part) {
+colsum_partial_kernel(ColsumSet cs, int cap, const int32_t* __restrict__ group_rows, int rows_clip,
+                      int stripe_rows, int n_stripes) {
   constexpr int VEC = Vec16<T>::N;
   constexpr int U = 8;
   __shared__ float red[COLSUM_BLOCK][VEC + 1];
+  // programmatic dependent launch: nothing global is read before the
+  // producer of x completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int ti = blockIdx.x >= cs.tile0[1] ? 1 : 0;
+  const T* x = (const T*)cs.x[ti];
+  const int cols = cs.cols[ti];
   const int vecs = cols / VEC;
-  const int vpb = min(vecs, COLSUM_THREADS);              // vectors per column tile
+  const int vpb = cs.vpb[ti];                              // vectors per column tile
   const int lanes = blockDim.x / vpb;
   const int v = threadIdx.x % vpb, lane = threadIdx.x / vpb;
   const int g = blockIdx.z, stripe = blockIdx.y;
-  const int cv = blockIdx.x * vpb + v;                     // my column vector
+  const int cv = (blockIdx.x - cs.tile0[ti]) * vpb + v;    // my column vector
   const bool active = lane < lanes && cv < vecs;
   const int rows = group_rows ? max(0, min(group_rows[g], rows_clip)) : cap;
   const int r0 = stripe * stripe_rows, r1 = min(rows, r0 + stripe_rows);
@@ -128,12 +138,13 @@ colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
 #pragma unroll
   for (int i = 0; i < VEC; ++i) red[threadIdx.x][i] = s[i];
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (lane == 0 && cv < vecs) {
     float o[VEC] = {};
     for (int l = 0; l < lanes; ++l)
 #pragma unroll
       for (int i = 0; i < VEC; ++i) o[i] += red[l * vpb + v][i];
-    float* q = part + ((long long)g * n_stripes + stripe) * cols + (long long)cv * VEC;
+    float* q = cs.part[ti] + ((long long)g * n_stripes + stripe) * cols + (long long)cv * VEC;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) q[i] = o[i];
   }
@@ -141,14 +152,16 @@ colsum_partial_kernel(const T* __restrict__ x, int cap, int cols,
 
 // block (32 columns x 32 stripe lanes): lane y sums stripes y, y+32, ...,
 // then the 32 lane sums are added in a fixed order
-__global__ void colsum_final_kernel(const float* __restrict__ part, int n_stripes, int cols,
-                                    int n_groups, float* __restrict__ out) {
+__global__ void colsum_final_kernel(ColsumSet cs, int n_stripes) {
   __shared__ float red[32][33];
+  asm volatile("griddepcontrol.wait;" ::: "memory");     // pass 1 complete
+  const int ti = blockIdx.x >= cs.blk0[1] ? 1 : 0;
+  const int cols = cs.cols[ti];
   const int g = blockIdx.y;
-  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int c = (blockIdx.x - cs.blk0[ti]) * 32 + threadIdx.x;
   float a[4] = {0.f, 0.f, 0.f, 0.f};
   if (c < cols) {
-    const float* p = part + (long long)g * n_stripes * cols + c;
+    const float* p = cs.part[ti] + (long long)g * n_stripes * cols + c;
     int k = threadIdx.y;
     for (; k + 96 < n_stripes; k += 128) {     // four independent loads in flight
 #pragma unroll
@@ -162,8 +175,105 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int n_stripe
     float t = 0.f;
 #pragma unroll 8
     for (int y = 0; y < 32; ++y) t += red[y][threadIdx.x];
-    out[(long long)g * cols + c] = t;
+    cs.out[ti][(long long)g * cols + c] = t;
   }
+}
+
+// aux = N / (T * T * k) * sum_e counts[e] * prob_sum[e] in fp32, experts in
+// order (arch.py:436-439: N * sum_e f_e P_e with f_e = counts[e] / (T k),
+// P_e = prob_sum[e] / T): one warp instead of five tensor ops
+__global__ void gate_aux_kernel(const int32_t* __restrict__ counts,
+                                const float* __restrict__ prob_sum, int n_experts, float scale,
+                                float* __restrict__ aux) {
+  if (threadIdx.x != 0) return;
+  float s = 0.f;
+  for (int e = 0; e < n_experts; ++e) s += (float)counts[e] * prob_sum[e];
+  *aux = s * scale;
+}
+
+template <typename K, typename... Args>
+int launch_pdl(K kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SCMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return SCMOE_OK;
+}
+
+// stripes for a set: ~6 blocks per SM over (column tiles of both x groups)
+int colsum_set_stripes(int num_groups, int group_cap, int col_tiles) {
+  int st = (6 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
+  return max(1, min(st, (group_cap + 7) / 8));
+}
+
+int colsum_tiles(int cols, int vec) {
+  const int vecs = (cols + vec - 1) / vec;
+  return (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
+}
+
+size_t colsum2_ws_bytes(int num_groups, int group_cap, int cols0, int cols1) {
+  if (num_groups < 1 || group_cap < 1 || cols0 < 1 || cols1 < 0) return 0;
+  // large enough for either vector width (bf16 8, fp32 4 per 16 bytes)
+  size_t st = 0;
+  for (int vec : {8, 4}) {
+    const int ct = colsum_tiles(cols0, vec) + (cols1 ? colsum_tiles(cols1, vec) : 0);
+    st = std::max(st, (size_t)colsum_set_stripes(num_groups, group_cap, ct));
+  }
+  return st * (size_t)num_groups * (size_t)(cols0 + cols1) * sizeof(float);
+}
+
+int colsum2_impl(const void* x0, const void* x1, int dtype, int num_groups, int group_cap,
+                 int cols0, int cols1, const int32_t* group_rows, int rows_clip, float* out0,
+                 float* out1, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
+  SCMOE_CHECK_ARG(num_groups >= 1 && cols0 >= 1 && cols1 >= 0 && group_cap >= 1,
+                  "bad colsum shape");
+  SCMOE_CHECK_ARG(workspace_bytes >= colsum2_ws_bytes(num_groups, group_cap, cols0, cols1),
+                  "colsum workspace too small");
+  if (rows_clip <= 0) rows_clip = group_cap;
+  const int vec = colsum_vec(dtype);
+  SCMOE_CHECK_ARG(cols0 % vec == 0 && cols1 % vec == 0 && ((uintptr_t)x0 & 15) == 0 &&
+                      ((uintptr_t)x1 & 15) == 0,
+                  "colsum needs 16-byte aligned rows (cols multiple of %d)", vec);
+  ColsumSet cs = {};
+  const int n = cols1 ? 2 : 1;
+  const void* xs[2] = {x0, x1};
+  const int cl[2] = {cols0, cols1};
+  float* outs[2] = {out0, out1};
+  cs.tile0[0] = cs.blk0[0] = 0;
+  for (int i = 0; i < 2; ++i) {
+    cs.x[i] = xs[i];
+    cs.cols[i] = cl[i];
+    cs.out[i] = outs[i];
+    const int vecs = cl[i] / vec;
+    cs.vpb[i] = std::max(1, std::min(vecs, COLSUM_THREADS));
+    const int ct = i < n ? (vecs + cs.vpb[i] - 1) / cs.vpb[i] : 0;
+    cs.tile0[i + 1] = cs.tile0[i] + ct;
+    cs.blk0[i + 1] = cs.blk0[i] + (i < n ? (cl[i] + 31) / 32 : 0);
+  }
+  const int n_stripes = colsum_set_stripes(num_groups, group_cap, cs.tile0[2]);
+  const int stripe_rows = (group_cap + n_stripes - 1) / n_stripes;
+  cs.part[0] = (float*)workspace;
+  cs.part[1] = cs.part[0] + (size_t)num_groups * n_stripes * cols0;
+  dim3 grid(cs.tile0[2], n_stripes, num_groups);
+  int rc = dtype == SCMOE_BF16
+               ? launch_pdl(colsum_partial_kernel<__nv_bfloat16>, grid, dim3(COLSUM_BLOCK), st, cs,
+                            group_cap, group_rows, rows_clip, stripe_rows, n_stripes)
+               : launch_pdl(colsum_partial_kernel<float>, grid, dim3(COLSUM_BLOCK), st, cs,
+                            group_cap, group_rows, rows_clip, stripe_rows, n_stripes);
+  if (rc) return rc;
+  SCMOE_LAUNCH_CHECK();
+  rc = launch_pdl(colsum_final_kernel, dim3(cs.blk0[2], num_groups), dim3(32, 32), st, cs,
+                  n_stripes);
+  if (rc) return rc;
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
 }
 
 // dst[j] = src[ids[j]] for j < min(*n_rows, max_rows); rows of row_bytes
@@ -354,45 +464,38 @@ extern "C" int scmoe_zero_tails(void* buf, int dtype, int num_groups, int group_
 }
 
 extern "C" size_t scmoe_grouped_colsum_workspace_bytes(int num_groups, int group_cap, int cols) {
-  if (num_groups < 1 || group_cap < 1 || cols < 1) return 0;
-  // large enough for either vector width (bf16 8, fp32 4 per 16 bytes)
-  const size_t st = (size_t)max(colsum_stripes(num_groups, group_cap, cols, 8),
-                                colsum_stripes(num_groups, group_cap, cols, 4));
-  return st * (size_t)num_groups * (size_t)cols * sizeof(float);
+  return colsum2_ws_bytes(num_groups, group_cap, cols, 0);
 }
 
 extern "C" int scmoe_grouped_colsum(const void* x, int dtype, int num_groups, int group_cap,
                                     int cols, const int32_t* group_rows, int rows_clip,
                                     float* out, void* workspace, size_t workspace_bytes,
                                     void* stream) {
-  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
-  SCMOE_CHECK_ARG(num_groups >= 1 && cols >= 1 && group_cap >= 1, "bad colsum shape");
-  SCMOE_CHECK_ARG(workspace_bytes >= scmoe_grouped_colsum_workspace_bytes(num_groups, group_cap,
-                                                                          cols),
-                  "colsum workspace too small");
-  if (rows_clip <= 0) rows_clip = group_cap;
-  const int vec = colsum_vec(dtype);
-  SCMOE_CHECK_ARG(cols % vec == 0 && ((uintptr_t)x & 15) == 0,
-                  "colsum needs 16-byte aligned rows (cols multiple of %d)", vec);
-  cudaStream_t st = (cudaStream_t)stream;
-  const int vecs = cols / vec;
-  const int vpb = min(vecs, COLSUM_THREADS);
-  const int col_tiles = (vecs + vpb - 1) / vpb;
-  const int n_stripes = colsum_stripes(num_groups, group_cap, cols, vec);
-  const int stripe_rows = (group_cap + n_stripes - 1) / n_stripes;
-  const int threads = (COLSUM_BLOCK / vpb) * vpb;          // whole row lanes of vpb vectors
-  dim3 grid(col_tiles, n_stripes, num_groups);
-  float* part = (float*)workspace;
-  if (dtype == SCMOE_BF16)
-    colsum_partial_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
-        (const __nv_bfloat16*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes,
-        part);
-  else
-    colsum_partial_kernel<float><<<grid, threads, 0, st>>>(
-        (const float*)x, group_cap, cols, group_rows, rows_clip, stripe_rows, n_stripes, part);
-  SCMOE_LAUNCH_CHECK();
-  colsum_final_kernel<<<dim3((cols + 31) / 32, num_groups), dim3(32, 32), 0, st>>>(
-      part, n_stripes, cols, num_groups, out);
+  return colsum2_impl(x, x, dtype, num_groups, group_cap, cols, 0, group_rows, rows_clip, out,
+                      nullptr, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" size_t scmoe_grouped_colsum2_workspace_bytes(int num_groups, int group_cap, int cols0,
+                                                        int cols1) {
+  return cols1 >= 1 ? colsum2_ws_bytes(num_groups, group_cap, cols0, cols1) : 0;
+}
+
+extern "C" int scmoe_grouped_colsum2(const void* x0, const void* x1, int dtype, int num_groups,
+                                     int group_cap, int cols0, int cols1,
+                                     const int32_t* group_rows, int rows_clip, float* out0,
+                                     float* out1, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+  SCMOE_CHECK_ARG(cols1 >= 1 && x1 && out1, "colsum2 needs a second matrix");
+  return colsum2_impl(x0, x1, dtype, num_groups, group_cap, cols0, cols1, group_rows, rows_clip,
+                      out0, out1, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int scmoe_gate_aux_loss(const int32_t* counts, const float* prob_sum, int n_tokens,
+                                   int n_experts, int k, float* aux, void* stream) {
+  SCMOE_CHECK_ARG(n_tokens >= 1 && n_experts >= 1 && k >= 1 && counts && prob_sum && aux,
+                  "bad aux-loss arguments");
+  const float scale = (float)((double)n_experts / ((double)n_tokens * (double)n_tokens * k));
+  gate_aux_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(counts, prob_sum, n_experts, scale, aux);
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

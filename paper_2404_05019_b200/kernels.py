@@ -497,6 +497,38 @@ def grouped_colsum(x: torch.Tensor, group_rows: Optional[torch.Tensor] = None, r
     return out if x.dim() == 3 else out.view(D)
 
 
+def gate_aux_loss(counts: torch.Tensor, prob_sum: torch.Tensor, n_tokens: int, k: int,
+                  stream=None) -> torch.Tensor:
+    """Balance loss N * sum_e f_e P_e from the gate kernel's counts and
+    probability sums, one launch (arch.py:436-439)."""
+    ensure_device(counts)
+    aux = torch.empty((), device=counts.device, dtype=torch.float32)
+    check(lib().scmoe_gate_aux_loss(ptr(_c(counts, "counts")), ptr(_c(prob_sum, "prob_sum")),
+                                    n_tokens, counts.shape[0], k, ptr(aux), stream_ptr(stream)))
+    return aux
+
+
+def grouped_colsum2(x0: torch.Tensor, x1: torch.Tensor, group_rows: Optional[torch.Tensor] = None,
+                    rows_clip: int = 0, stream=None):
+    """(grouped_colsum(x0), grouped_colsum(x1)) for two matrices with the same
+    groups and dtype, one launch per pass."""
+    ensure_device(x0)
+    a = x0 if x0.dim() == 3 else x0.unsqueeze(0)
+    b = x1 if x1.dim() == 3 else x1.unsqueeze(0)
+    G, C, D0 = a.shape
+    if b.shape[:2] != (G, C) or b.dtype != a.dtype:
+        raise ValueError("grouped_colsum2 needs the same groups, rows and dtype")
+    D1 = b.shape[2]
+    out = torch.empty(G * (D0 + D1), device=x0.device, dtype=torch.float32)
+    o0, o1 = out[:G * D0].view(G, D0), out[G * D0:].view(G, D1)
+    ws_bytes = lib().scmoe_grouped_colsum2_workspace_bytes(G, C, D0, D1)
+    ws = torch.empty(ws_bytes, device=x0.device, dtype=torch.uint8)
+    check(lib().scmoe_grouped_colsum2(ptr(_c(a, "x0")), ptr(_c(b, "x1")), dtype_code(a.dtype), G, C,
+                                      D0, D1, ptr(group_rows), rows_clip, ptr(o0), ptr(o1),
+                                      ptr(ws), ws_bytes, stream_ptr(stream)))
+    return (o0 if x0.dim() == 3 else o0.view(D0)), (o1 if x1.dim() == 3 else o1.view(D1))
+
+
 def dispatch_scaled(x: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor, n_experts: int,
                     capacity: int, row_scale: Optional[torch.Tensor],
                     out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

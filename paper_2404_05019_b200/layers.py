@@ -114,11 +114,8 @@ class GateDecision:
                               minlength=self.n_experts).to(torch.int32)
 
     def aux_loss(self) -> torch.Tensor:
-        """N * sum_i f_i P_i (arch.py:436-439 / gating.py:159-170)."""
-        t, n, k = self.n_tokens, self.n_experts, self.k
-        f = self.counts.to(torch.float32) / float(t * k)
-        p = self.prob_sum / float(t)
-        return n * (f * p).sum()
+        """N * sum_i f_i P_i (arch.py:436-439 / gating.py:159-170), one kernel."""
+        return K.gate_aux_loss(self.counts, self.prob_sum, self.n_tokens, self.k)
 
     def to_numpy(self) -> dict:
         return dict(logits=self.logits.double().cpu().numpy(),

@@ -169,11 +169,9 @@ class FFNFn(torch.autograd.Function):
             # gelu'(z) in the data-gradient GEMM's epilogue, zero tails
             dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_MUL_AUX,
                                    group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
-            db1_g = None
         else:
             dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
                                    group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
-            db1_g = None
         fuse_res = has_res and ctx.res_is_x
         parked = _take(ctx.link)
         extra = dy3 if fuse_res else (parked.view(G, C, d) if parked is not None else None)
@@ -186,8 +184,8 @@ class FFNFn(torch.autograd.Function):
         # bias gradients: column sums over the valid rows (HBM-bound, 8 row
         # loads in flight per thread), then the source groups of each weight
         # group summed like the weight gradients
-        db2 = _wsum(K.grouped_colsum(dy3, group_rows, rows_clip), W)
-        db1 = _wsum(db1_g if db1_g is not None else K.grouped_colsum(dz, group_rows, rows_clip), W)
+        db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
+        db2, db1 = _wsum(db2_g, W), _wsum(db1_g, W)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),
                 (dy if has_res and not fuse_res else None), None, None, None)
@@ -206,7 +204,7 @@ class GateFn(torch.autograd.Function):
     def forward(ctx, src, w_gate_t, w_noise_t, logits, indices, counts, weights, prob_sum, k,
                 eps, noise_pre):
         t, n = logits.shape
-        aux = (counts.to(torch.float32) * prob_sum).sum() * (n / float(t * t * k))
+        aux = K.gate_aux_loss(counts, prob_sum, t, k)
         ctx.save_for_backward(src, w_gate_t, w_noise_t, logits, indices, counts, weights, eps,
                               noise_pre)
         return weights.clone(), aux
