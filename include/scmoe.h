@@ -108,6 +108,19 @@ int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld_x, const f
                              int32_t* indices, float* weights, int32_t* slots, uint8_t* dropped,
                              int32_t* counts, float* prob_sum, void* workspace,
                              size_t workspace_bytes, void* stream);
+/* Both of the above in one entry (w_split may be null; noise as in
+ * scmoe_gate_topk), plus `sync`: two uint32 words the caller zeroes ONCE
+ * and keeps for the gate's lifetime.  Every launch leaves them zero, so the
+ * tensor-core path issues no per-call memset of its cross-CTA counter (in a
+ * CUDA graph a memset node costs ~8 us of idle GPU).  Launches sharing one
+ * `sync` must not overlap in time (one stream per gate).  Null = the
+ * workspace's counter, zeroed per call. */
+int scmoe_gate_topk_ex(const void* x, int x_dtype, long long ld_x, const float* w_gate_t,
+                       const void* w_split, const float* w_noise_t, const float* eps,
+                       const int32_t* exclude, int n_tokens, int d_model, int n_experts, int k,
+                       int quota, float* logits, int32_t* indices, float* weights,
+                       int32_t* slots, uint8_t* dropped, int32_t* counts, float* prob_sum,
+                       void* workspace, size_t workspace_bytes, uint32_t* sync, void* stream);
 
 /*
  * K2 — dispatch ("encode"): copy each kept selection's row
@@ -215,6 +228,18 @@ int scmoe_grouped_colsum2(const void* x0, const void* x1, int dtype, int num_gro
  * experts summed in order. */
 int scmoe_gate_aux_loss(const int32_t* counts, const float* prob_sum, int n_tokens,
                         int n_experts, int k, float* aux, void* stream);
+
+/* out[i] = dtype(src[0] / div), i < n: the constant gradient of a mean loss
+ * (grad.py:52-67) from a device scalar without a host sync; 16-byte aligned
+ * out. */
+int scmoe_fill_div(void* out, int dtype, long long n, const float* src, float div, void* stream);
+
+/* *out = mean(x[0..n)) accumulated in fp32, deterministic two-pass (the
+ * "mean" LossSpec, grad.py:52-67); workspace of scmoe_mean_workspace_bytes()
+ * bytes; no memset. */
+size_t scmoe_mean_workspace_bytes(void);
+int scmoe_mean(const void* x, int dtype, long long n, float* out, void* workspace,
+               size_t workspace_bytes, void* stream);
 
 /* Expert migration (offload.py:109-182 made real): dst[j] = src[ids[j]] for
  * j < min(*n_rows, max_rows), rows of row_bytes.  src may be pinned host

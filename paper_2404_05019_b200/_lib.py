@@ -38,6 +38,8 @@ SIGNATURES = [
     ("scmoe_gate_split_weights", _i, [_vp, _i, _i, _vp, _vp]),
     ("scmoe_gate_topk_presplit", _i, [_vp, _i, _ll, _vp, _vp, _vp, _i, _i, _i, _i, _i,
                                       _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    ("scmoe_gate_topk_ex", _i, [_vp, _i, _ll, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
+                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     ("scmoe_dispatch", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),
     ("scmoe_grouped_gemm", _i, [_vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _i, _i, _i,
                                 _vp]),
@@ -60,6 +62,9 @@ SIGNATURES = [
     ("scmoe_grouped_colsum_workspace_bytes", _sz, [_i, _i, _i]),
     ("scmoe_grouped_colsum", _i, [_vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _vp]),
     ("scmoe_gate_aux_loss", _i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    ("scmoe_fill_div", _i, [_vp, _i, ctypes.c_longlong, _vp, ctypes.c_float, _vp]),
+    ("scmoe_mean_workspace_bytes", _sz, []),
+    ("scmoe_mean", _i, [_vp, _i, ctypes.c_longlong, _vp, _vp, _sz, _vp]),
     ("scmoe_grouped_colsum2_workspace_bytes", _sz, [_i, _i, _i, _i]),
     ("scmoe_grouped_colsum2", _i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
     ("scmoe_dispatch_scaled", _i, [_vp, _i, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),

@@ -4,6 +4,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -189,6 +190,104 @@ __global__ void gate_aux_kernel(const int32_t* __restrict__ counts,
   float s = 0.f;
   for (int e = 0; e < n_experts; ++e) s += (float)counts[e] * prob_sum[e];
   *aux = s * scale;
+}
+
+// out[i] = dtype(src[0] * (1 / div)) for i < n: the constant gradient of a mean
+// (grad.py:52-67) straight from the device scalar, 16-byte stores
+template <typename T>
+__global__ void fill_div_kernel(T* __restrict__ out, long long n, const float* __restrict__ src,
+                                float div) {
+  // torch's tensor / python-scalar multiplies by the fp32 reciprocal:
+  // bit-identical to (g / n).to(dtype)
+  const float v = __ldg(src) * (1.0f / div);
+  T t;
+  if constexpr (std::is_same<T, float>::value) t = v;
+  else t = __float2bfloat16_rn(v);
+  constexpr int V = 16 / sizeof(T);
+  T pack[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) pack[i] = t;
+  const uint4 w = *reinterpret_cast<const uint4*>(pack);
+  const long long n_vec = n / V;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  uint4* o = reinterpret_cast<uint4*>(out);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_vec; i += stride)
+    o[i] = w;
+  for (long long i = n_vec * V + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    out[i] = t;
+}
+
+// mean of n elements in fp32, deterministic: pass 1 = MEAN_BLOCKS blocks,
+// each a fixed contiguous range (16-byte loads, 4 in flight per thread, a
+// fixed-order block tree) -> one partial per block; pass 2 = one block,
+// fixed-order tree over the partials, / n.  No memset (a torch reduction
+// zeroes its semaphores with a memset node: ~8 us of idle GPU in a graph).
+constexpr int MEAN_BLOCKS = 296;
+template <typename T>
+__global__ void __launch_bounds__(256) mean_partial_kernel(const T* __restrict__ x, long long n,
+                                                           float* __restrict__ part) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float red[256];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long per = (n + MEAN_BLOCKS - 1) / MEAN_BLOCKS;
+  const long long per_v = (per + V - 1) / V * V;                // whole 16-byte vectors
+  const long long lo = min(n, (long long)blockIdx.x * per_v), hi = min(n, lo + per_v);
+  float acc = 0.f;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(x + lo) & 15) == 0);
+  long long i = lo;
+  if (vec_ok) {
+    const long long nv = (hi - lo) / V;
+    const uint4* xv = reinterpret_cast<const uint4*>(x + lo);
+    long long j = threadIdx.x;
+    for (; j + 768 < nv; j += 1024) {
+      uint4 w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = ld_nc_v4(xv + j + 256 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        Vec16<T> t;
+        t.raw = w[u];
+        float f[V];
+        t.to_float(f);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc += f[q];
+      }
+    }
+    for (; j < nv; j += 256) {
+      Vec16<T> t;
+      t.raw = ld_nc_v4(xv + j);
+      float f[V];
+      t.to_float(f);
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc += f[q];
+    }
+    i = lo + nv * V;
+  }
+  for (long long r = i + threadIdx.x; r < hi; r += 256) acc += (float)x[r];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+#pragma unroll
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(512) mean_final_kernel(const float* __restrict__ part,
+                                                         long long n, float* __restrict__ out) {
+  __shared__ float red[512];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  red[threadIdx.x] = threadIdx.x < MEAN_BLOCKS ? part[threadIdx.x] : 0.f;
+  __syncthreads();
+#pragma unroll
+  for (int o = 256; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0] / (float)n;
 }
 
 template <typename K, typename... Args>
@@ -496,6 +595,45 @@ extern "C" int scmoe_gate_aux_loss(const int32_t* counts, const float* prob_sum,
                   "bad aux-loss arguments");
   const float scale = (float)((double)n_experts / ((double)n_tokens * (double)n_tokens * k));
   gate_aux_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(counts, prob_sum, n_experts, scale, aux);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" int scmoe_fill_div(void* out, int dtype, long long n, const float* src, float div,
+                              void* stream) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
+  SCMOE_CHECK_ARG(n >= 0 && src && (n == 0 || out) && ((uintptr_t)out & 15) == 0,
+                  "fill needs a 16-byte aligned output");
+  if (n == 0) return SCMOE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (int)std::min<long long>((n / 8 + 255) / 256 + 1, (long long)num_sms() * 8);
+  if (dtype == SCMOE_BF16)
+    fill_div_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((__nv_bfloat16*)out, n, src, div);
+  else
+    fill_div_kernel<float><<<grid, 256, 0, st>>>((float*)out, n, src, div);
+  SCMOE_LAUNCH_CHECK();
+  return SCMOE_OK;
+}
+
+extern "C" size_t scmoe_mean_workspace_bytes(void) { return MEAN_BLOCKS * sizeof(float); }
+
+extern "C" int scmoe_mean(const void* x, int dtype, long long n, float* out, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  SCMOE_CHECK_ARG(dtype == SCMOE_F32 || dtype == SCMOE_BF16, "bad dtype %d", dtype);
+  SCMOE_CHECK_ARG(n >= 1 && x && out, "mean needs n >= 1");
+  SCMOE_CHECK_ARG(workspace && workspace_bytes >= MEAN_BLOCKS * sizeof(float),
+                  "mean workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = (float*)workspace;
+  int rc = dtype == SCMOE_BF16
+               ? launch_pdl(mean_partial_kernel<__nv_bfloat16>, dim3(MEAN_BLOCKS), dim3(256), st,
+                            (const __nv_bfloat16*)x, n, part)
+               : launch_pdl(mean_partial_kernel<float>, dim3(MEAN_BLOCKS), dim3(256), st,
+                            (const float*)x, n, part);
+  if (rc) return rc;
+  SCMOE_LAUNCH_CHECK();
+  rc = launch_pdl(mean_final_kernel, dim3(1), dim3(512), st, (const float*)part, n, out);
+  if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
 }

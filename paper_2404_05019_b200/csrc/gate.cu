@@ -816,6 +816,12 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
         __nanosleep(64);
         if (clock64() - t0 > (40LL << 30)) __trap();   // ~20 s: never hang the GPU
       }
+      // the last CTA past the wait leaves both words zero for the next launch
+      // (a caller-kept sync state then needs no memset node per launch)
+      if (atomicAdd(ctrs + 3, 1u) == gridDim.x - 1) {
+        atomicExch(ctrs + 2, 0u);
+        atomicExch(ctrs + 3, 0u);
+      }
       gate_trace(3);
     }
     consumer_sync<RT, 2>();
@@ -1011,14 +1017,16 @@ template <int NT>
 int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* presplit,
                    const int32_t* excl, int T_, int d, int N, int k, int quota, float* logits,
                    int32_t* idx, float* w, int32_t* slots, uint8_t* drop, int32_t* counts,
-                   float* prob_sum, uint8_t* ws, cudaStream_t st) {
+                   float* prob_sum, uint8_t* ws, uint32_t* sync, cudaStream_t st) {
   using C = GateTC<NT>;
   const int n16 = (T_ + 15) / 16;
   const int ngrp = (d + 63) / 64;
   // persistent and fully resident (one CTA per SM): the in-kernel wait for
   // every CTA's counts cannot deadlock
   const int grid = min(min(n16, num_sms()), 1024);
-  uint32_t* ctrs = reinterpret_cast<uint32_t*>(ws);
+  // sync: caller-kept words (zero before the first launch, left zero by
+  // every launch); else the workspace's, zeroed here (a memset node)
+  uint32_t* ctrs = sync ? sync - 2 : reinterpret_cast<uint32_t*>(ws);
   uint32_t* cta_cnt = reinterpret_cast<uint32_t*>(ws + CTR_BYTES);
   float* cta_psum = reinterpret_cast<float*>(ws + CTR_BYTES + (size_t)grid * N * 4);
   const uint8_t* blob = (const uint8_t*)presplit;
@@ -1029,8 +1037,9 @@ int launch_gate_tc(const void* x, long long ld_x, const float* wg, const void* p
     SCMOE_LAUNCH_CHECK();
     blob = b;
   }
-  // publish counter of the in-kernel prefix (a memset node in a graph)
-  SCMOE_CUDA_TRY(cudaMemsetAsync(ctrs, 0, 16, st));
+  // publish counter of the in-kernel prefix (a memset node in a graph:
+  // ~8 us of idle GPU around it in a replay)
+  if (!sync) SCMOE_CUDA_TRY(cudaMemsetAsync(ctrs, 0, 16, st));
   static bool attr_set = false;   // once per instantiation, never inside a graph capture
   if (!attr_set) {
     SCMOE_CUDA_TRY(cudaFuncSetAttribute(gate_topk_tc_kernel<NT>,
@@ -1133,7 +1142,7 @@ int gate_topk_impl(const void* x, int x_dtype, long long ld_x, const float* w_ga
                    const int32_t* exclude, int n_tokens, int d_model, int n_experts, int k,
                    int quota, float* logits, int32_t* indices, float* weights, int32_t* slots,
                    uint8_t* dropped, int32_t* counts, float* prob_sum, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+                   size_t workspace_bytes, uint32_t* sync, void* stream) {
   SCMOE_CHECK_ARG(n_tokens >= 1, "n_tokens must be >= 1 (got %d)", n_tokens);
   SCMOE_CHECK_ARG(n_experts >= 1 && n_experts <= SCMOE_MAX_EXPERTS, "n_experts=%d out of [1,%d]",
                   n_experts, SCMOE_MAX_EXPERTS);
@@ -1160,10 +1169,10 @@ int gate_topk_impl(const void* x, int x_dtype, long long ld_x, const float* w_ga
         n_experts <= 8
             ? launch_gate_tc<1>(x, ld_x, w_gate_t, w_split, exclude, n_tokens, d_model, n_experts,
                                 k, quota, logits, indices, weights, slots, dropped, counts,
-                                prob_sum, ws, st)
+                                prob_sum, ws, sync, st)
             : launch_gate_tc<2>(x, ld_x, w_gate_t, w_split, exclude, n_tokens, d_model, n_experts,
                                 k, quota, logits, indices, weights, slots, dropped, counts,
-                                prob_sum, ws, st);
+                                prob_sum, ws, sync, st);
     if (rc != SCMOE_ERR_UNSUPPORTED) return rc;   // very large T: the FMA kernel below
   }
   if (x_dtype == SCMOE_BF16)
@@ -1187,6 +1196,21 @@ extern "C" int scmoe_gate_topk(const void* x, int x_dtype, long long ld_x,
   return scmoe::gate_topk_impl(x, x_dtype, ld_x, w_gate_t, nullptr, w_noise_t, eps, exclude,
                                n_tokens, d_model, n_experts, k, quota, logits, indices, weights,
                                slots, dropped, counts, prob_sum, workspace, workspace_bytes,
+                               nullptr, stream);
+}
+
+extern "C" int scmoe_gate_topk_ex(const void* x, int x_dtype, long long ld_x,
+                                  const float* w_gate_t, const void* w_split,
+                                  const float* w_noise_t, const float* eps,
+                                  const int32_t* exclude, int n_tokens, int d_model,
+                                  int n_experts, int k, int quota, float* logits,
+                                  int32_t* indices, float* weights, int32_t* slots,
+                                  uint8_t* dropped, int32_t* counts, float* prob_sum,
+                                  void* workspace, size_t workspace_bytes, uint32_t* sync,
+                                  void* stream) {
+  return scmoe::gate_topk_impl(x, x_dtype, ld_x, w_gate_t, w_split, w_noise_t, eps, exclude,
+                               n_tokens, d_model, n_experts, k, quota, logits, indices, weights,
+                               slots, dropped, counts, prob_sum, workspace, workspace_bytes, sync,
                                stream);
 }
 
@@ -1229,7 +1253,7 @@ extern "C" int scmoe_gate_topk_presplit(const void* x, int x_dtype, long long ld
   return scmoe::gate_topk_impl(x, x_dtype, ld_x, w_gate_t, w_split, nullptr, nullptr, exclude,
                                n_tokens, d_model, n_experts, k, quota, logits, indices, weights,
                                slots, dropped, counts, prob_sum, workspace, workspace_bytes,
-                               stream);
+                               nullptr, stream);
 }
 
 #ifdef SCMOE_GATE_TRACE

@@ -58,9 +58,11 @@ def gate_split_weights(w_gate_t: torch.Tensor, stream=None) -> Optional[torch.Te
 def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
               w_noise_t: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
               exclude: Optional[torch.Tensor] = None, w_split: Optional[torch.Tensor] = None,
-              stream=None) -> GateOut:
+              sync: Optional[torch.Tensor] = None, stream=None) -> GateOut:
     """K1/K1b: logits, top-k, masked-softmax weights and capacity slots.
-    `w_split` (from gate_split_weights) skips the per-call weight split."""
+    `w_split` (from gate_split_weights) skips the per-call weight split;
+    `sync` (>= 2 int32, zeroed once, left zero by every call; one stream per
+    sync) replaces the per-call counter memset."""
     ensure_device(x)
     if x.dim() != 2 or x.stride(1) != 1:
         raise ValueError("x must be a row-major (T, d) matrix")
@@ -82,18 +84,16 @@ def gate_topk(x: torch.Tensor, w_gate_t: torch.Tensor, k: int, quota: int,
         eps = _c(eps.to(torch.float32), "eps")
     if exclude is not None:
         exclude = _c(exclude.to(torch.int32).reshape(-1), "exclude")
-    if w_split is not None and w_noise_t is None:
-        check(lib().scmoe_gate_topk_presplit(
-            ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")), ptr(w_split),
-            ptr(exclude), T, d, N, k, quota,
-            ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
-            ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
-    else:
-        check(lib().scmoe_gate_topk(
-            ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")),
-            ptr(w_noise_t), ptr(eps), ptr(exclude), T, d, N, k, quota,
-            ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
-            ptr(prob_sum), ptr(ws), ws_bytes, stream_ptr(stream)))
+    if sync is not None and (sync.dtype != torch.int32 or sync.numel() < 2 or
+                             sync.device != x.device):
+        raise ValueError("sync must be >= 2 int32 words on the tokens' device")
+    if w_noise_t is not None:
+        w_split = None
+    check(lib().scmoe_gate_topk_ex(
+        ptr(x), dtype_code(x.dtype), x.stride(0), ptr(_c(w_gate_t, "w_gate_t")), ptr(w_split),
+        ptr(w_noise_t), ptr(eps), ptr(exclude), T, d, N, k, quota,
+        ptr(logits), ptr(indices), ptr(weights), ptr(slots), ptr(dropped), ptr(counts),
+        ptr(prob_sum), ptr(ws), ws_bytes, ptr(sync), stream_ptr(stream)))
     return GateOut(logits, indices, weights, slots, dropped, counts, prob_sum, quota)
 
 
@@ -506,6 +506,28 @@ def gate_aux_loss(counts: torch.Tensor, prob_sum: torch.Tensor, n_tokens: int, k
     check(lib().scmoe_gate_aux_loss(ptr(_c(counts, "counts")), ptr(_c(prob_sum, "prob_sum")),
                                     n_tokens, counts.shape[0], k, ptr(aux), stream_ptr(stream)))
     return aux
+
+
+def mean_f32(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """mean of every element of x (bf16 / fp32) accumulated in fp32, as a
+    0-dim fp32 tensor; deterministic, two launches, no memset."""
+    ensure_device(x)
+    out = torch.empty((), device=x.device, dtype=torch.float32)
+    ws_bytes = lib().scmoe_mean_workspace_bytes()
+    ws = torch.empty(ws_bytes, device=x.device, dtype=torch.uint8)
+    check(lib().scmoe_mean(ptr(_c(x, "x")), dtype_code(x.dtype), x.numel(), ptr(out), ptr(ws),
+                           ws_bytes, stream_ptr(stream)))
+    return out
+
+
+def fill_div(out: torch.Tensor, src: torch.Tensor, div: float, stream=None) -> torch.Tensor:
+    """out[:] = (src / div) in out's dtype, src a one-element fp32 device tensor."""
+    ensure_device(out)
+    if src.dtype != torch.float32 or src.numel() != 1:
+        raise ValueError("src must be a one-element fp32 tensor")
+    check(lib().scmoe_fill_div(ptr(_c(out, "out")), dtype_code(out.dtype), out.numel(),
+                               ptr(_c(src, "src")), float(div), stream_ptr(stream)))
+    return out
 
 
 def grouped_colsum2(x0: torch.Tensor, x1: torch.Tensor, group_rows: Optional[torch.Tensor] = None,

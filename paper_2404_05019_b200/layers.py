@@ -189,6 +189,16 @@ class Top1Gate(nn.Module):
             self._split_key = key
         return self._split
 
+    def _sync_words(self, device) -> torch.Tensor:
+        """The tensor-core gate's cross-CTA counter, kept per gate (zeroed
+        once here, left zero by every launch): no memset node per call.  A
+        gate's launches never overlap in time (one stream per forward)."""
+        w = getattr(self, "_sync", None)
+        if w is None or w.device != device:
+            w = torch.zeros(4, device=device, dtype=torch.int32)
+            self._sync = w
+        return w
+
     def forward(self, x_src: torch.Tensor, eps: Optional[torch.Tensor] = None,
                 generator: Optional[torch.Generator] = None, replay: Optional[MoEReplay] = None,
                 stream=None) -> GateDecision:
@@ -205,7 +215,8 @@ class Top1Gate(nn.Module):
         g = K.gate_topk(x_src, self.w_gate_t, self.k, quota,
                         w_noise_t=self.w_noise_t if self.noise_enabled else None,
                         eps=eps if self.noise_enabled else None,
-                        w_split=self.presplit(x_src), stream=stream)
+                        w_split=self.presplit(x_src), sync=self._sync_words(x_src.device),
+                        stream=stream)
         # uint8 0/1 flags reinterpreted as bool: no conversion kernel
         dec = GateDecision(g.logits, g.indices, g.weights, g.dropped.view(torch.bool), g.slots,
                            g.counts, g.prob_sum, quota, quota,

@@ -281,7 +281,6 @@ class CombineFn(torch.autograd.Function):
         dout = dout.contiguous()
         t, k = indices.shape
         n_exp = y.shape[0]
-        kept_sel = slots < capacity
         d_se = d_xcur = d_wcg = None
         c_rt = None
         if mode == "direct_add":
@@ -311,7 +310,7 @@ class CombineFn(torch.autograd.Function):
             # <d routed_t, y[e_j, slot_j]> for kept selections (c_rt folded in)
             gathered = y[indices.long().clamp(max=n_exp - 1), slots.long().clamp(max=capacity - 1)]
             dro = dout.float() if c_rt is None else dout.float() * c_rt[:, None]
-            d_weights = (gathered.float() * dro[:, None, :]).sum(-1) * kept_sel
+            d_weights = (gathered.float() * dro[:, None, :]).sum(-1) * (slots < capacity)
         d_res = dout if has_res else None
         if has_res and ctx.link is not None:
             _park(ctx.link, dout)
@@ -373,12 +372,16 @@ class MeanLossFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, out):
         ctx.shape, ctx.dtype, ctx.n = out.shape, out.dtype, out.numel()
+        if out.dtype in (torch.bfloat16, torch.float32) and out.is_contiguous():
+            return K.mean_f32(out)
         return out.mean(dtype=torch.float32)
 
     @staticmethod
     def backward(ctx, g):
-        v = (g / ctx.n).to(ctx.dtype)
-        return torch.empty(ctx.shape, device=g.device, dtype=ctx.dtype).fill_(v)
+        out = torch.empty(ctx.shape, device=g.device, dtype=ctx.dtype)
+        if g.dtype == torch.float32 and ctx.dtype in (torch.bfloat16, torch.float32):
+            return K.fill_div(out, g.contiguous(), float(ctx.n))   # = (g / n).to(dtype), one pass
+        return out.fill_((g / ctx.n).to(ctx.dtype))
 
 
 def mean_loss(out: torch.Tensor) -> torch.Tensor:

@@ -206,4 +206,58 @@ def test_mean_loss_gradient():
     x2 = x.detach().clone().requires_grad_(True)
     l2 = x2.mean(dtype=torch.float32)
     l2.backward()
-    assert torch.equal(l, l2) and torch.equal(x.grad, x2.grad)
+    # the loss is our deterministic two-pass fp32 mean (another summation
+    # order than torch's); the gradient fill is bit-identical
+    torch.testing.assert_close(l, l2, rtol=1e-5, atol=1e-7)
+    assert torch.equal(x.grad, x2.grad)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n", [1, 7, 8, 1000, 18432 * 384 + 3])
+def test_fill_div_matches_torch(dtype, n):
+    """The mean-loss backward's constant gradient: bit-identical to
+    (g / n).to(dtype) broadcast by torch."""
+    g = torch.tensor(0.7310585, device="cuda", dtype=torch.float32)
+    out = torch.empty(n, device="cuda", dtype=dtype)
+    K.fill_div(out, g, float(n))
+    ref = torch.empty(n, device="cuda", dtype=dtype).fill_((g / n).to(dtype))
+    assert torch.equal(out, ref)
+
+
+def test_gate_aux_loss_matches_formula():
+    g = torch.Generator(device="cuda").manual_seed(4)
+    counts = torch.randint(0, 500, (8,), device="cuda", generator=g, dtype=torch.int32)
+    ps = torch.rand(8, device="cuda", generator=g) * 100
+    T, k = 1000, 2
+    aux = K.gate_aux_loss(counts, ps, T, k)
+    ref = 8 * ((counts.double() / (T * k)) * (ps.double() / T)).sum()
+    torch.testing.assert_close(aux.double(), ref, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n", [1, 5, 300, 18432 * 384, 1000003])
+def test_mean_f32(dtype, n):
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(n, device="cuda", generator=g).to(dtype)
+    m = K.mean_f32(x)
+    torch.testing.assert_close(m.double(), x.double().mean(), rtol=1e-5, atol=1e-6)
+    assert torch.equal(m, K.mean_f32(x))          # deterministic
+    off = K.mean_f32(x[1:]) if n > 1 else None   # unaligned start: the scalar path
+    if off is not None:
+        torch.testing.assert_close(off.double(), x[1:].double().mean(), rtol=1e-5, atol=1e-6)
+
+
+def test_gate_sync_words_left_zero():
+    """scmoe_gate_topk_ex with caller-kept sync words: identical decisions to
+    the per-call memset path, words zero after every launch."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(5000, 256, device="cuda", generator=g).bfloat16()
+    w = torch.randn(8, 256, device="cuda", generator=g) / 16
+    quota = K.expert_quota(1.0, 5000, 2, 8)
+    sync = torch.zeros(4, device="cuda", dtype=torch.int32)
+    a = K.gate_topk(x, w, 2, quota)
+    for _ in range(3):
+        b = K.gate_topk(x, w, 2, quota, sync=sync)
+        assert torch.equal(a.slots, b.slots) and torch.equal(a.indices, b.indices)
+        assert torch.equal(a.counts, b.counts) and torch.equal(a.prob_sum, b.prob_sum)
+        assert int(sync.abs().sum()) == 0
