@@ -81,31 +81,35 @@ struct ColsumSet {
   const void* x[2];
   int cols[2];
   int vpb[2];          // column vectors per pass-1 tile
-  int tile0[3];        // pass-1 column-tile ranges
+  int tiles[2];        // pass-1 column tiles
+  int stripes[2];      // row stripes (per group), sized for equal bytes per block
+  int stripe_rows[2];
+  int pblk0[3];        // pass-1 block ranges (tiles x stripes per tensor)
   int blk0[3];         // pass-2 32-column block ranges
-  float* part[2];      // [G][n_stripes][cols]
+  float* part[2];      // [G][stripes][cols]
   float* out[2];       // [G][cols]
 };
 
 template <typename T>
 __global__ void __launch_bounds__(COLSUM_BLOCK)
-colsum_partial_kernel(ColsumSet cs, int cap, const int32_t* __restrict__ group_rows, int rows_clip,
-                      int stripe_rows, int n_stripes) {
+colsum_partial_kernel(ColsumSet cs, int cap, const int32_t* __restrict__ group_rows, int rows_clip) {
   constexpr int VEC = Vec16<T>::N;
   constexpr int U = 8;
   __shared__ float red[COLSUM_BLOCK][VEC + 1];
   // programmatic dependent launch: nothing global is read before the
   // producer of x completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int ti = blockIdx.x >= cs.tile0[1] ? 1 : 0;
+  const int ti = (int)blockIdx.x >= cs.pblk0[1] ? 1 : 0;
   const T* x = (const T*)cs.x[ti];
   const int cols = cs.cols[ti];
   const int vecs = cols / VEC;
   const int vpb = cs.vpb[ti];                              // vectors per column tile
   const int lanes = blockDim.x / vpb;
   const int v = threadIdx.x % vpb, lane = threadIdx.x / vpb;
-  const int g = blockIdx.z, stripe = blockIdx.y;
-  const int cv = (blockIdx.x - cs.tile0[ti]) * vpb + v;    // my column vector
+  const int local = blockIdx.x - cs.pblk0[ti];
+  const int g = blockIdx.z, stripe = local / cs.tiles[ti];
+  const int n_stripes = cs.stripes[ti], stripe_rows = cs.stripe_rows[ti];
+  const int cv = (local % cs.tiles[ti]) * vpb + v;         // my column vector
   const bool active = lane < lanes && cv < vecs;
   const int rows = group_rows ? max(0, min(group_rows[g], rows_clip)) : cap;
   const int r0 = stripe * stripe_rows, r1 = min(rows, r0 + stripe_rows);
@@ -153,10 +157,11 @@ colsum_partial_kernel(ColsumSet cs, int cap, const int32_t* __restrict__ group_r
 
 // block (32 columns x 32 stripe lanes): lane y sums stripes y, y+32, ...,
 // then the 32 lane sums are added in a fixed order
-__global__ void colsum_final_kernel(ColsumSet cs, int n_stripes) {
+__global__ void colsum_final_kernel(ColsumSet cs) {
   __shared__ float red[32][33];
   asm volatile("griddepcontrol.wait;" ::: "memory");     // pass 1 complete
-  const int ti = blockIdx.x >= cs.blk0[1] ? 1 : 0;
+  const int ti = (int)blockIdx.x >= cs.blk0[1] ? 1 : 0;
+  const int n_stripes = cs.stripes[ti];
   const int cols = cs.cols[ti];
   const int g = blockIdx.y;
   const int c = (blockIdx.x - cs.blk0[ti]) * 32 + threadIdx.x;
@@ -305,26 +310,42 @@ int launch_pdl(K kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
   return SCMOE_OK;
 }
 
-// stripes for a set: ~6 blocks per SM over (column tiles of both x groups)
-int colsum_set_stripes(int num_groups, int group_cap, int col_tiles) {
-  int st = (6 * num_sms() + col_tiles * num_groups - 1) / (col_tiles * num_groups);
-  return max(1, min(st, (group_cap + 7) / 8));
-}
-
 int colsum_tiles(int cols, int vec) {
   const int vecs = (cols + vec - 1) / vec;
   return (vecs + COLSUM_THREADS - 1) / COLSUM_THREADS;
 }
 
+// Row stripes per group for each matrix: ~6 pass-1 blocks per SM in total,
+// shared out in proportion to each matrix's bytes so every block reads about
+// the same amount (short, latency-bound row loops with many blocks in
+// flight; fewer, longer stripes measured slower; one stripe count for both
+// starved the wide matrix)
+void colsum_set_stripes(int num_groups, int group_cap, const int* cols, int n, int vec,
+                        int* stripes) {
+  long long tot = 0;
+  for (int i = 0; i < n; ++i) tot += cols[i];
+  const double target = 6.0 * num_sms();
+  for (int i = 0; i < n; ++i) {
+    const double share = target * (double)cols[i] / (double)tot;
+    int st = (int)(share / ((double)colsum_tiles(cols[i], vec) * num_groups) + 0.5);
+    stripes[i] = max(1, min(st, (group_cap + 7) / 8));
+  }
+}
+
 size_t colsum2_ws_bytes(int num_groups, int group_cap, int cols0, int cols1) {
   if (num_groups < 1 || group_cap < 1 || cols0 < 1 || cols1 < 0) return 0;
   // large enough for either vector width (bf16 8, fp32 4 per 16 bytes)
-  size_t st = 0;
+  const int cl[2] = {cols0, cols1};
+  const int n = cols1 ? 2 : 1;
+  size_t best = 0;
   for (int vec : {8, 4}) {
-    const int ct = colsum_tiles(cols0, vec) + (cols1 ? colsum_tiles(cols1, vec) : 0);
-    st = std::max(st, (size_t)colsum_set_stripes(num_groups, group_cap, ct));
+    int st[2] = {0, 0};
+    colsum_set_stripes(num_groups, group_cap, cl, n, vec, st);
+    size_t b = 0;
+    for (int i = 0; i < n; ++i) b += (size_t)st[i] * num_groups * cl[i] * sizeof(float);
+    best = std::max(best, b);
   }
-  return st * (size_t)num_groups * (size_t)(cols0 + cols1) * sizeof(float);
+  return best;
 }
 
 int colsum2_impl(const void* x0, const void* x1, int dtype, int num_groups, int group_cap,
@@ -345,31 +366,32 @@ int colsum2_impl(const void* x0, const void* x1, int dtype, int num_groups, int 
   const void* xs[2] = {x0, x1};
   const int cl[2] = {cols0, cols1};
   float* outs[2] = {out0, out1};
-  cs.tile0[0] = cs.blk0[0] = 0;
+  colsum_set_stripes(num_groups, group_cap, cl, n, vec, cs.stripes);
+  cs.pblk0[0] = cs.blk0[0] = 0;
+  float* part = (float*)workspace;
   for (int i = 0; i < 2; ++i) {
     cs.x[i] = xs[i];
     cs.cols[i] = cl[i];
     cs.out[i] = outs[i];
     const int vecs = cl[i] / vec;
     cs.vpb[i] = std::max(1, std::min(vecs, COLSUM_THREADS));
-    const int ct = i < n ? (vecs + cs.vpb[i] - 1) / cs.vpb[i] : 0;
-    cs.tile0[i + 1] = cs.tile0[i] + ct;
+    cs.tiles[i] = i < n ? (vecs + cs.vpb[i] - 1) / cs.vpb[i] : 0;
+    if (i >= n) cs.stripes[i] = 1;
+    cs.stripe_rows[i] = (group_cap + cs.stripes[i] - 1) / cs.stripes[i];
+    cs.pblk0[i + 1] = cs.pblk0[i] + cs.tiles[i] * cs.stripes[i];
     cs.blk0[i + 1] = cs.blk0[i] + (i < n ? (cl[i] + 31) / 32 : 0);
+    cs.part[i] = part;
+    if (i < n) part += (size_t)num_groups * cs.stripes[i] * cl[i];
   }
-  const int n_stripes = colsum_set_stripes(num_groups, group_cap, cs.tile0[2]);
-  const int stripe_rows = (group_cap + n_stripes - 1) / n_stripes;
-  cs.part[0] = (float*)workspace;
-  cs.part[1] = cs.part[0] + (size_t)num_groups * n_stripes * cols0;
-  dim3 grid(cs.tile0[2], n_stripes, num_groups);
+  dim3 grid(cs.pblk0[2], 1, num_groups);
   int rc = dtype == SCMOE_BF16
                ? launch_pdl(colsum_partial_kernel<__nv_bfloat16>, grid, dim3(COLSUM_BLOCK), st, cs,
-                            group_cap, group_rows, rows_clip, stripe_rows, n_stripes)
+                            group_cap, group_rows, rows_clip)
                : launch_pdl(colsum_partial_kernel<float>, grid, dim3(COLSUM_BLOCK), st, cs,
-                            group_cap, group_rows, rows_clip, stripe_rows, n_stripes);
+                            group_cap, group_rows, rows_clip);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
-  rc = launch_pdl(colsum_final_kernel, dim3(cs.blk0[2], num_groups), dim3(32, 32), st, cs,
-                  n_stripes);
+  rc = launch_pdl(colsum_final_kernel, dim3(cs.blk0[2], num_groups), dim3(32, 32), st, cs);
   if (rc) return rc;
   SCMOE_LAUNCH_CHECK();
   return SCMOE_OK;
