@@ -597,6 +597,39 @@ __device__ __forceinline__ void epilogue_chunk_res(uint32_t (&r)[32], const floa
 }
 
 // fp32 wgrad partial: 32 columns of one output row
+// fp32 split-K partials of 32 columns through the warp's staging buffer in
+// two 16-column halves: every store instruction writes 8 rows x 64 B (whole
+// sectors) instead of 32 rows x 16 B — row-per-thread stores left the
+// 1-tile-per-CTA weight gradients epilogue-bound (ncu: tensor pipe 33-42%
+// with the mainloop at full MMA rate)
+__device__ __forceinline__ void stage_flush_f32(const uint4* __restrict__ stg, int lane,
+                                                float* row0, long long ld, uint32_t row_mask,
+                                                int ncols) {
+  __syncwarp();                       // every lane's row is staged
+  const int j = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = (lane >> 2) + 8 * i;
+    const uint4 v = lds128(smem_u32(stg + rr * 4 + (j ^ ((rr >> 1) & 3))));
+    if (((row_mask >> rr) & 1u) && j * 4 < ncols) st_v4(row0 + rr * ld + j * 4, v);
+  }
+}
+__device__ __forceinline__ void epilogue_chunk_f32_staged(const uint32_t (&r)[32], bool zero,
+                                                          uint4* __restrict__ stg, int lane,
+                                                          float* row0, long long ld,
+                                                          uint32_t row_mask, int ncols) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    __syncwarp();                     // the previous flush's reads are done
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      stage_put(stg, lane, u,
+                zero ? make_uint4(0, 0, 0, 0)
+                     : make_uint4(r[16 * h + 4 * u], r[16 * h + 4 * u + 1], r[16 * h + 4 * u + 2],
+                                  r[16 * h + 4 * u + 3]));
+    stage_flush_f32(stg, lane, row0 + 16 * h, ld, row_mask, ncols - 16 * h);
+  }
+}
 __device__ __forceinline__ void epilogue_chunk_f32(const Params& p, const uint32_t (&r)[32],
                                                    bool row_ok, bool zero, long long row_off,
                                                    int n) {
@@ -858,11 +891,13 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
       bool row_ok, pad_row = false;
       long long row_off;
       __nv_bfloat16* orow0 = nullptr;      // row row_w0 of the output / aux
+      float* frow0 = nullptr;              // wgrad: row row_w0 of this split's partial
       __nv_bfloat16* arow0 = nullptr;
       const float* brow = nullptr;
       if (WGRAD) {
         row_ok = row < p.m_out;
         row_off = (((long long)tc.s * p.n_wgroups + tc.g) * p.m_out + row) * p.N;
+        frow0 = p.out_f32 + (((long long)tc.s * p.n_wgroups + tc.g) * p.m_out + row_w0) * p.N;
       } else {
         const int rows = group_rows_of(p, tc.g);
         row_ok = row < rows;
@@ -992,7 +1027,10 @@ __global__ void __launch_bounds__(Threads<E>::value, 1)
         }
         const int n = tc.n0 + part * COLS_W + c * 32;
         if (WGRAD) {
-          epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
+          if (n < p.N && !(p.dbg & 16))
+            epilogue_chunk_f32_staged(cur, empty, stg, lane, frow0 + n, p.N, wmask, p.N - n);
+          else if (p.dbg & 16)
+            epilogue_chunk_f32(p, cur, row_ok, empty, row_off, n);
         } else if (fast && fast_gelu && n + 32 <= p.N) {
           // bias + GELU (+ the pre-activation store in training); plain bias
           // chunks of a partial tile take the general path below
@@ -1360,12 +1398,14 @@ int grouped_wgrad_bf16(const void* a, const void* b, void* out, void* ws, size_t
   SCMOE_CHECK_ARG(m_out % 8 == 0 && n_out % 8 == 0, "wgrad needs m_out, n_out multiples of 8");
   SCMOE_CHECK_ARG(aligned16(a) && aligned16(b) && aligned16(out) && aligned16(ws),
                   "wgrad operands must be 16-byte aligned");
-  const int sms = num_sms();
+  const int sms = gemm_sms();          // honours the SM budget (concurrent backward GEMMs)
   // Tile shape: 2-SM 256x256 when the outputs alone fill the CTA pairs
   // (configs[2]-size weights); small weights (configs[1]: 384 / 1152 / 1536
   // wide) run split-K on 1-SM 128x128 tiles with 4 accumulator stages — the
   // fastest of the four shapes on every configs[1] weight (scripts/ab_wgrad.py:
   // 546-610 TFLOP/s vs 458-591).
+  // (2-SM 256x256 for the configs[1] weights too: within +-3% of 1-SM
+  // 128x128 in interleaved A/B, scripts/ab_wgrad.py — not adopted)
   const long long tiles_big = (long long)n_wgroups * ((m_out + 255) / 256) * ((n_out + 255) / 256);
   const bool two = g_gemm_mode == 2 || (g_gemm_mode == 0 && tiles_big >= sms / 2);
   const int tile_m = two ? 256 : 128;

@@ -196,25 +196,41 @@ def set_gemm_mode(mode: int) -> None:
     check(lib().scmoe_set_gemm_mode(mode))
 
 
+_SM_BUDGET = [0]
+
+
 class gemm_sm_budget:
     """Context manager: persistent GEMMs launched inside use at most `sms`
-    SMs (None / 0 = all) — room for a concurrent exchange kernel."""
+    SMs (None / 0 = all) — room for a concurrent exchange kernel or a
+    concurrent GEMM.  Nested budgets take the smaller; the previous budget is
+    restored on exit."""
 
     def __init__(self, sms: Optional[int]):
         self.sms = int(sms or 0)
 
     def __enter__(self):
-        check(lib().scmoe_set_gemm_sm_budget(self.sms))
+        self.prev = _SM_BUDGET[0]
+        new = self.sms if not self.prev else (min(self.sms, self.prev) if self.sms else self.prev)
+        _SM_BUDGET[0] = new
+        check(lib().scmoe_set_gemm_sm_budget(new))
         return self
 
     def __exit__(self, *exc):
-        check(lib().scmoe_set_gemm_sm_budget(0))
+        _SM_BUDGET[0] = self.prev
+        check(lib().scmoe_set_gemm_sm_budget(self.prev))
         return False
 
 
 def set_gemm_epilogue_warps(e: int) -> None:
     """0 = auto (16 for small-K elementwise-heavy tiles), 8 or 16 forced."""
     check(lib().scmoe_set_gemm_epilogue_warps(e))
+
+
+def set_gemm_flags(flags: int) -> None:
+    """Experiment flags of the GEMM (A/B scripts): bit 0 row-per-thread
+    epilogue operand loads, bit 3 no programmatic dependent launch, bit 4
+    row-per-thread fp32 split-K partial stores."""
+    check(lib().scmoe_set_gemm_flags(flags))
 
 
 def set_gemm_tile_n(bn: int) -> None:

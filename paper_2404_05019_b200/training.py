@@ -53,6 +53,45 @@ def _take(link) -> Optional[torch.Tensor]:
     return item[1]
 
 
+# Backward concurrency: a layer's data-gradient GEMM and its weight-gradient
+# GEMM are independent.  With CONCURRENT_BWD the weight gradient runs on a
+# side stream beside the data gradient, each persistent GEMM on half of the
+# SMs (scmoe_set_gemm_sm_budget): every K = 384 GEMM of the configs[1] step
+# carries a ~5-8 us fixed cost (pipeline fill, one-tile epilogue, teardown,
+# scripts/wgrad_scaling.py) that the pair now pays side by side.
+CONCURRENT_BWD = True
+_SIDE = {}
+
+
+class _Side:
+    """Fork the current stream onto the device's side stream for `with`, with
+    the GEMM SM budget halved for launches issued inside; join() makes the
+    current stream wait for everything the side stream was given."""
+
+    def __init__(self, dev: torch.device):
+        self.main = torch.cuda.current_stream(dev)
+        st = _SIDE.get(dev.index)
+        if st is None:
+            st = _SIDE[dev.index] = torch.cuda.Stream(dev)
+        self.side = st
+        self.half = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+        self.outs = []
+
+    def fork(self):
+        self.side.wait_stream(self.main)
+
+    def on_side(self):
+        return torch.cuda.stream(self.side)
+
+    def keep(self, *ts):
+        self.outs.extend(t for t in ts if t is not None)
+
+    def join(self):
+        self.main.wait_stream(self.side)
+        for t in self.outs:                 # produced on the side stream, consumed on main
+            t.record_stream(self.main)
+
+
 def _wgrad_dtype(w: torch.Tensor) -> torch.dtype:
     """bf16 weights get their gradient straight from the split reduction."""
     return torch.bfloat16 if w.dtype == torch.bfloat16 else torch.float32
@@ -87,6 +126,19 @@ class LinearFn(torch.autograd.Function):
             res_grad = None
         else:
             res_grad = dy if ctx.has_res else None
+        both = ctx.needs_input_grad[0] and ctx.needs_input_grad[1]
+        sd = _Side(dy.device) if (CONCURRENT_BWD and both) else None
+        if sd is not None:
+            # dW on the side stream beside dx, half of the SMs each
+            sd.fork()
+            with K.gemm_sm_budget(sd.half):
+                with sd.on_side():
+                    dwt = _as_param_grad(K.grouped_wgrad(dy, x, out_dtype=_wgrad_dtype(wt)), wt)
+                extra = _take(link) if not ctx.has_res else None
+                dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1], residual=extra)
+            sd.keep(dwt)
+            sd.join()
+            return dx, dwt, res_grad, None
         if ctx.needs_input_grad[0]:
             extra = _take(link) if not ctx.has_res else None
             dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1], residual=extra)
@@ -164,27 +216,41 @@ class FFNFn(torch.autograd.Function):
         grouped = group_rows is not None
         if grouped:
             K.zero_tails(dy3, group_rows, rows_clip)
-        if SPLIT_GELU:
-            # z holds gelu'(z) here (saved by the forward): dz = (dy W2) *
-            # gelu'(z) in the data-gradient GEMM's epilogue, zero tails
-            dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_MUL_AUX,
-                                   group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
-        else:
-            dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=_lib.EPI_GELU_BWD,
-                                   group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+        epi = _lib.EPI_MUL_AUX if SPLIT_GELU else _lib.EPI_GELU_BWD
         fuse_res = has_res and ctx.res_is_x
         parked = _take(ctx.link)
         extra = dy3 if fuse_res else (parked.view(G, C, d) if parked is not None else None)
-        dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
-                               residual=extra)
-        dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
-                               out_dtype=_wgrad_dtype(w23))
-        dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows, rows_clip=rows_clip,
-                               out_dtype=_wgrad_dtype(w13))
-        # bias gradients: column sums over the valid rows (HBM-bound, 8 row
-        # loads in flight per thread), then the source groups of each weight
-        # group summed like the weight gradients
-        db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
+        sd = _Side(dy3.device) if CONCURRENT_BWD else None
+        if sd is not None:
+            sd.fork()
+        with K.gemm_sm_budget(sd.half if sd is not None else 0):
+            if sd is not None:
+                with sd.on_side():           # dW2 beside dz (both read dy)
+                    dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows,
+                                           rows_clip=rows_clip, out_dtype=_wgrad_dtype(w23))
+            # SPLIT_GELU: z holds gelu'(z) (saved by the forward): dz = (dy W2) *
+            # gelu'(z) in the data-gradient GEMM's epilogue, zero tails
+            dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=epi,
+                                   group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
+            if sd is not None:
+                sd.fork()                    # dz ready
+                with sd.on_side():           # dW1 and the bias gradients beside dx
+                    dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows,
+                                           rows_clip=rows_clip, out_dtype=_wgrad_dtype(w13))
+                    db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
+            dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
+                                   residual=extra)
+        if sd is not None:
+            sd.keep(dw2t, dw1t, db2_g, db1_g)
+            sd.join()
+        else:
+            dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows,
+                                   rows_clip=rows_clip, out_dtype=_wgrad_dtype(w23))
+            dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows,
+                                   rows_clip=rows_clip, out_dtype=_wgrad_dtype(w13))
+            # bias gradients: column sums over the valid rows, both matrices
+            # in one launch per pass
+            db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
         db2, db1 = _wsum(db2_g, W), _wsum(db1_g, W)
         return ((dx.view(C, d) if two_d else dx), dw1t.to(w13.dtype).view(w1_shape),
                 db1.view(b1_shape), dw2t.to(w23.dtype).view(w2_shape), db2.view(b2_shape),

@@ -14,14 +14,18 @@ res = {}
 for name, M, N in shapes:
     a = torch.randn(1, T, M, device="cuda").bfloat16()
     b = torch.randn(1, T, N, device="cuda").bfloat16()
-    def arm(mode, bn):
+    def arm(mode, bn, flags=0):
         def f():
             K.set_gemm_mode(mode)
             K.set_gemm_tile_n(bn)
+            K.set_gemm_flags(flags)
             K.grouped_wgrad(a, b, n_wgroups=1)
+            K.set_gemm_flags(0)
         return f
-    arms = {"auto": arm(0, 0), "1sm128": arm(1, 128), "1sm256": arm(1, 256), "2sm128": arm(2, 128),
-            "2sm256": arm(2, 256)}
+    # *_rowst: the row-per-thread fp32 partial stores (flag 16) instead of staged
+    arms = {"auto": arm(0, 0), "auto_rowst": arm(0, 0, 16), "1sm128": arm(1, 128),
+            "1sm256": arm(1, 256), "2sm128": arm(2, 128), "2sm256": arm(2, 256),
+            "2sm256_rowst": arm(2, 256, 16)}
     for _ in range(3):
         for f in arms.values(): f()
     for r in range(5):
