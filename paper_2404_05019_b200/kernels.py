@@ -210,7 +210,7 @@ class gemm_sm_budget:
 
     def __enter__(self):
         self.prev = _SM_BUDGET[0]
-        new = self.sms if not self.prev else (min(self.sms, self.prev) if self.sms else self.prev)
+        new = min(self.sms, self.prev) if (self.sms and self.prev) else (self.sms or self.prev)
         _SM_BUDGET[0] = new
         check(lib().scmoe_set_gemm_sm_budget(new))
         return self

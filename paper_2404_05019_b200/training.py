@@ -60,6 +60,10 @@ def _take(link) -> Optional[torch.Tensor]:
 # carries a ~5-8 us fixed cost (pipeline fill, one-tile epilogue, teardown,
 # scripts/wgrad_scaling.py) that the pair now pays side by side.
 CONCURRENT_BWD = True
+# SMs of the side (weight-gradient) / main (data-gradient) GEMMs while both
+# run, as fractions of the device's SMs (0 = no budget)
+BWD_SIDE_FRAC = 0.5
+BWD_MAIN_FRAC = 0.5
 _SIDE = {}
 
 
@@ -74,7 +78,9 @@ class _Side:
         if st is None:
             st = _SIDE[dev.index] = torch.cuda.Stream(dev)
         self.side = st
-        self.half = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+        n = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.side_sms = int(n * BWD_SIDE_FRAC)
+        self.main_sms = int(n * BWD_MAIN_FRAC)
         self.outs = []
 
     def fork(self):
@@ -131,8 +137,8 @@ class LinearFn(torch.autograd.Function):
         if sd is not None:
             # dW on the side stream beside dx, half of the SMs each
             sd.fork()
-            with K.gemm_sm_budget(sd.half):
-                with sd.on_side():
+            with K.gemm_sm_budget(sd.main_sms):
+                with sd.on_side(), K.gemm_sm_budget(sd.side_sms):
                     dwt = _as_param_grad(K.grouped_wgrad(dy, x, out_dtype=_wgrad_dtype(wt)), wt)
                 extra = _take(link) if not ctx.has_res else None
                 dx = K.grouped_gemm_ex(dy, wt, _KN, wt.shape[1], residual=extra)
@@ -223,9 +229,9 @@ class FFNFn(torch.autograd.Function):
         sd = _Side(dy3.device) if CONCURRENT_BWD else None
         if sd is not None:
             sd.fork()
-        with K.gemm_sm_budget(sd.half if sd is not None else 0):
+        with K.gemm_sm_budget(sd.main_sms if sd is not None else 0):
             if sd is not None:
-                with sd.on_side():           # dW2 beside dz (both read dy)
+                with sd.on_side(), K.gemm_sm_budget(sd.side_sms):   # dW2 beside dz (both read dy)
                     dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows,
                                            rows_clip=rows_clip, out_dtype=_wgrad_dtype(w23))
             # SPLIT_GELU: z holds gelu'(z) (saved by the forward): dz = (dy W2) *
@@ -234,7 +240,7 @@ class FFNFn(torch.autograd.Function):
                                    group_rows=group_rows, rows_clip=rows_clip, zero_tail=grouped)
             if sd is not None:
                 sd.fork()                    # dz ready
-                with sd.on_side():           # dW1 and the bias gradients beside dx
+                with sd.on_side(), K.gemm_sm_budget(sd.side_sms):   # dW1, bias grads beside dx
                     dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows,
                                            rows_clip=rows_clip, out_dtype=_wgrad_dtype(w13))
                     db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
