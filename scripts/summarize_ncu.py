@@ -44,6 +44,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_bytes.sum",
            "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_sector_hit_rate.pct",
            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_elapsed",
            "smsp__average_warp_latency_issue_stalled_long_scoreboard",
