@@ -262,3 +262,38 @@ def test_gate_backward_kernel(dtype, N, k, noise):
     close(d_wg, g64.grad, 1e-4)
     if noise:
         close(d_wn, n64.grad, 1e-4)
+
+
+@pytest.mark.parametrize("n_exp", [1, 8])
+def test_concurrent_backward_matches_serial(n_exp):
+    """training.CONCURRENT_BWD (weight gradients on a side stream, half of the
+    SMs per GEMM) gives the serial backward's gradients: same kernels, only
+    the split-K split count of the weight gradients changes with the SM
+    budget (fp32 partials, a different summation order), inside a CUDA graph
+    too (the side stream forks from and joins the capture stream)."""
+    from paper_2404_05019_b200 import training as TR
+    from paper_2404_05019_b200.runtime import CapturedStep
+    T, d, h = 2304, 384, 1536
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    grads = {}
+    old = TR.CONCURRENT_BWD
+    try:
+        for conc in (False, True):
+            TR.CONCURRENT_BWD = conc
+            blk = P.ScMoEBlockPair(d, h, n_exp, variant="scmoe", shortcut_pos="pos2", n_heads=12,
+                                   seq_len=144, capacity_factor=1.25, dtype=torch.bfloat16,
+                                   generator=torch.Generator(device="cuda").manual_seed(12))
+            blk.requires_grad_(True)
+            step = CapturedStep(lambda xx, b=blk: b.train_step(xx, lr=0.0), [x], warmup=1)
+            step.replay()
+            torch.cuda.synchronize()
+            grads[conc] = {n: p.grad.detach().float().clone()
+                           for n, p in blk.named_parameters() if p.grad is not None}
+    finally:
+        TR.CONCURRENT_BWD = old
+    assert grads[False].keys() == grads[True].keys() and len(grads[True]) > 10
+    for n in grads[True]:
+        a, b = grads[False][n], grads[True][n]
+        scale = a.abs().max().clamp_min(1e-6)
+        assert float((a - b).abs().max() / scale) < 2e-2, n
