@@ -62,6 +62,9 @@ def _take(link) -> Optional[torch.Tensor]:
 CONCURRENT_BWD = True
 # SMs of the side (weight-gradient) / main (data-gradient) GEMMs while both
 # run, as fractions of the device's SMs (0 = no budget)
+# concurrent backward: db2 (column sums of dy) beside the dz GEMM with dW2,
+# db1 beside the dx GEMM with dW1 — balances the two streams' phases
+SPLIT_COLSUM = True
 BWD_SIDE_FRAC = 0.5
 BWD_MAIN_FRAC = 0.5
 _SIDE = {}
@@ -231,9 +234,11 @@ class FFNFn(torch.autograd.Function):
             sd.fork()
         with K.gemm_sm_budget(sd.main_sms if sd is not None else 0):
             if sd is not None:
-                with sd.on_side(), K.gemm_sm_budget(sd.side_sms):   # dW2 beside dz (both read dy)
+                with sd.on_side(), K.gemm_sm_budget(sd.side_sms):   # dW2, db2 beside dz (read dy)
                     dw2t = K.grouped_wgrad(dy3, hid, n_wgroups=W, group_rows=group_rows,
                                            rows_clip=rows_clip, out_dtype=_wgrad_dtype(w23))
+                    if SPLIT_COLSUM:
+                        db2_g = K.grouped_colsum(dy3, group_rows, rows_clip)
             # SPLIT_GELU: z holds gelu'(z) (saved by the forward): dz = (dy W2) *
             # gelu'(z) in the data-gradient GEMM's epilogue, zero tails
             dz = K.grouped_gemm_ex(dy3, w23, _KN, h, aux_in=z, epilogue=epi,
@@ -243,7 +248,10 @@ class FFNFn(torch.autograd.Function):
                 with sd.on_side(), K.gemm_sm_budget(sd.side_sms):   # dW1, bias grads beside dx
                     dw1t = K.grouped_wgrad(dz, x3, n_wgroups=W, group_rows=group_rows,
                                            rows_clip=rows_clip, out_dtype=_wgrad_dtype(w13))
-                    db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
+                    if SPLIT_COLSUM:
+                        db1_g = K.grouped_colsum(dz, group_rows, rows_clip)
+                    else:
+                        db2_g, db1_g = K.grouped_colsum2(dy3, dz, group_rows, rows_clip)
             dx = K.grouped_gemm_ex(dz, w13, _KN, d, group_rows=group_rows, rows_clip=rows_clip,
                                    residual=extra)
         if sd is not None:
