@@ -1160,6 +1160,7 @@ def run_ours(args):
                    "ep_backend": args.ep_backend if group is not None else None,
                    "p2p_ctas": args.p2p_ctas if group is not None else None,
                    "window_sm_budget": (not args.no_sm_budget) if group is not None else None,
+                   "routed_stream": (sc.routed_stream_infer if group is None else None),
                    "ep_note": ep_note,
                    "l2": "working set > L2 (~1 GB weights+activations per step), no flush"},
         "speedup_vs_top2": med["t2"] / med["sc"] if "t2" in med else None,

@@ -230,6 +230,15 @@ class ScMoEBlockPair(nn.Module):
         self.ep_backend, self.p2p_ctas, self.p2p_return = ep_backend, p2p_ctas, p2p_return
         # reserve p2p_ctas SMs for the exchange kernels during the window
         self.overlap_sm_budget = True
+        # one GPU: the routed ops (gate, dispatch, expert FFN) on a side stream
+        # beside the window ops — the shortcut makes them independent until
+        # the shared expert's fused combine, so at N = 1 the two streams'
+        # persistent GEMMs fill each other's wave tails (no exchange to hide).
+        # Inference: on; True joins at the shared expert (fused combine),
+        # "decode" at the combine (unfused) — measured slower.  Training:
+        # routed_stream_train (experiment)
+        self.routed_stream_infer = True
+        self.routed_stream_train = False
         self._xchg = None
         if variant not in VARIANTS:
             raise ConfigError(f"unknown variant {variant!r}")
@@ -616,6 +625,7 @@ class ScMoEBlockPair(nn.Module):
         def shared():
             dec = env.get("dec")
             if ("y" in env and not train and not use_ep and chunks == 1 and off is None
+                    and not env.get("no_fuse")
                     and self.variant in ("scmoe", "shared")
                     and moe.shared.can_fuse_combine(env["x_cur"], dec, moe.combine_mode)):
                 # the routed rows are ready: the combine (+ the block residual)
@@ -682,7 +692,39 @@ class ScMoEBlockPair(nn.Module):
         # the exchange runs concurrently instead of queueing behind them
         budget = self._window_sm_budget() if (use_ep and not train and (chunks == 1 or p2p)) else 0
         in_flight = False
-        for name in self.order():
+        order = self.order()
+        # (a per-op recorder — calibration, op timings — gets the serial order:
+        # its events time each op alone)
+        if ((self.routed_stream_train if train else self.routed_stream_infer) and not use_ep
+                and chunks == 1 and off is None and self.variant == "scmoe" and recorder is None):
+            side = self.comm_stream()
+            forked = False
+            join_at = ("decode",) if self.routed_stream_infer == "decode" else ("shared", "decode")
+            if self.routed_stream_infer == "decode":
+                env["no_fuse"] = True
+            for name in order:
+                if name in ("gate", "encode", "expert"):
+                    if not forked:
+                        side.wait_stream(st)
+                        forked = True
+                    with rec.op(name, "compute", side), torch.cuda.stream(side):
+                        ops[name]()
+                    continue
+                if name in join_at and forked:
+                    st.wait_stream(side)          # the fused combine reads the routed rows
+                    forked = False
+                    for key in ("y", "buf", "w", "aux", "kept"):
+                        t = env.get(key)
+                        if isinstance(t, torch.Tensor):
+                            t.record_stream(st)
+                    dec = env["dec"]
+                    for t in (dec.logits, dec.indices, dec.weights, dec.dropped, dec.slots,
+                              dec.counts, dec.prob_sum):
+                        t.record_stream(st)
+                with rec.op(name, "compute", st):
+                    ops[name]()
+            order = []
+        for name in order:
             if name == "expert":   # NCCL combine / push return run behind the expert
                 in_flight = (not p2p) or self.p2p_return == "push"
             with rec.op(name, "compute", st):

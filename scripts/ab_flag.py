@@ -2,6 +2,7 @@
 graph per setting, interleaved rounds, medians):
 
     python scripts/ab_flag.py training.SPLIT_COLSUM [n_experts]
+    python scripts/ab_flag.py blk.routed_stream_train [n_experts]   # block attribute
 """
 import importlib, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,16 +10,19 @@ import torch
 import paper_2404_05019_b200 as P
 from paper_2404_05019_b200.runtime import CapturedStep
 modname, flag = sys.argv[1].rsplit(".", 1)
-mod = importlib.import_module("paper_2404_05019_b200." + modname)
+mod = None if modname == "blk" else importlib.import_module("paper_2404_05019_b200." + modname)
 n_exp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 T, d, h = 18432, 384, 1536
 x = torch.randn(T, d, device="cuda").bfloat16()
 graphs = {}
 for val in (False, True):
-    setattr(mod, flag, val)
+    if mod is not None:
+        setattr(mod, flag, val)
     blk = P.ScMoEBlockPair(d, h, n_exp, variant="scmoe", shortcut_pos="pos2", n_heads=12, seq_len=144,
                            capacity_factor=1.25, dtype=torch.bfloat16,
                            generator=torch.Generator(device="cuda").manual_seed(1)).requires_grad_(True)
+    if mod is None:
+        setattr(blk, flag, val)
     graphs[val] = CapturedStep(lambda xx, b=blk: b.train_step(xx, lr=1e-4), [x], warmup=3)
 res = {k: [] for k in graphs}
 for r in range(6):
