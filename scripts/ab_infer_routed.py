@@ -1,4 +1,4 @@
-import os, statistics, sys
+import os, random, statistics, sys
 sys.path.insert(0, os.getcwd())
 import torch
 import paper_2404_05019_b200 as P
@@ -21,8 +21,11 @@ with torch.no_grad():
     for k in (True, "decode"):
         print(k, "identical:", torch.equal(ref, graphs[k].replay().clone()))
     res = {k: [] for k in graphs}
-    for r in range(8):
-        for val, g in graphs.items():
+    rng = random.Random(0)
+    for r in range(12):
+        items = list(graphs.items())
+        rng.shuffle(items)                 # power-cap drift hits every arm alike
+        for val, g in items:
             for _ in range(2): g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
