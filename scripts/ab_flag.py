@@ -2,7 +2,7 @@
 graph per setting, interleaved rounds, medians):
 
     python scripts/ab_flag.py training.SPLIT_COLSUM [n_experts]
-    python scripts/ab_flag.py blk.routed_stream_train [n_experts]   # block attribute
+    python scripts/ab_flag.py blk.routed_stream_train [n_experts] [False,gate]   # block attribute
 """
 import importlib, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,7 +15,9 @@ n_exp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 T, d, h = 18432, 384, 1536
 x = torch.randn(T, d, device="cuda").bfloat16()
 graphs = {}
-for val in (False, True):
+vals = (False, True) if len(sys.argv) <= 3 else tuple(
+    {"True": True, "False": False}.get(v, v) for v in sys.argv[3].split(","))
+for val in vals:
     if mod is not None:
         setattr(mod, flag, val)
     blk = P.ScMoEBlockPair(d, h, n_exp, variant="scmoe", shortcut_pos="pos2", n_heads=12, seq_len=144,
