@@ -518,6 +518,9 @@ def gate_aux_loss(counts: torch.Tensor, prob_sum: torch.Tensor, n_tokens: int, k
     """Balance loss N * sum_e f_e P_e from the gate kernel's counts and
     probability sums, one launch (arch.py:436-439)."""
     ensure_device(counts)
+    if counts.dtype != torch.int32 or prob_sum.dtype != torch.float32 or \
+            prob_sum.numel() != counts.numel():
+        raise ValueError("aux loss needs int32 counts and fp32 prob_sum of one length")
     aux = torch.empty((), device=counts.device, dtype=torch.float32)
     check(lib().scmoe_gate_aux_loss(ptr(_c(counts, "counts")), ptr(_c(prob_sum, "prob_sum")),
                                     n_tokens, counts.shape[0], k, ptr(aux), stream_ptr(stream)))
