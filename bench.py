@@ -455,7 +455,10 @@ def hbm_kernel_times(moe, x, reps: int = 10):
                 g.replay()
             torch.cuda.synchronize()
         dev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
-        own = [e for e in dev if "reduce_kernel" not in e.name]   # drop the flush's sum
+        # drop the flush's sum and the memset torch's reduction issues for its
+        # semaphores (none of the measured ops issues a memset: the gate keeps
+        # its counter in per-gate sync words)
+        own = [e for e in dev if "reduce_kernel" not in e.name and "Memset" not in e.name]
         us = sum(getattr(e, "device_time_total", 0.0) or e.cuda_time_total for e in own) / reps
         res_d[name] = {"us": us, "bytes": nbytes, "gbps": nbytes / us / 1e3,
                        "kernels": sorted({e.name.split("(")[0][-60:] for e in own})}
@@ -498,7 +501,8 @@ def hbm_kernel_times(moe, x, reps: int = 10):
             g.replay()
             torch.cuda.synchronize()
         dev = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
-                      and "reduce_kernel" not in e.name], key=lambda e: e.time_range.start)
+                      and "reduce_kernel" not in e.name and "Memset" not in e.name],
+                     key=lambda e: e.time_range.start)
         per_op = len(dev) // R
         tail = dev[per_op:]                       # ops 2..R: each pays its predecessor's drain
         us = sum(getattr(e, "device_time_total", 0.0) or e.cuda_time_total for e in tail) / (R - 1)
