@@ -840,10 +840,24 @@ __global__ void __launch_bounds__(GT_THREADS, 1) gate_topk_tc_kernel(
       float ps = 0.f;
       if (e < N) {
         const int lim = last ? (int)gridDim.x : (int)blockIdx.x;
-#pragma unroll 4
-        for (int c2 = p; c2 < lim; c2 += P) {
-          if (c2 < (int)blockIdx.x) acc += __ldcg(cta_cnt + (size_t)c2 * N + e);
-          if (last) ps += __ldcg(cta_psum + (size_t)c2 * N + e);
+        // every row of a batch loaded before any is added: one round trip per
+        // 16 rows (148 CTAs: one batch at N <= 8, two at N <= 16) instead of
+        // one per 4; the additions keep the rows' order (deterministic)
+        constexpr int BATCH = 16;
+        for (int c0 = p; c0 < lim; c0 += BATCH * P) {
+          uint32_t v[BATCH];
+          float f[BATCH];
+#pragma unroll
+          for (int i = 0; i < BATCH; ++i) {
+            const int c2 = c0 + i * P;
+            v[i] = (c2 < lim && c2 < (int)blockIdx.x) ? __ldcg(cta_cnt + (size_t)c2 * N + e) : 0u;
+            f[i] = (last && c2 < lim) ? __ldcg(cta_psum + (size_t)c2 * N + e) : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < BATCH; ++i) {
+            acc += v[i];
+            if (last && c0 + i * P < lim) ps += f[i];
+          }
         }
       }
       s_red[p][e] = acc;
