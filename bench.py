@@ -1220,7 +1220,8 @@ def run_ours(args):
                     frac=v["gbps"] / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                     sustained_frac=v["sustained_gbps"] / peaks["hbm_gbs"]
                     if peaks.get("hbm_gbs") else None) for k, v in hbm_ops.items()},
-        "hbm_kernels_note": "us / frac: CUPTI durations of one op's kernels after a 512 MB read "
+        "hbm_kernels_note": "us / frac: CUPTI durations of one op's kernels (no memsets: none of "
+                            "the ops issues one) after a 512 MB read "
                             "flush of L2 (the op's writes can still be draining from L2 when its "
                             "kernel ends, so frac may exceed 1 against the measured copy peak); "
                             "sustained_*: 6 back-to-back ops on rotating input and output "
