@@ -391,3 +391,28 @@ def test_compat_drives_the_real_reference_model(variant, pos, mode, freq):
     assert arch.moe_shared.__module__.startswith("scmoelab")
     ref_out, _ = arch.forward(cfg, params, tokens, replay=arch.replay_from_trace(gpu_trace))
     _check(gpu_out, ref_out, 1e-4, "reference arch.forward through compat")
+
+
+@pytest.mark.parametrize("pos", ["pos1", "pos2", "pos3"])
+def test_routed_side_stream_bit_identical(pos):
+    """Inference with the routed ops on the side stream (routed_stream_infer,
+    the default) equals the serial issue order bit for bit, eager and inside a
+    CUDA graph, with the fused shared-expert combine."""
+    from paper_2404_05019_b200.runtime import CapturedStep
+    T, d, h, N = 2048, 256, 512, 8
+    blk = P.ScMoEBlockPair(d, h, N, variant="scmoe", shortcut_pos=pos, n_heads=4, seq_len=256,
+                           causal=True, capacity_factor=1.25, dtype=torch.bfloat16,
+                           generator=torch.Generator(device="cuda").manual_seed(31))
+    x = torch.randn(T, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(32))
+    x = x.bfloat16()
+    with torch.no_grad():
+        blk.routed_stream_infer = False
+        ref, dref, _ = blk(x)
+        ref = ref.clone()
+        blk.routed_stream_infer = True
+        out, dec, _ = blk(x)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        assert torch.equal(dec.slots, dref.slots) and torch.equal(dec.indices, dref.indices)
+        g = CapturedStep(lambda xx: blk(xx)[0], [x])
+        assert torch.equal(g.replay().clone(), ref)
