@@ -325,6 +325,13 @@ int scmoe_shared_ffn_combine(const void* x, int dtype, const void* w1t, const fl
                              const int32_t* slots, const float* weights, int capacity, int k,
                              void* hidden, void* out, int n_tokens, int d_model, int d_hidden,
                              void* stream);
+/* Its second half alone: out = the fused-combine GEMM2 over an already
+ * computed hidden = gelu(x_cur W1 + b1) (a caller that runs GEMM1 while the
+ * routed rows are still being produced on another stream). */
+int scmoe_ffn2_combine(const void* hidden, int dtype, const void* w2t, const float* b2,
+                       const void* residual, const void* expert_out, const int32_t* indices,
+                       const int32_t* slots, const float* weights, int capacity, int k, void* out,
+                       int n_tokens, int d_model, int d_hidden, void* stream);
 
 /*
  * K5 — combine ("decode") + combination gate + optional residual:

@@ -80,6 +80,8 @@ SIGNATURES = [
                                   _i, _i, _i, _vp, _vp]),
     ("scmoe_shared_ffn_combine", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                       _i, _i, _vp, _vp, _i, _i, _i, _vp]),
+    ("scmoe_ffn2_combine", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _i, _i,
+                                _i, _vp]),
     ("scmoe_pack_heads", _i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     ("scmoe_expert_ffn_to_peers", _i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp,
                                        _i, _i, _i, _vp]),

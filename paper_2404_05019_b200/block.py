@@ -49,6 +49,9 @@ def layer_norm(x: torch.Tensor) -> torch.Tensor:
     return F.layer_norm(x.float(), (x.shape[-1],), eps=1e-6).to(x.dtype)
 
 
+# inference with the routed side stream: the shared expert's GEMM1 runs before
+# the join, only its GEMM2 (with the fused combine) waits for the routed rows
+SHARED_SPLIT_JOIN = True
 PACKED_ATTENTION = True     # training attention through flash-attn's packed-QKV kernels
 ATTN_TRAIN = "cudnn_packed"  # "cudnn_packed" | "flash_packed" | "autograd"
 # windows of <= 192 rows (configs[1]: 144) run our own attention kernels on
@@ -624,16 +627,26 @@ class ScMoEBlockPair(nn.Module):
 
         def shared():
             dec = env.get("dec")
+            join = env.pop("join", None)     # routed side stream still running
             if ("y" in env and not train and not use_ep and chunks == 1 and off is None
                     and not env.get("no_fuse")
                     and self.variant in ("scmoe", "shared")
                     and moe.shared.can_fuse_combine(env["x_cur"], dec, moe.combine_mode)):
                 # the routed rows are ready: the combine (+ the block residual)
                 # runs in the shared expert's GEMM2 epilogue; decode is a no-op
-                env["out"] = moe.shared.forward_combine(env["x_cur"], env["y"], dec,
-                                                        residual=env["h_mh_cur"])
+                if join is not None:
+                    # GEMM1 beside the routed expert; only GEMM2 waits for its rows
+                    hid = moe.shared.hidden(env["x_cur"])
+                    join()
+                    env["out"] = moe.shared.combine_from_hidden(hid, env["y"], dec,
+                                                                residual=env["h_mh_cur"])
+                else:
+                    env["out"] = moe.shared.forward_combine(env["x_cur"], env["y"], dec,
+                                                            residual=env["h_mh_cur"])
                 env["fused"] = True
                 return
+            if join is not None:
+                join()
             # training: the block residual's gradient (combine) is added in the
             # shared expert's data-gradient GEMM when x_cur is the residual
             xc = env["x_cur"]
@@ -711,16 +724,22 @@ class ScMoEBlockPair(nn.Module):
                         ops[name]()
                     continue
                 if name in join_at and forked:
-                    st.wait_stream(side)          # the fused combine reads the routed rows
                     forked = False
-                    for key in ("y", "buf", "w", "aux", "kept"):
-                        t = env.get(key)
-                        if isinstance(t, torch.Tensor):
+
+                    def _join():
+                        st.wait_stream(side)      # the combine reads the routed rows
+                        for key in ("y", "buf", "w", "aux", "kept"):
+                            t = env.get(key)
+                            if isinstance(t, torch.Tensor):
+                                t.record_stream(st)
+                        dec = env["dec"]
+                        for t in (dec.logits, dec.indices, dec.weights, dec.dropped, dec.slots,
+                                  dec.counts, dec.prob_sum):
                             t.record_stream(st)
-                    dec = env["dec"]
-                    for t in (dec.logits, dec.indices, dec.weights, dec.dropped, dec.slots,
-                              dec.counts, dec.prob_sum):
-                        t.record_stream(st)
+                    if name == "shared" and SHARED_SPLIT_JOIN:
+                        env["join"] = _join       # shared() joins between its two GEMMs
+                    else:
+                        _join()
                 with rec.op(name, "compute", st):
                     ops[name]()
             order = []

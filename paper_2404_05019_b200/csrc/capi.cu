@@ -510,6 +510,18 @@ extern "C" int scmoe_shared_ffn_combine(const void* x, int dtype, const void* w1
   int rc = scmoe_grouped_gemm(x, dtype, w1t, b1, nullptr, hidden, 1, 1, n_tokens, nullptr,
                               n_tokens, d_hidden, d_model, SCMOE_EPI_BIAS_GELU, stream);
   if (rc) return rc;
+  return scmoe_ffn2_combine(hidden, dtype, w2t, b2, residual, expert_out, indices, slots, weights,
+                            capacity, k, out, n_tokens, d_model, d_hidden, stream);
+}
+
+extern "C" int scmoe_ffn2_combine(const void* hidden, int dtype, const void* w2t, const float* b2,
+                                  const void* residual, const void* expert_out,
+                                  const int32_t* indices, const int32_t* slots,
+                                  const float* weights, int capacity, int k, void* out,
+                                  int n_tokens, int d_model, int d_hidden, void* stream) {
+  using namespace scmoe;
+  SCMOE_CHECK_ARG(dtype == SCMOE_BF16, "the fused combine runs on bf16");
+  SCMOE_CHECK_ARG(k >= 1 && k <= 2 && capacity >= 1, "fused combine: k <= 2");
   const CombineSpec cs{expert_out, indices, slots, weights, capacity, k};
   return grouped_gemm_bf16(hidden, w2t, 0, b2, residual, nullptr, nullptr, out, 1, 1, n_tokens,
                            nullptr, n_tokens, d_model, d_hidden, SCMOE_EPI_BIAS, 0,

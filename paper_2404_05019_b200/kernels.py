@@ -607,6 +607,27 @@ def pack_heads(srcs, out: Optional[torch.Tensor] = None, stream=None) -> torch.T
     return out
 
 
+def ffn2_combine(hidden: torch.Tensor, w2t: torch.Tensor, b2: torch.Tensor,
+                 expert_out: torch.Tensor, indices: torch.Tensor, slots: torch.Tensor,
+                 weights: torch.Tensor, capacity: int, residual: Optional[torch.Tensor] = None,
+                 out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """The second half of shared_ffn_combine over a precomputed hidden =
+    gelu(x W1 + b1): GEMM2 with the direct-add combine in its epilogue."""
+    ensure_device(hidden)
+    T, h = hidden.shape
+    d = w2t.shape[-2]
+    if out is None:
+        out = torch.empty(T, d, device=hidden.device, dtype=hidden.dtype)
+    if residual is not None:
+        _c(residual, "residual")
+    check(lib().scmoe_ffn2_combine(
+        ptr(_c(hidden, "hidden")), dtype_code(hidden.dtype), ptr(_c(w2t, "w2t")), ptr(b2),
+        ptr(residual), ptr(_c(expert_out, "expert_out")), ptr(_c(indices, "indices")),
+        ptr(_c(slots, "slots")), ptr(_c(weights, "weights")), capacity, indices.shape[1],
+        ptr(out), T, d, h, stream_ptr(stream)))
+    return out
+
+
 def shared_ffn_combine(x: torch.Tensor, w1t: torch.Tensor, b1: torch.Tensor, w2t: torch.Tensor,
                        b2: torch.Tensor, expert_out: torch.Tensor, indices: torch.Tensor,
                        slots: torch.Tensor, weights: torch.Tensor, capacity: int,

@@ -336,6 +336,17 @@ class SharedExpert(nn.Module):
                                     dec.indices, dec.slots, dec.weights, dec.capacity,
                                     residual=residual, stream=stream)
 
+    def hidden(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Inference: gelu(x W1 + b1), the first GEMM of forward_combine (same
+        kernel and epilogue: bit-identical)."""
+        return K.grouped_gemm(x, self.w1t, self.b1, gelu=True, stream=stream)
+
+    def combine_from_hidden(self, hid: torch.Tensor, expert_out: torch.Tensor, dec,
+                            residual: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """forward_combine's second GEMM with the fused combine, over hidden()."""
+        return K.ffn2_combine(hid, self.w2t, self.b2, expert_out, dec.indices, dec.slots,
+                              dec.weights, dec.capacity, residual=residual, stream=stream)
+
     def can_fuse_combine(self, x: torch.Tensor, dec, combine_mode: str) -> bool:
         return (combine_mode == "direct_add" and x.dtype == torch.bfloat16 and dec.k <= 2
                 and not torch.is_grad_enabled() and FUSED_COMBINE)

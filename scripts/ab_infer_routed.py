@@ -13,16 +13,21 @@ t2 = P.ScMoEBlockPair(d, h, N, variant="standard", k_routed=2, n_heads=32, seq_l
 x = torch.randn(T, d, device="cuda").bfloat16()
 graphs = {}
 with torch.no_grad():
+    import paper_2404_05019_b200.block as B
     for val in (False, True, "decode"):
         blk.routed_stream_infer = val
         graphs[val] = CapturedStep(lambda xx: blk(xx)[0], [x])
+    blk.routed_stream_infer = True
+    B.SHARED_SPLIT_JOIN = False
+    graphs["no-split"] = CapturedStep(lambda xx: blk(xx)[0], [x])
+    B.SHARED_SPLIT_JOIN = True
     graphs["top2"] = CapturedStep(lambda xx: t2(xx)[0], [x])
     ref = graphs[False].replay().clone()
-    for k in (True, "decode"):
+    for k in (True, "decode", "no-split"):
         print(k, "identical:", torch.equal(ref, graphs[k].replay().clone()))
     res = {k: [] for k in graphs}
     rng = random.Random(0)
-    for r in range(12):
+    for r in range(int(os.environ.get("ROUNDS", "12"))):
         items = list(graphs.items())
         rng.shuffle(items)                 # power-cap drift hits every arm alike
         for val, g in items:
