@@ -307,3 +307,21 @@ def test_gate_presplit_equals_per_call_split():
     torch.cuda.synchronize()
     assert torch.equal(d2.indices, ref.indices) and torch.equal(d2.slots, ref.slots)
     assert not torch.equal(d1.indices, d2.indices)
+
+
+@pytest.mark.parametrize("T,d,N,k", [(65536, 2048, 16, 2), (3000, 4096, 12, 1)])
+def test_gate_tensor_core_sync_words_wide(T, d, N, k):
+    """The streamed-blob tensor-core gate (N > 8) with caller-kept sync words,
+    called repeatedly: the same decisions as the per-call-memset path, the
+    words left zero."""
+    g = torch.Generator(device="cuda").manual_seed(T + N)
+    x = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, d, device="cuda", generator=g) / d ** 0.5
+    quota = K.expert_quota(1.0, T, k, N)
+    ref = K.gate_topk(x, w, k, quota)
+    sync = torch.zeros(2, device="cuda", dtype=torch.int32)
+    for _ in range(3):
+        out = K.gate_topk(x, w, k, quota, sync=sync)
+        assert torch.equal(out.slots, ref.slots) and torch.equal(out.indices, ref.indices)
+        assert torch.equal(out.dropped, ref.dropped) and torch.equal(out.counts, ref.counts)
+        assert int(sync.abs().sum()) == 0

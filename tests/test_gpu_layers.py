@@ -416,3 +416,21 @@ def test_routed_side_stream_bit_identical(pos):
         assert torch.equal(dec.slots, dref.slots) and torch.equal(dec.indices, dref.indices)
         g = CapturedStep(lambda xx: blk(xx)[0], [x])
         assert torch.equal(g.replay().clone(), ref)
+
+
+def test_every_block_routed_side_stream_bit_identical():
+    """The every-block placement (ScMoEBlock, pos1) with the routed ops on the
+    side stream equals the serial order bit for bit."""
+    T, d, h, N = 1024, 256, 512, 16
+    blk = P.ScMoEBlock(d, h, N, variant="scmoe", shortcut_pos="pos1", n_heads=4, seq_len=256,
+                       causal=True, capacity_factor=2.0, dtype=torch.bfloat16,
+                       generator=torch.Generator(device="cuda").manual_seed(41))
+    x = torch.randn(T, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(42))
+    x = x.bfloat16()
+    with torch.no_grad():
+        blk.routed_stream_infer = False
+        ref = blk(x)[0].clone()
+        blk.routed_stream_infer = True
+        out = blk(x)[0]
+        torch.cuda.synchronize()
+    assert torch.equal(out, ref)
