@@ -93,10 +93,18 @@ gelu_fwd_kernel(const uint4* __restrict__ z, uint4* __restrict__ h, uint4* __res
   for (; i + 3 * stride < n; i += 4 * stride) {
     uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(z + base + i + u * stride);
+    for (int u = 0; u < 4; ++u)      // z is dead after this pass: evict-first (GRAD)
+      v[u] = GRAD ? __ldcs(z + base + i + u * stride) : ld_nc_v4(z + base + i + u * stride);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (GRAD) gelu_vec2(v[u], h[base + i + u * stride], dg[base + i + u * stride]);
+      if (GRAD) {
+        // gelu'(z) is read only by the backward: a streaming (evict-first)
+        // store keeps h — read by the next GEMM right away — in L2
+        uint4 hv, dv;
+        gelu_vec2(v[u], hv, dv);
+        h[base + i + u * stride] = hv;
+        __stcs(dg + base + i + u * stride, dv);
+      }
       else h[base + i + u * stride] = gelu_vec(v[u]);
     }
   }
@@ -105,7 +113,7 @@ gelu_fwd_kernel(const uint4* __restrict__ z, uint4* __restrict__ h, uint4* __res
       uint4 a = make_uint4(0, 0, 0, 0), b = a;
       if (i < n) gelu_vec2(ld_nc_v4(z + base + i), a, b);
       h[base + i] = a;
-      dg[base + i] = b;
+      __stcs(dg + base + i, b);
     } else {
       h[base + i] = i < n ? gelu_vec(ld_nc_v4(z + base + i)) : make_uint4(0, 0, 0, 0);
     }
