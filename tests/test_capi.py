@@ -58,3 +58,41 @@ def test_sass_contains_tcgen05_and_tma():
     assert "UTCHMMA" in sass   # tcgen05.mma
     assert "UTMALDG" in sass   # TMA tensor load
     assert "LDTM" in sass      # tcgen05.ld
+
+
+def test_host_queries_of_the_round_two_entries():
+    """Workspace queries and argument checks of the entries added in round 2
+    (two-matrix column sums, mean, aux loss, fill, the gate with sync words,
+    the split fused combine) answer on the host."""
+    so = _lib.load_library()
+    one = so.scmoe_grouped_colsum_workspace_bytes(1, 18432, 384)
+    two = so.scmoe_grouped_colsum2_workspace_bytes(1, 18432, 384, 1536)
+    assert one > 0 and two > one
+    assert so.scmoe_grouped_colsum2_workspace_bytes(1, 18432, 384, 0) == 0
+    assert so.scmoe_mean_workspace_bytes() >= 4
+    assert so.scmoe_gate_aux_loss(None, None, 0, 8, 1, None, None) == _lib.SCMOE_ERR_ARG
+    assert so.scmoe_fill_div(None, 9, 8, None, 1.0, None) == _lib.SCMOE_ERR_ARG
+    assert so.scmoe_mean(None, 1, 0, None, None, 0, None) == _lib.SCMOE_ERR_ARG
+    rc = so.scmoe_gate_topk_ex(None, 1, 8, None, None, None, None, None, 0, 8, 4, 1, 1, None,
+                               None, None, None, None, None, None, None, 0, None, None)
+    assert rc == _lib.SCMOE_ERR_ARG and b"n_tokens" in so.scmoe_last_error()
+    rc = so.scmoe_ffn2_combine(None, 0, None, None, None, None, None, None, None, 1, 1, None,
+                               8, 8, 8, None)
+    assert rc == _lib.SCMOE_ERR_ARG       # fp32: the fused combine runs on bf16
+
+
+def test_gemm_sm_budget_nesting():
+    """Nested SM budgets take the smaller and restore the outer on exit
+    (the concurrent backward nests a side budget in the main one)."""
+    from paper_2404_05019_b200 import kernels as K
+    assert K._SM_BUDGET[0] == 0
+    with K.gemm_sm_budget(74):
+        assert K._SM_BUDGET[0] == 74
+        with K.gemm_sm_budget(96):
+            assert K._SM_BUDGET[0] == 74
+        with K.gemm_sm_budget(16):
+            assert K._SM_BUDGET[0] == 16
+        assert K._SM_BUDGET[0] == 74
+        with K.gemm_sm_budget(0):
+            assert K._SM_BUDGET[0] == 74
+    assert K._SM_BUDGET[0] == 0
