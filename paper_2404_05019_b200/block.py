@@ -237,10 +237,13 @@ class ScMoEBlockPair(nn.Module):
         # beside the window ops — the shortcut makes them independent until
         # the shared expert's fused combine, so at N = 1 the two streams'
         # persistent GEMMs fill each other's wave tails (no exchange to hide).
-        # Inference: on; True joins at the shared expert (fused combine),
-        # "decode" at the combine (unfused) — measured slower.  Training:
-        # routed_stream_train (experiment)
-        self.routed_stream_infer = True
+        # Inference: on.  "decode" (default) joins at the combine: the shared
+        # expert runs whole beside the routed path and the combine kernel
+        # follows (shuffled graph A/B: faster than the fused shared-expert
+        # combine in 4 of 5 runs, by 0.4-1.6%); True joins inside the shared
+        # expert (GEMM1 before, GEMM2 with the fused combine after).
+        # Training: routed_stream_train (experiment, slower)
+        self.routed_stream_infer = "decode"
         self.routed_stream_train = False
         self._xchg = None
         if variant not in VARIANTS:

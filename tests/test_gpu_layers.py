@@ -409,13 +409,14 @@ def test_routed_side_stream_bit_identical(pos):
         blk.routed_stream_infer = False
         ref, dref, _ = blk(x)
         ref = ref.clone()
-        blk.routed_stream_infer = True
-        out, dec, _ = blk(x)
-        torch.cuda.synchronize()
-        assert torch.equal(out, ref)
-        assert torch.equal(dec.slots, dref.slots) and torch.equal(dec.indices, dref.indices)
-        g = CapturedStep(lambda xx: blk(xx)[0], [x])
-        assert torch.equal(g.replay().clone(), ref)
+        for mode in (True, "decode"):        # join in the shared expert / at the combine
+            blk.routed_stream_infer = mode
+            out, dec, _ = blk(x)
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), mode
+            assert torch.equal(dec.slots, dref.slots) and torch.equal(dec.indices, dref.indices)
+            g = CapturedStep(lambda xx: blk(xx)[0], [x])
+            assert torch.equal(g.replay().clone(), ref), mode
 
 
 def test_every_block_routed_side_stream_bit_identical():
@@ -430,7 +431,7 @@ def test_every_block_routed_side_stream_bit_identical():
     with torch.no_grad():
         blk.routed_stream_infer = False
         ref = blk(x)[0].clone()
-        blk.routed_stream_infer = True
+        blk.routed_stream_infer = "decode"
         out = blk(x)[0]
         torch.cuda.synchronize()
     assert torch.equal(out, ref)
